@@ -1,0 +1,180 @@
+/*
+ * ldurepart_b200 — C ABI of the B200-native repartition / update / solve path.
+ *
+ * Drop-in boundary for the reference package `ldurepart`
+ * (/root/reference/pkg/src/ldurepart/).  Every entry point names the reference
+ * interface it replaces (file:line).  Plain pointers and sizes only: device
+ * pointers are `void*`/typed pointers into memory owned by the caller (PyTorch
+ * in this repo), host pointers are ordinary (pinned or pageable) memory.
+ *
+ * Status codes: 0 = ok; LRB_EVALUE maps to Python ValueError, LRB_ERUNTIME to
+ * RuntimeError, LRB_ECUDA to a CUDA failure, LRB_ENOTPD to
+ * ValueError("cg: matrix is not positive definite") (solver.py:129-130),
+ * LRB_ETIMEOUT to a cross-device barrier timeout.  The thread-local message of
+ * the last failure is returned by lrb_last_error().
+ *
+ * There is no CPU fallback: every compute entry point launches sm_100a code.
+ */
+#ifndef LDUREPART_B200_H
+#define LDUREPART_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRB_OK 0
+#define LRB_EVALUE (-1)
+#define LRB_ERUNTIME (-2)
+#define LRB_ECUDA (-3)
+#define LRB_ENOTPD (-4)
+#define LRB_ETIMEOUT (-5)
+
+#define LRB_METHOD_CG 0        /* solver.py:100-147 (unpreconditioned CG) */
+#define LRB_METHOD_PCG 1       /* Jacobi-PCG */
+#define LRB_METHOD_BICGSTAB 2  /* BiCGStab */
+
+const char* lrb_last_error(void);
+const char* lrb_version(void);
+int lrb_device_count(void);
+/* Number of kernels this library has launched since load (bench gpu_launches). */
+uint64_t lrb_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * Create path (host, integer; bit-exact with the reference).
+ * ------------------------------------------------------------------------ */
+typedef struct lrb_plan lrb_plan;
+
+/* Fused owner plan from the LDU addressing of its alpha sources.
+ * Replaces, for one owner k, extract_sparsity (repart.py:143-174),
+ * fuse_patterns (repart.py:197-236), pack_order_pairs (repart.py:253-270),
+ * build_scatter_map (repart.py:273-304) and _build_matrix (repart.py:307-318).
+ *   total_cells        pm.total_cells
+ *   row_lo, row_hi     I_GPU(k) (core.py:198-202)
+ *   n_src              alpha; src_rows[n_src+1] = global row offsets of the sources
+ *   face_off[n_src+1], lower[], upper[]   concatenated source-local face addresses
+ *   ifc_off[n_src+1], ifc_row[] (source-local), ifc_col[] (global)
+ *                      interface entries in pack order (blocks by neighbour rank)
+ *   n_gpu, gpu_offsets[n_gpu+1]  GPU row ranges, to resolve halo owners
+ *   n_threads          host worker threads (<= 0: hardware concurrency)          */
+int lrb_plan_build_ldu(int64_t total_cells, int64_t row_lo, int64_t row_hi, int32_t n_src,
+                       const int64_t* src_rows, const int64_t* face_off,
+                       const int64_t* lower, const int64_t* upper, const int64_t* ifc_off,
+                       const int64_t* ifc_row, const int64_t* ifc_col, int32_t n_gpu,
+                       const int64_t* gpu_offsets, int32_t n_threads, lrb_plan** out);
+
+/* Same plan from explicit buffer provenance: buffer entry b carries global
+ * (buf_row[b], buf_col[b]); seg_off[n_seg+1] splits the buffer by source.
+ * Serves the low-level fuse_patterns / build_scatter_map API (repart.py:197-304). */
+int lrb_plan_build_coo(int64_t total_cells, int64_t row_lo, int64_t row_hi, int64_t n_buf,
+                       const int64_t* buf_row, const int64_t* buf_col, int32_t n_seg,
+                       const int64_t* seg_off, int32_t n_gpu, const int64_t* gpu_offsets,
+                       lrb_plan** out);
+
+/* info[0..9] = n_rows, nnz_local, nnz_nonlocal, n_halo, n_buf, n_slices,
+ *              sell_entries, max_row_len, n_seg, part_device_bytes */
+int lrb_plan_info(const lrb_plan* plan, int64_t* info);
+/* Reference DistributedCooMatrix patterns in CSR form (core.py:247-288):
+ * loc_ptr/nl_ptr [n+1]; loc_col part-local; nl_col = index into halo_cols. */
+int lrb_plan_export_csr(const lrb_plan* plan, int64_t* loc_ptr, int64_t* loc_col,
+                        int64_t* nl_ptr, int64_t* nl_col, int64_t* halo_cols);
+/* Reference ScatterMap (repart.py:82-106): to_local[b], index[b] per buffer entry. */
+int lrb_plan_export_scatter(const lrb_plan* plan, uint8_t* to_local, int64_t* index);
+/* Halo owners: hpart[s] (GPU rank) and hidx[s] (row in that part) per halo slot. */
+int lrb_plan_export_halo(const lrb_plan* plan, int32_t* hpart, int32_t* hidx);
+/* The device layout (SELL-32) as built on the host: slice_ptr[n_slices+1],
+ * col/src[sell_entries] (col >= n: halo slot col-n; -1: padding), dpos[n]. */
+int lrb_plan_export_sell(const lrb_plan* plan, int64_t* slice_ptr, int32_t* col, int32_t* src,
+                         int8_t* dpos);
+void lrb_plan_destroy(lrb_plan* plan);
+
+/* ------------------------------------------------------------------------
+ * Device part (one fused owner part on one GPU).
+ * ------------------------------------------------------------------------ */
+typedef struct lrb_part lrb_part;
+
+/* Lay the part out in a caller-owned device arena of plan_info()[9] bytes
+ * (256-byte aligned) and upload the SELL matrix, scatter inverse and halo
+ * tables.  host_stage (pinned, n_buf doubles, nullable) serves pageable and
+ * staged updates.  Replaces ctx.alloc_device (repart.py:347). */
+int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64_t dev_bytes,
+                    double* host_stage, int64_t host_stage_len, lrb_part** out);
+void lrb_part_destroy(lrb_part* part);
+/* Device pointers of the receive buffer and vectors (for tests / bench). */
+int lrb_part_pointers(const lrb_part* part, void** ptrs /* [16] */);
+
+/* Direct update of one source segment (update.py:72-83, transport.py:115-123):
+ * n_pieces host arrays are copied back to back into segment `seg` of the
+ * owner's receive buffer (diag | upper | lower | interface blocks: no host
+ * pack), pinned pieces straight to the device, pageable pieces via the pinned
+ * stage; then that segment's scatter kernel runs on the segment's stream.
+ * Returns once the host pieces may be reused (H2D complete). */
+int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces,
+                       const double* const* pieces, const int64_t* piece_len);
+/* Staged update (update.py:85-102): the owner copies all sources' pieces
+ * into the pinned stage, then one H2D of the whole buffer and the scatter. */
+int lrb_update_staged(lrb_part* part, int32_t n_pieces, const double* const* pieces,
+                      const int64_t* piece_len);
+/* Staged update, source side: copy one source's pieces into the owner's
+ * pinned host stage at segment `seg` (the owner-side host gather,
+ * update.py:85-100); the owner then calls lrb_update_staged with the stage. */
+int lrb_stage_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                      const int64_t* piece_len);
+/* apply_scatter (update.py:105-112) of the whole device-resident buffer. */
+int lrb_apply_scatter(lrb_part* part);
+/* Write host values into the receive buffer (DeviceBuffer.fill, transport.py:115-123). */
+int lrb_part_fill(lrb_part* part, int64_t offset, const double* values, int64_t n);
+/* Read back the receive buffer (DeviceBuffer.values, transport.py:125-127). */
+int lrb_part_read_buffer(lrb_part* part, double* out);
+/* Read the fused values in the reference's row-major local / non-local order
+ * (DistributedCooMatrix.local.vals / non_local.vals). */
+int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_vals);
+/* Make the part's solve stream wait for all pending segment scatters. */
+int lrb_part_join(lrb_part* part);
+int lrb_part_sync(lrb_part* part);
+/* Device time (ms) between the last two lrb_part_mark() calls on the solve stream. */
+int lrb_part_mark(lrb_part* part);
+int lrb_part_elapsed_ms(lrb_part* part, float* ms);
+
+/* ------------------------------------------------------------------------
+ * Team: the owner parts of the active communicator C_a (transport.py:461-472).
+ * Parts are in GPU-rank order.  Parts on the same device run in one
+ * persistent kernel; parts on different devices of this process exchange halo
+ * values and partial dot products through NVLink peer memory.
+ * ------------------------------------------------------------------------ */
+typedef struct lrb_team lrb_team;
+
+int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out);
+/* As lrb_team_create with an explicit device rank per part: parts on one CUDA
+ * device but with different ranks run as separate kernels that synchronise
+ * through the cross-device (peer-memory flag) protocol — exercised by the
+ * tests on a single GPU. */
+int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* dev_rank_of_part,
+                       lrb_team** out);
+void lrb_team_destroy(lrb_team* team);
+
+/* Distributed SpMV y = A x (solver.py:80-97): x_host/y_host per part. */
+int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host);
+
+typedef struct lrb_report {
+  int32_t iterations;
+  int32_t converged;
+  int32_t breakdown;
+  int32_t status;
+  double residual;
+  double bnorm;
+  double device_ms;   /* solve-kernel device time */
+} lrb_report;
+
+/* Krylov solve (cg_solve, solver.py:100-147; PCG/BiCGStab per SURVEY App. A).
+ * b_host/x_host per part (nullable: b already on device / leave x on device).
+ * hist (nullable) receives the recurrence residual per iteration. */
+int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
+                   double* const* x_host, double tol, int32_t max_iter, lrb_report* rep,
+                   double* hist, int32_t hist_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDUREPART_B200_H */

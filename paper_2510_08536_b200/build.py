@@ -1,0 +1,59 @@
+"""Build the native library in-tree: libldurepart_b200.so (sm_100a only).
+
+    python -m paper_2510_08536_b200.build        # or __graft_entry__.build()
+
+The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libldurepart_b200.so")
+SOURCES = ["plan.cpp", "device.cu"]
+HEADERS = ["lrb_internal.h", "kernels.cuh"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC,-O3,-pthread,-Wall,-Wno-unused-function", "-shared"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA toolkit is required to build ldurepart_b200")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(os.path.dirname(HERE), "include", "ldurepart_b200.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES],
+           "-o", LIB + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("ldurepart_b200 native build failed")
+    log = os.path.join(HERE, "csrc", "ptxas.log")
+    with open(log, "w") as fh:
+        fh.write(res.stderr)
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,907 @@
+// Device part / team management and the C-ABI entry points of the hot path.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a (see build.py).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ldurepart_b200.h"
+#include "kernels.cuh"
+#include "lrb_internal.h"
+
+struct lrb_plan;
+
+namespace lrb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+static std::atomic<uint64_t> g_launches{0};
+const Plan& plan_of(const lrb_plan* p);
+
+#define LRB_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" +   \
+                std::to_string(__LINE__) + ")");                                           \
+      return LRB_ECUDA;                                                                    \
+    }                                                                                      \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+static int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
+
+// Arena layout of one part (all sections 256-byte aligned).
+struct Layout {
+  int64_t slice_ptr, col, src, dpos, hpart, hidx, val, recv, vec, total;
+  static constexpr int kVecs = 12;
+};
+
+static Layout layout_of(const Plan& P) {
+  Layout L{};
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    int64_t at = o;
+    o = align256(o + std::max<int64_t>(bytes, 1));
+    return at;
+  };
+  const int64_t E = P.sell_entries();
+  const int64_t h = int64_t(P.halo_cols.size());
+  L.slice_ptr = take(8 * (P.n_slices + 1));
+  L.col = take(4 * E);
+  L.src = take(4 * E);
+  L.dpos = take(P.n);
+  L.hpart = take(4 * h);
+  L.hidx = take(4 * h);
+  L.val = take(8 * E);
+  L.recv = take(8 * P.n_buf);
+  L.vec = o;
+  o += Layout::kVecs * align256(8 * std::max<int64_t>(P.n, 1));
+  L.total = o;
+  return L;
+}
+
+int64_t part_device_bytes(const Plan& P) { return layout_of(P).total; }
+
+}  // namespace lrb
+
+using namespace lrb;
+
+struct lrb_part {
+  int device = 0;
+  PartDev d{};                      // device pointers (host copy)
+  std::vector<int64_t> seg_off, seg_rows, loc_ptr, nl_ptr, slice_ptr;
+  int64_t nnz_l = 0, nnz_n = 0;
+  cudaStream_t main = nullptr;
+  std::vector<cudaStream_t> seg_stream;
+  std::vector<cudaEvent_t> seg_h2d, seg_done;
+  std::vector<char> seg_pending;
+  cudaEvent_t main_done = nullptr, mark_a = nullptr, mark_b = nullptr;
+  int marks = 0;
+  double* stage = nullptr;          // pinned, n_buf doubles (caller-owned)
+  int64_t stage_len = 0;
+  cudaEvent_t stage_free = nullptr; // last H2D from the whole-buffer stage
+  std::mutex mu;
+};
+
+namespace lrb {
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+static int launch_scatter(lrb_part* P, int64_t r0, int64_t r1, cudaStream_t st) {
+  if (r1 <= r0) return LRB_OK;
+  const int64_t first = r0 & ~int64_t(31);
+  const int64_t threads = r1 - first;
+  const int64_t blocks = (threads + 255) / 256;
+  scatter_rows_kernel<<<unsigned(blocks), 256, 0, st>>>(P->d, r0, r1);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  LRB_CUDA(cudaGetLastError());
+  return LRB_OK;
+}
+
+}  // namespace lrb
+
+extern "C" {
+
+const char* lrb_last_error(void) { return lrb::g_err.c_str(); }
+const char* lrb_version(void) { return "ldurepart_b200 0.1.0 (sm_100a)"; }
+uint64_t lrb_launch_count(void) { return lrb::g_launches.load(); }
+
+int lrb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64_t dev_bytes,
+                    double* host_stage, int64_t host_stage_len, lrb_part** out) {
+  if (!plan || !dev_arena || !out) {
+    set_error("lrb_part_create: null argument");
+    return LRB_EVALUE;
+  }
+  const Plan& P = plan_of(plan);
+  const Layout L = layout_of(P);
+  if (dev_bytes < L.total) {
+    set_error("lrb_part_create: device arena too small");
+    return LRB_EVALUE;
+  }
+  if ((reinterpret_cast<uintptr_t>(dev_arena) & 255) != 0) {
+    set_error("lrb_part_create: device arena must be 256-byte aligned");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(device);
+  auto part = std::make_unique<lrb_part>();
+  part->device = device;
+  char* base = static_cast<char*>(dev_arena);
+  PartDev& D = part->d;
+  D.n = P.n;
+  D.n_halo = int64_t(P.halo_cols.size());
+  D.n_buf = P.n_buf;
+  D.n_slices = P.n_slices;
+  D.slice_ptr = reinterpret_cast<const int64_t*>(base + L.slice_ptr);
+  D.col = reinterpret_cast<const int32_t*>(base + L.col);
+  D.src = reinterpret_cast<const int32_t*>(base + L.src);
+  D.dpos = reinterpret_cast<const int8_t*>(base + L.dpos);
+  D.hpart = reinterpret_cast<const int32_t*>(base + L.hpart);
+  D.hidx = reinterpret_cast<const int32_t*>(base + L.hidx);
+  D.val = reinterpret_cast<double*>(base + L.val);
+  D.recv = reinterpret_cast<double*>(base + L.recv);
+  double* vecs[Layout::kVecs];
+  const int64_t vstride = align256(8 * std::max<int64_t>(P.n, 1));
+  for (int i = 0; i < Layout::kVecs; ++i) vecs[i] = reinterpret_cast<double*>(base + L.vec + i * vstride);
+  D.x = vecs[0];
+  D.r = vecs[1];
+  D.p0 = vecs[2];
+  D.p1 = vecs[3];
+  D.q = vecs[4];
+  D.b = vecs[5];
+  D.dinv = vecs[6];
+  D.rhat = vecs[7];
+  D.v0 = vecs[8];
+  D.v1 = vecs[9];
+  D.s = vecs[10];
+  D.t = vecs[11];
+
+  LRB_CUDA(cudaStreamCreateWithFlags(&part->main, cudaStreamNonBlocking));
+  const int n_seg = int(P.seg_off.size()) - 1;
+  part->seg_stream.resize(n_seg);
+  part->seg_h2d.resize(n_seg);
+  part->seg_done.resize(n_seg);
+  part->seg_pending.assign(n_seg, 0);
+  for (int s = 0; s < n_seg; ++s) {
+    LRB_CUDA(cudaStreamCreateWithFlags(&part->seg_stream[s], cudaStreamNonBlocking));
+    LRB_CUDA(cudaEventCreateWithFlags(&part->seg_h2d[s], cudaEventDisableTiming));
+    LRB_CUDA(cudaEventCreateWithFlags(&part->seg_done[s], cudaEventDisableTiming));
+  }
+  LRB_CUDA(cudaEventCreateWithFlags(&part->main_done, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventCreateWithFlags(&part->stage_free, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventCreate(&part->mark_a));
+  LRB_CUDA(cudaEventCreate(&part->mark_b));
+  part->seg_off = P.seg_off;
+  part->seg_rows = P.seg_rows;
+  part->loc_ptr = P.loc_ptr;
+  part->nl_ptr = P.nl_ptr;
+  part->slice_ptr = P.slice_ptr;
+  part->nnz_l = int64_t(P.loc_col.size());
+  part->nnz_n = int64_t(P.nl_col.size());
+  part->stage = host_stage;
+  part->stage_len = host_stage_len;
+
+  // upload the create-once index arrays; values and vectors start at zero
+  cudaStream_t st = part->main;
+  const int64_t E = P.sell_entries();
+  LRB_CUDA(cudaMemsetAsync(dev_arena, 0, L.total, st));
+  LRB_CUDA(cudaMemcpyAsync(base + L.slice_ptr, P.slice_ptr.data(), 8 * (P.n_slices + 1),
+                           cudaMemcpyHostToDevice, st));
+  if (E) {
+    LRB_CUDA(cudaMemcpyAsync(base + L.col, P.sell_col.data(), 4 * E, cudaMemcpyHostToDevice, st));
+    LRB_CUDA(cudaMemcpyAsync(base + L.src, P.sell_src.data(), 4 * E, cudaMemcpyHostToDevice, st));
+  }
+  if (P.n) LRB_CUDA(cudaMemcpyAsync(base + L.dpos, P.dpos.data(), P.n, cudaMemcpyHostToDevice, st));
+  if (D.n_halo) {
+    LRB_CUDA(cudaMemcpyAsync(base + L.hpart, P.hpart.data(), 4 * D.n_halo, cudaMemcpyHostToDevice, st));
+    LRB_CUDA(cudaMemcpyAsync(base + L.hidx, P.hidx.data(), 4 * D.n_halo, cudaMemcpyHostToDevice, st));
+  }
+  LRB_CUDA(cudaStreamSynchronize(st));
+  LRB_CUDA(cudaEventRecord(part->main_done, st));
+  *out = part.release();
+  return LRB_OK;
+}
+
+void lrb_part_destroy(lrb_part* part) {
+  if (!part) return;
+  {
+    DeviceGuard g(part->device);
+    cudaStreamSynchronize(part->main);
+    for (auto s : part->seg_stream) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    for (auto e : part->seg_h2d) cudaEventDestroy(e);
+    for (auto e : part->seg_done) cudaEventDestroy(e);
+    cudaEventDestroy(part->main_done);
+    cudaEventDestroy(part->stage_free);
+    cudaEventDestroy(part->mark_a);
+    cudaEventDestroy(part->mark_b);
+    cudaStreamDestroy(part->main);
+  }
+  delete part;
+}
+
+int lrb_part_pointers(const lrb_part* part, void** ptrs) {
+  if (!part || !ptrs) {
+    set_error("lrb_part_pointers: null argument");
+    return LRB_EVALUE;
+  }
+  const PartDev& D = part->d;
+  void* v[16] = {D.recv, D.val, D.x, D.r, D.p0, D.p1, D.q, D.b, D.dinv, D.rhat, D.v0, D.v1, D.s, D.t,
+                 (void*)D.col, (void*)D.src};
+  std::memcpy(ptrs, v, sizeof(v));
+  return LRB_OK;
+}
+
+static int check_pieces(lrb_part* part, int64_t expect, int32_t n_pieces, const int64_t* piece_len,
+                        const char* who, int seg) {
+  int64_t tot = 0;
+  for (int i = 0; i < n_pieces; ++i) tot += piece_len[i];
+  if (tot != expect) {
+    set_error(std::string("update pattern violation: ") + who + " " + std::to_string(seg) +
+              " delivered " + std::to_string(tot) + " coefficients, pattern expects " +
+              std::to_string(expect));
+    return LRB_EVALUE;
+  }
+  return LRB_OK;
+}
+
+int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                       const int64_t* piece_len) {
+  if (!part || seg < 0 || seg >= int(part->seg_stream.size())) {
+    set_error("lrb_update_segment: bad segment");
+    return LRB_EVALUE;
+  }
+  const int64_t off = part->seg_off[seg], len = part->seg_off[seg + 1] - off;
+  int rc = check_pieces(part, len, n_pieces, piece_len, "segment", seg);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  cudaStream_t st = part->seg_stream[seg];
+  // the scatter below rewrites values the last solve may still read
+  LRB_CUDA(cudaStreamWaitEvent(st, part->main_done, 0));
+  bool all_pinned = true;
+  for (int i = 0; i < n_pieces && all_pinned; ++i)
+    if (piece_len[i]) all_pinned = is_pinned(pieces[i]);
+  double* dst = part->d.recv + off;
+  if (all_pinned) {
+    int64_t o = 0;
+    for (int i = 0; i < n_pieces; ++i) {
+      if (piece_len[i])
+        LRB_CUDA(cudaMemcpyAsync(dst + o, pieces[i], 8 * piece_len[i], cudaMemcpyHostToDevice, st));
+      o += piece_len[i];
+    }
+  } else {
+    if (!part->stage || part->stage_len < part->seg_off.back()) {
+      set_error("lrb_update_segment: pageable input needs a pinned stage");
+      return LRB_EVALUE;
+    }
+    // previous copy out of this stage slice must have landed
+    LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
+    LRB_CUDA(cudaEventSynchronize(part->stage_free));
+    int64_t o = 0;
+    for (int i = 0; i < n_pieces; ++i) {
+      if (piece_len[i]) std::memcpy(part->stage + off + o, pieces[i], 8 * piece_len[i]);
+      o += piece_len[i];
+    }
+    if (len) LRB_CUDA(cudaMemcpyAsync(dst, part->stage + off, 8 * len, cudaMemcpyHostToDevice, st));
+  }
+  LRB_CUDA(cudaEventRecord(part->seg_h2d[seg], st));
+  if (!part->seg_rows.empty()) {
+    rc = launch_scatter(part, part->seg_rows[seg], part->seg_rows[seg + 1], st);
+    if (rc) return rc;
+  }
+  LRB_CUDA(cudaEventRecord(part->seg_done[seg], st));
+  {
+    std::lock_guard<std::mutex> lk(part->mu);
+    part->seg_pending[seg] = 1;
+  }
+  // host pieces are reusable once the copy has landed
+  LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
+  return LRB_OK;
+}
+
+int lrb_part_join(lrb_part* part) {
+  if (!part) {
+    set_error("lrb_part_join: null part");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(part->device);
+  bool any = false;
+  std::lock_guard<std::mutex> lk(part->mu);
+  for (size_t s = 0; s < part->seg_pending.size(); ++s) {
+    if (!part->seg_pending[s]) continue;
+    LRB_CUDA(cudaStreamWaitEvent(part->main, part->seg_done[s], 0));
+    part->seg_pending[s] = 0;
+    any = true;
+  }
+  if (any && part->seg_rows.empty()) {
+    int rc = launch_scatter(part, 0, part->d.n, part->main);
+    if (rc) return rc;
+  }
+  return LRB_OK;
+}
+
+int lrb_update_staged(lrb_part* part, int32_t n_pieces, const double* const* pieces,
+                      const int64_t* piece_len) {
+  if (!part) {
+    set_error("lrb_update_staged: null part");
+    return LRB_EVALUE;
+  }
+  const int64_t total = part->seg_off.back();
+  int rc = check_pieces(part, total, n_pieces, piece_len, "owner", 0);
+  if (rc) return rc;
+  if (!part->stage || part->stage_len < total) {
+    set_error("lrb_update_staged: no pinned stage");
+    return LRB_EVALUE;
+  }
+  rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  LRB_CUDA(cudaEventSynchronize(part->stage_free));
+  for (size_t s = 0; s < part->seg_h2d.size(); ++s) LRB_CUDA(cudaEventSynchronize(part->seg_h2d[s]));
+  int64_t o = 0;
+  for (int i = 0; i < n_pieces; ++i) {
+    if (piece_len[i] && pieces[i] != part->stage + o)
+      std::memcpy(part->stage + o, pieces[i], 8 * piece_len[i]);
+    o += piece_len[i];
+  }
+  if (total)
+    LRB_CUDA(cudaMemcpyAsync(part->d.recv, part->stage, 8 * total, cudaMemcpyHostToDevice, part->main));
+  LRB_CUDA(cudaEventRecord(part->stage_free, part->main));
+  rc = launch_scatter(part, 0, part->d.n, part->main);
+  if (rc) return rc;
+  LRB_CUDA(cudaEventSynchronize(part->stage_free));
+  return LRB_OK;
+}
+
+int lrb_stage_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                      const int64_t* piece_len) {
+  if (!part || seg < 0 || seg >= int(part->seg_stream.size())) {
+    set_error("lrb_stage_segment: bad segment");
+    return LRB_EVALUE;
+  }
+  const int64_t off = part->seg_off[seg], len = part->seg_off[seg + 1] - off;
+  int rc = check_pieces(part, len, n_pieces, piece_len, "segment", seg);
+  if (rc) return rc;
+  if (!part->stage || part->stage_len < part->seg_off.back()) {
+    set_error("lrb_stage_segment: no pinned stage");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(part->device);
+  LRB_CUDA(cudaEventSynchronize(part->stage_free));
+  LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
+  int64_t o = 0;
+  for (int i = 0; i < n_pieces; ++i) {
+    if (piece_len[i]) std::memcpy(part->stage + off + o, pieces[i], 8 * piece_len[i]);
+    o += piece_len[i];
+  }
+  return LRB_OK;
+}
+
+int lrb_apply_scatter(lrb_part* part) {
+  if (!part) {
+    set_error("lrb_apply_scatter: null part");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  return launch_scatter(part, 0, part->d.n, part->main);
+}
+
+int lrb_part_fill(lrb_part* part, int64_t offset, const double* values, int64_t n) {
+  if (!part || offset < 0 || n < 0 || offset + n > part->d.n_buf) {
+    set_error("device buffer fill out of bounds");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  if (n) LRB_CUDA(cudaMemcpyAsync(part->d.recv + offset, values, 8 * n, cudaMemcpyHostToDevice, part->main));
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  return LRB_OK;
+}
+
+int lrb_part_read_buffer(lrb_part* part, double* out) {
+  if (!part || !out) {
+    set_error("lrb_part_read_buffer: null argument");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  if (part->d.n_buf)
+    LRB_CUDA(cudaMemcpyAsync(out, part->d.recv, 8 * part->d.n_buf, cudaMemcpyDeviceToHost, part->main));
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  return LRB_OK;
+}
+
+int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_vals) {
+  if (!part) {
+    set_error("lrb_part_read_values: null part");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  const int64_t E = part->slice_ptr.back();
+  std::vector<double> sell(E);
+  if (E) LRB_CUDA(cudaMemcpyAsync(sell.data(), part->d.val, 8 * E, cudaMemcpyDeviceToHost, part->main));
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  for (int64_t r = 0; r < part->d.n; ++r) {
+    const int64_t base = part->slice_ptr[r / kSlice] + (r % kSlice);
+    int64_t k = 0;
+    for (int64_t j = part->loc_ptr[r]; j < part->loc_ptr[r + 1]; ++j, ++k)
+      if (local_vals) local_vals[j] = sell[base + k * kSlice];
+    for (int64_t j = part->nl_ptr[r]; j < part->nl_ptr[r + 1]; ++j, ++k)
+      if (nonlocal_vals) nonlocal_vals[j] = sell[base + k * kSlice];
+  }
+  return LRB_OK;
+}
+
+int lrb_part_sync(lrb_part* part) {
+  if (!part) {
+    set_error("lrb_part_sync: null part");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  for (auto s : part->seg_stream) LRB_CUDA(cudaStreamSynchronize(s));
+  return LRB_OK;
+}
+
+int lrb_part_mark(lrb_part* part) {
+  if (!part) {
+    set_error("lrb_part_mark: null part");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(part->device);
+  std::swap(part->mark_a, part->mark_b);
+  LRB_CUDA(cudaEventRecord(part->mark_b, part->main));
+  part->marks++;
+  return LRB_OK;
+}
+
+int lrb_part_elapsed_ms(lrb_part* part, float* ms) {
+  if (!part || !ms || part->marks < 2) {
+    set_error("lrb_part_elapsed_ms: need two marks");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(part->device);
+  LRB_CUDA(cudaEventSynchronize(part->mark_b));
+  LRB_CUDA(cudaEventElapsedTime(ms, part->mark_a, part->mark_b));
+  return LRB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Team
+// ---------------------------------------------------------------------------
+namespace lrb {
+
+struct TeamDevice {
+  int device = 0;       // CUDA device
+  int rank = 0;         // device rank in the team
+  std::vector<int> parts;
+  int64_t n_tiles = 0;
+  int grid = 0;
+  cudaStream_t stream = nullptr;  // main stream of the first local part
+  void* ws = nullptr;             // device workspace (cudaMalloc, create time)
+  TeamDev host{};                 // kernel argument
+  PartDev* parts_dev = nullptr;
+  SolveOut* out_dev = nullptr;
+  double* hist_dev = nullptr;
+  int hist_cap = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+}  // namespace lrb
+
+struct lrb_team {
+  std::vector<lrb_part*> parts;
+  std::vector<lrb::TeamDevice> devs;
+  std::vector<int> dev_of_part;
+  std::mutex mu;
+};
+
+namespace lrb {
+
+static int team_hist_capacity(TeamDevice& D, int cap) {
+  if (cap <= D.hist_cap) return LRB_OK;
+  DeviceGuard g(D.device);
+  if (D.hist_dev) cudaFree(D.hist_dev);
+  D.hist_dev = nullptr;
+  LRB_CUDA(cudaMalloc(&D.hist_dev, sizeof(double) * cap));
+  D.hist_cap = cap;
+  return LRB_OK;
+}
+
+template <class K>
+static int max_grid(K kernel, int device, int64_t n_tiles, int n_share) {
+  int sms = 0, per_sm = 0;
+  LRB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTPB, 0));
+  int64_t cap = int64_t(sms) * std::max(per_sm, 1) / std::max(n_share, 1);
+  return int(std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(n_tiles, 1))));
+}
+
+}  // namespace lrb
+
+extern "C" {
+
+// dev_rank_of_part (nullable): explicit device rank per part; parts sharing a
+// CUDA device but given different ranks run as separate kernels (used by the
+// tests to exercise the cross-device protocol on one GPU).
+int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* dev_rank_of_part,
+                       lrb_team** out) {
+  if (n_parts < 1 || !parts || !out) {
+    set_error("lrb_team_create: bad arguments");
+    return LRB_EVALUE;
+  }
+  auto team = std::make_unique<lrb_team>();
+  team->parts.assign(parts, parts + n_parts);
+  // device ranks: by explicit map, else by CUDA device in order of appearance
+  std::vector<int> rank_of(n_parts);
+  std::map<int, int> seen;
+  for (int p = 0; p < n_parts; ++p) {
+    int key = dev_rank_of_part ? dev_rank_of_part[p] : parts[p]->device;
+    auto it = seen.find(key);
+    if (it == seen.end()) it = seen.emplace(key, int(seen.size())).first;
+    rank_of[p] = it->second;
+  }
+  const int n_dev = int(seen.size());
+  team->devs.resize(n_dev);
+  team->dev_of_part = rank_of;
+  for (int p = 0; p < n_parts; ++p) {
+    auto& D = team->devs[rank_of[p]];
+    if (!D.parts.empty() && parts[D.parts.back()]->device != parts[p]->device) {
+      set_error("lrb_team_create: parts of one device rank must share a CUDA device");
+      return LRB_EVALUE;
+    }
+    if (!D.parts.empty() && D.parts.back() != p - 1) {
+      set_error("lrb_team_create: parts of one device must be consecutive GPU ranks");
+      return LRB_EVALUE;
+    }
+    D.parts.push_back(p);
+    D.device = parts[p]->device;
+    D.rank = rank_of[p];
+  }
+  // physical sharing (several device ranks on one CUDA device)
+  std::map<int, int> share;
+  for (auto& D : team->devs) share[D.device]++;
+  // peer access between distinct devices
+  for (auto& A : team->devs)
+    for (auto& B : team->devs)
+      if (A.device != B.device) {
+        DeviceGuard g(A.device);
+        int can = 0;
+        LRB_CUDA(cudaDeviceCanAccessPeer(&can, A.device, B.device));
+        if (!can) {
+          set_error("lrb_team_create: no peer access between devices");
+          return LRB_EVALUE;
+        }
+        cudaError_t e = cudaDeviceEnablePeerAccess(B.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          set_error(std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+          return LRB_ECUDA;
+        }
+        cudaGetLastError();
+      }
+  // per-device workspace
+  std::vector<PartDev> table(n_parts);
+  for (auto& D : team->devs) {
+    int64_t t = 0;
+    for (int p : D.parts) {
+      lrb_part* P = parts[p];
+      P->d.tile0 = t;
+      P->d.ntiles = (P->d.n + kTile - 1) / kTile;
+      t += P->d.ntiles;
+    }
+    D.n_tiles = t;
+  }
+  for (int p = 0; p < n_parts; ++p) table[p] = parts[p]->d;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    D.stream = parts[D.parts.front()]->main;
+    const int64_t n_tiles = std::max<int64_t>(D.n_tiles, 1);
+    size_t bytes = 0;
+    auto take = [&](size_t b) {
+      size_t at = bytes;
+      bytes = (bytes + b + 255) & ~size_t(255);
+      return at;
+    };
+    size_t o_parts = take(sizeof(PartDev) * n_parts);
+    size_t o_tp = take(sizeof(int32_t) * n_tiles);
+    size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
+    size_t o_pred = take(sizeof(double) * kMaxRed * n_parts);
+    size_t o_red = take(sizeof(double) * kMaxRed);
+    size_t o_bar = take(sizeof(unsigned) * 2);
+    size_t o_epoch = take(sizeof(unsigned long long));
+    size_t o_flags = take(sizeof(unsigned long long) * n_dev);
+    size_t o_peer_flags = take(sizeof(void*) * n_dev);
+    size_t o_peer_red = take(sizeof(void*) * n_dev);
+    size_t o_out = take(sizeof(SolveOut));
+    LRB_CUDA(cudaMalloc(&D.ws, bytes));
+    LRB_CUDA(cudaMemset(D.ws, 0, bytes));
+    char* w = static_cast<char*>(D.ws);
+    D.parts_dev = reinterpret_cast<PartDev*>(w + o_parts);
+    D.out_dev = reinterpret_cast<SolveOut*>(w + o_out);
+    TeamDev& H = D.host;
+    H.n_parts = n_parts;
+    H.dev_rank = D.rank;
+    H.n_dev = n_dev;
+    H.part_begin = D.parts.front();
+    H.part_end = D.parts.back() + 1;
+    H.n_tiles = D.n_tiles;
+    H.parts = D.parts_dev;
+    H.tile_part = reinterpret_cast<int32_t*>(w + o_tp);
+    H.partials = reinterpret_cast<double*>(w + o_partials);
+    H.part_red = reinterpret_cast<double*>(w + o_pred);
+    H.red = reinterpret_cast<double*>(w + o_red);
+    H.bar_count = reinterpret_cast<unsigned*>(w + o_bar);
+    H.bar_gen = H.bar_count + 1;
+    H.epoch = reinterpret_cast<unsigned long long*>(w + o_epoch);
+    H.flags = reinterpret_cast<unsigned long long*>(w + o_flags);
+    H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
+    H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
+    H.out = D.out_dev;
+    H.timeout_ns = 20LL * 1000 * 1000 * 1000;
+    std::vector<int32_t> tp(n_tiles, 0);
+    for (int p : D.parts)
+      for (int64_t t = 0; t < parts[p]->d.ntiles; ++t) tp[parts[p]->d.tile0 + t] = p;
+    LRB_CUDA(cudaMemcpy(D.parts_dev, table.data(), sizeof(PartDev) * n_parts, cudaMemcpyHostToDevice));
+    LRB_CUDA(cudaMemcpy((void*)H.tile_part, tp.data(), sizeof(int32_t) * n_tiles, cudaMemcpyHostToDevice));
+    LRB_CUDA(cudaEventCreate(&D.t0));
+    LRB_CUDA(cudaEventCreate(&D.t1));
+    const int n_share = share[D.device];
+    int g1 = max_grid(team_cg_kernel<false>, D.device, D.n_tiles, n_share);
+    int g2 = max_grid(team_cg_kernel<true>, D.device, D.n_tiles, n_share);
+    int g3 = max_grid(team_bicgstab_kernel, D.device, D.n_tiles, n_share);
+    D.grid = std::min(g1, std::min(g2, g3));
+  }
+  // peer pointer tables
+  std::vector<void*> pf(n_dev), pr(n_dev);
+  for (auto& D : team->devs) {
+    pf[D.rank] = D.host.flags;
+    pr[D.rank] = D.host.part_red;
+  }
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaMemcpy(D.host.peer_flags, pf.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
+    LRB_CUDA(cudaMemcpy(D.host.peer_part_red, pr.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
+  }
+  *out = team.release();
+  return LRB_OK;
+}
+
+int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out) {
+  return lrb_team_create_ex(n_parts, parts, nullptr, out);
+}
+
+void lrb_team_destroy(lrb_team* team) {
+  if (!team) return;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    cudaStreamSynchronize(D.stream);
+    if (D.ws) cudaFree(D.ws);
+    if (D.hist_dev) cudaFree(D.hist_dev);
+    if (D.t0) cudaEventDestroy(D.t0);
+    if (D.t1) cudaEventDestroy(D.t1);
+  }
+  delete team;
+}
+
+// Every part's main stream: pending scatters joined; other local parts' main
+// streams made to wait for the device stream's previous work and vice versa.
+static int team_prologue(lrb_team* team, lrb::TeamDevice& D) {
+  for (int p : D.parts) {
+    int rc = lrb_part_join(team->parts[p]);
+    if (rc) return rc;
+  }
+  DeviceGuard g(D.device);
+  for (int p : D.parts) {
+    lrb_part* P = team->parts[p];
+    if (P->main == D.stream) continue;
+    LRB_CUDA(cudaEventRecord(P->main_done, P->main));
+    LRB_CUDA(cudaStreamWaitEvent(D.stream, P->main_done, 0));
+  }
+  return LRB_OK;
+}
+
+static int team_epilogue(lrb_team* team, lrb::TeamDevice& D) {
+  DeviceGuard g(D.device);
+  LRB_CUDA(cudaEventRecord(team->parts[D.parts.front()]->main_done, D.stream));
+  for (int p : D.parts) {
+    lrb_part* P = team->parts[p];
+    if (P->main != D.stream) LRB_CUDA(cudaStreamWaitEvent(P->main, team->parts[D.parts.front()]->main_done, 0));
+    LRB_CUDA(cudaEventRecord(P->main_done, D.stream));
+  }
+  return LRB_OK;
+}
+
+int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host) {
+  if (!team || !x_host || !y_host) {
+    set_error("lrb_team_spmv: null argument");
+    return LRB_EVALUE;
+  }
+  std::lock_guard<std::mutex> lk(team->mu);
+  for (auto& D : team->devs) {
+    int rc = team_prologue(team, D);
+    if (rc) return rc;
+    DeviceGuard g(D.device);
+    for (int p : D.parts) {
+      lrb_part* P = team->parts[p];
+      if (P->d.n)
+        LRB_CUDA(cudaMemcpyAsync(P->d.s, x_host[p], 8 * P->d.n, cudaMemcpyHostToDevice, D.stream));
+    }
+  }
+  // all x must be resident before any device reads halo values
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaStreamSynchronize(D.stream));
+  }
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    for (int p : D.parts) {
+      lrb_part* P = team->parts[p];
+      if (!P->d.n) continue;
+      spmv_kernel<<<unsigned((P->d.n + 255) / 256), 256, 0, D.stream>>>(D.parts_dev, p);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      LRB_CUDA(cudaGetLastError());
+      LRB_CUDA(cudaMemcpyAsync(y_host[p], P->d.t, 8 * P->d.n, cudaMemcpyDeviceToHost, D.stream));
+    }
+  }
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaStreamSynchronize(D.stream));
+    int rc = team_epilogue(team, D);
+    if (rc) return rc;
+  }
+  return LRB_OK;
+}
+
+int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
+                   double* const* x_host, double tol, int32_t max_iter, lrb_report* rep,
+                   double* hist, int32_t hist_cap) {
+  if (!team || !rep) {
+    set_error("lrb_team_solve: null argument");
+    return LRB_EVALUE;
+  }
+  if (!(tol > 0)) {
+    set_error("tol must be positive");
+    return LRB_EVALUE;
+  }
+  if (method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+    set_error("lrb_team_solve: unknown method");
+    return LRB_EVALUE;
+  }
+  std::lock_guard<std::mutex> lk(team->mu);
+  const bool multi = team->devs.size() > 1;
+  for (auto& D : team->devs) {
+    int rc = team_prologue(team, D);
+    if (rc) return rc;
+    if (hist && hist_cap > 0) {
+      rc = team_hist_capacity(D, hist_cap);
+      if (rc) return rc;
+    }
+    DeviceGuard g(D.device);
+    if (b_host)
+      for (int p : D.parts) {
+        lrb_part* P = team->parts[p];
+        if (P->d.n)
+          LRB_CUDA(cudaMemcpyAsync(P->d.b, b_host[p], 8 * P->d.n, cudaMemcpyHostToDevice, D.stream));
+      }
+    LRB_CUDA(cudaMemsetAsync(D.out_dev, 0, sizeof(SolveOut), D.stream));
+    TeamDev& H = D.host;
+    H.tol = tol;
+    H.max_iter = max_iter;
+    H.hist = (hist && hist_cap > 0) ? D.hist_dev : nullptr;
+    H.hist_cap = hist_cap;
+  }
+  if (multi) {
+    // a device must not start reading peers' b/x before their copies land
+    for (auto& D : team->devs) {
+      DeviceGuard g(D.device);
+      LRB_CUDA(cudaStreamSynchronize(D.stream));
+    }
+  }
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    void* args[] = {&D.host};
+    void* fn = method == LRB_METHOD_CG    ? (void*)team_cg_kernel<false>
+               : method == LRB_METHOD_PCG ? (void*)team_cg_kernel<true>
+                                          : (void*)team_bicgstab_kernel;
+    LRB_CUDA(cudaEventRecord(D.t0, D.stream));
+    if (multi) {
+      // co-residency across devices is guaranteed by separate GPUs; within a
+      // device the grid fits one wave (max_grid)
+      LRB_CUDA(cudaLaunchKernel(fn, dim3(D.grid), dim3(kTPB), args, 0, D.stream));
+    } else {
+      LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(D.grid), dim3(kTPB), args, 0, D.stream));
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    LRB_CUDA(cudaEventRecord(D.t1, D.stream));
+    if (x_host)
+      for (int p : D.parts) {
+        lrb_part* P = team->parts[p];
+        if (P->d.n && x_host[p])
+          LRB_CUDA(cudaMemcpyAsync(x_host[p], P->d.x, 8 * P->d.n, cudaMemcpyDeviceToHost, D.stream));
+      }
+  }
+  SolveOut so{};
+  float ms = 0.f;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaStreamSynchronize(D.stream));
+    SolveOut o{};
+    LRB_CUDA(cudaMemcpy(&o, D.out_dev, sizeof(SolveOut), cudaMemcpyDeviceToHost));
+    float m = 0.f;
+    LRB_CUDA(cudaEventElapsedTime(&m, D.t0, D.t1));
+    ms = std::max(ms, m);
+    if (D.rank == 0) so = o;
+    if (o.status && !so.status) so.status = o.status;
+    int rc = team_epilogue(team, D);
+    if (rc) return rc;
+  }
+  if (hist && hist_cap > 0) {
+    auto& D0 = team->devs[0];
+    DeviceGuard g(D0.device);
+    int n = std::min<int>(hist_cap, std::max(so.iterations, 0));
+    if (n) LRB_CUDA(cudaMemcpy(hist, D0.hist_dev, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  }
+  rep->iterations = so.iterations;
+  rep->converged = so.converged;
+  rep->breakdown = so.breakdown;
+  rep->status = so.status;
+  rep->residual = so.residual;
+  rep->bnorm = so.bnorm;
+  rep->device_ms = ms;
+  if (so.status == LRB_ENOTPD) {
+    set_error("cg: matrix is not positive definite");
+    return LRB_ENOTPD;
+  }
+  if (so.status == LRB_ETIMEOUT) {
+    set_error("team barrier timed out (a device of the team did not arrive)");
+    return LRB_ETIMEOUT;
+  }
+  return LRB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,487 @@
+// sm_100a kernels of the hot path: segment scatter (update), distributed SpMV
+// and the persistent team Krylov solvers (CG / Jacobi-PCG / BiCGStab).
+//
+// Rounding contract (parity with the reference, solver.py:80-147):
+//  * every product and sum is a separately rounded __dmul_rn / __dadd_rn /
+//    __dsub_rn (no FMA contraction), in the reference's elementwise order;
+//  * a row's SpMV accumulates its local entries in stored order, then its
+//    non-local entries, starting from 0.0 — bit-identical to np.add.at;
+//  * dot products: per-tile fixed-order tree, tiles summed in fixed order per
+//    part, parts summed in ascending GPU rank ((p0 + p1) + p2)... exactly the
+//    reference's allreduce order (transport.py:450-458).  Only the in-part
+//    summation order differs from OpenBLAS ddot (tolerance parity).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lrb_internal.h"
+
+namespace lrb {
+
+__device__ __forceinline__ double vload(const double* p) { return *(const volatile double*)p; }
+__device__ __forceinline__ unsigned vload(const unsigned* p) { return *(const volatile unsigned*)p; }
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// SELL-32 row access
+// ---------------------------------------------------------------------------
+struct RowRef {
+  int64_t base;
+  int w;
+};
+__device__ __forceinline__ RowRef row_ref(const PartDev& P, int64_t i) {
+  const int64_t s = i >> 5;
+  const int64_t b = __ldg(P.slice_ptr + s);
+  const int64_t e = __ldg(P.slice_ptr + s + 1);
+  return RowRef{b + (i & 31), int((e - b) >> 5)};
+}
+
+// y_i = sum_k a_ik * f(col_k), reference order, no FMA.  f(Q, j) returns the
+// vector value at row j of part Q (local part or halo owner).
+template <class F>
+__device__ __forceinline__ double row_spmv(const PartDev& P, const PartDev* __restrict__ parts,
+                                           int64_t i, F&& f) {
+  const RowRef rr = row_ref(P, i);
+  double acc = 0.0;
+  for (int k = 0; k < rr.w; ++k) {
+    const int64_t e = rr.base + int64_t(k) * kSlice;
+    const int c = __ldg(P.col + e);
+    if (c < 0) break;
+    const double a = __ldg(P.val + e);
+    double xv;
+    if (c < P.n) {
+      xv = f(P, int64_t(c));
+    } else {
+      const int h = c - int(P.n);
+      xv = f(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+    }
+    acc = __dadd_rn(acc, __dmul_rn(a, xv));
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Update: gather-permute one segment's rows from the receive buffer
+// (apply_scatter, update.py:105-112).  One thread per row; a warp covers one
+// SELL slice so the value stores and index loads are 128/256-byte coalesced.
+// Also refreshes dinv for Jacobi (1/diag, correctly rounded like numpy).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) scatter_rows_kernel(PartDev P, int64_t r0, int64_t r1) {
+  const int64_t i = (r0 & ~int64_t(31)) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < r0 || i >= r1) return;
+  const RowRef rr = row_ref(P, i);
+  const int dk = __ldg(P.dpos + i);
+  for (int k = 0; k < rr.w; ++k) {
+    const int64_t e = rr.base + int64_t(k) * kSlice;
+    const int b = __ldg(P.src + e);
+    if (b < 0) break;
+    const double v = __ldg(P.recv + b);
+    P.val[e] = v;
+    if (k == dk) P.dinv[i] = 1.0 / v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Distributed SpMV y = A x for the API spmv(): x in part.s, y in part.t
+// (halo read straight from the owner's x, any device of the team).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ parts, int p) {
+  const PartDev& P = parts[p];
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const double y = row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.s[j]; });
+  P.t[i] = y;
+}
+
+// ---------------------------------------------------------------------------
+// Team barrier with fused deterministic reduction.
+// ---------------------------------------------------------------------------
+template <int NR>
+__device__ __forceinline__ void block_sum(double (&acc)[NR], double (*sm)[kMaxRed]) {
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int j = 0; j < NR; ++j) sm[w][j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double s = sm[0][j];
+      for (int q = 1; q < kTPB / 32; ++q) s = __dadd_rn(s, sm[q][j]);
+      acc[j] = s;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void team_fail(const TeamDev& T, int code) {
+  atomicCAS((int*)&T.out->status, 0, code);
+}
+
+// All blocks of this device arrive; the last one reduces the tile partials of
+// every local part in fixed order, exchanges part values with the peer devices
+// (NVLink peer stores + release/acquire flags), sums all parts in ascending
+// GPU rank and releases everybody.  Returns the team-reduced values in red[].
+template <int NR>
+__device__ void team_sync(const TeamDev& T, double* red) {
+  __shared__ unsigned s_last, s_gen;
+  __shared__ double sm[kTPB / 32][kMaxRed];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_gen = vload(T.bar_gen);
+    if (T.n_dev > 1)
+      __threadfence_system();
+    else
+      __threadfence();
+    const unsigned t = atomicAdd(T.bar_count, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int p = T.part_begin; p < T.part_end; ++p) {
+      const PartDev& P = T.parts[p];
+      double acc[NR];
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+      for (int64_t t = threadIdx.x; t < P.ntiles; t += kTPB) {
+        const double* src = T.partials + (P.tile0 + t) * kMaxRed;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[j] = __dadd_rn(acc[j], vload(src + j));
+      }
+      block_sum<NR>(acc, sm);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          T.part_red[p * kMaxRed + j] = acc[j];
+          for (int d = 0; d < T.n_dev; ++d)
+            if (d != T.dev_rank) T.peer_part_red[d][p * kMaxRed + j] = acc[j];
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (T.n_dev > 1) {
+        __threadfence_system();
+        const unsigned long long e = ++(*T.epoch);
+        for (int d = 0; d < T.n_dev; ++d)
+          if (d != T.dev_rank) st_release_sys(T.peer_flags[d] + T.dev_rank, e);
+        const long long t0 = global_ns();
+        for (int d = 0; d < T.n_dev; ++d) {
+          if (d == T.dev_rank) continue;
+          while (ld_acquire_sys(T.flags + d) < e) {
+            __nanosleep(64);
+            if (global_ns() - t0 > T.timeout_ns) {
+              team_fail(T, LRB_ETIMEOUT);
+              break;
+            }
+          }
+        }
+        __threadfence_system();
+      }
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        double s = vload(T.part_red + j);
+        for (int p = 1; p < T.n_parts; ++p) s = __dadd_rn(s, vload(T.part_red + p * kMaxRed + j));
+        T.red[j] = s;
+      }
+      *T.bar_count = 0;
+      __threadfence();
+      atomicAdd(T.bar_gen, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    const long long t0 = global_ns();
+    while (vload(T.bar_gen) == s_gen) {
+      __nanosleep(32);
+      if (global_ns() - t0 > T.timeout_ns) {
+        team_fail(T, LRB_ETIMEOUT);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NR; ++j) red[j] = vload(T.red + j);
+}
+
+// Tile-loop helper: runs body(P, i, acc) over every row of every tile of this
+// block, stores the per-tile partials, then team-syncs.  The row order inside
+// a tile and the reduction tree are fixed, so partials are deterministic.
+template <int NR, class Body>
+__device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
+  __shared__ double sm[kTPB / 32][kMaxRed];
+  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) {
+    const int p = __ldg(T.tile_part + tile);
+    const PartDev P = T.parts[p];  // by value: no aliasing with the vector stores
+    const int64_t row0 = (tile - P.tile0) * kTile;
+    double acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int m = 0; m < kRPT; ++m) {
+      const int64_t i = row0 + m * kTPB + threadIdx.x;
+      if (i < P.n) body(P, i, acc);
+    }
+    block_sum<NR>(acc, sm);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) T.partials[tile * kMaxRed + j] = acc[j];
+    }
+  }
+  team_sync<NR>(T, red);
+}
+
+__device__ __forceinline__ bool team_failed(const TeamDev& T) {
+  return *(const volatile int*)&T.out->status != 0;
+}
+
+// ---------------------------------------------------------------------------
+// CG / Jacobi-PCG (solver.py:100-147).
+//
+// Per iteration two fused phases (+ the true-residual phase every 10th
+// iteration or when the recurrence residual meets tol):
+//  A: p_new = z + beta*p_old computed on the fly for every row and neighbour
+//     (z = r, or dinv*r for PCG), q = A p_new, store p_new and q, partial p.q
+//  B: x += step*p, r -= step*q, partial r.r (and r.z for PCG)
+//  C: y = A x, partial |b - y|^2
+// p is double-buffered so phase A can read neighbours' p_old while writing p_new.
+// ---------------------------------------------------------------------------
+template <bool JAC>
+__global__ void __launch_bounds__(kTPB) team_cg_kernel(TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  double red[2];
+  // phase 0: x = 0, r = b, partial b.b (and r.z)
+  team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    const double b = P.b[i];
+    P.x[i] = 0.0;
+    P.r[i] = b;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+    if (JAC) acc[1] = __dadd_rn(acc[1], __dmul_rn(b, __dmul_rn(P.dinv[i], b)));
+  });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  double rho = JAC ? red[1] : bb;
+  double beta = 0.0, res = 1.0;
+  int pa = 0;  // p_old lives in p0 when pa == 0
+  bool first = true, converged = false;
+  int it = 0;
+  for (it = 1; it <= T.max_iter; ++it) {
+    // ---- phase A: p_new, q = A p_new, p.q
+    team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+      auto pnew = [&](const PartDev& Q, int64_t j) -> double {
+        const double r = Q.r[j];
+        const double z = JAC ? __dmul_rn(Q.dinv[j], r) : r;
+        if (first) return z;
+        const double po = pa ? Q.p1[j] : Q.p0[j];
+        return __dadd_rn(z, __dmul_rn(beta, po));
+      };
+      const double pi = pnew(P, i);
+      const double qi = row_spmv(P, parts, i, pnew);
+      (pa ? P.p0 : P.p1)[i] = pi;
+      P.q[i] = qi;
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
+    });
+    if (team_failed(T)) break;
+    const double pq = red[0];
+    if (pq <= 0.0) {
+      if (lead) team_fail(T, LRB_ENOTPD);
+      break;
+    }
+    const double step = rho / pq;
+    pa ^= 1;  // p_new is now p_old for the elementwise phase and the next iteration
+    // ---- phase B: x += step p, r -= step q, r.r (, r.z)
+    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+      const double p = (pa ? P.p1 : P.p0)[i];
+      const double x = __dadd_rn(P.x[i], __dmul_rn(step, p));
+      const double r = __dsub_rn(P.r[i], __dmul_rn(step, P.q[i]));
+      P.x[i] = x;
+      P.r[i] = r;
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+      if (JAC) acc[1] = __dadd_rn(acc[1], __dmul_rn(r, __dmul_rn(P.dinv[i], r)));
+    });
+    if (team_failed(T)) break;
+    const double rr_new = red[0];
+    const double rho_new = JAC ? red[1] : rr_new;
+    const double rec = sqrt(rr_new) / bnorm;
+    if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
+    if (rec <= T.tol || it % 10 == 0) {
+      // ---- phase C: true residual |b - A x|
+      team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+        const double ax =
+            row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
+        const double d = __dsub_rn(P.b[i], ax);
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+      });
+      if (team_failed(T)) break;
+      res = sqrt(red[0]) / bnorm;
+      if (res <= T.tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      res = rec;
+    }
+    beta = rho_new / rho;
+    rho = rho_new;
+    first = false;
+  }
+  if (lead) {
+    out->iterations = it > T.max_iter ? T.max_iter : it;
+    out->converged = converged ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BiCGStab (oracle/krylov.py:bicgstab).  Three fused phases:
+//  1: p_new = r + beta*(p_old - omega*v_old) on the fly, v = A p_new, rhat.v
+//  2: s = r - alpha*v on the fly, t = A s, t.s, t.t
+//  3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r
+// p and v are double-buffered.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTPB) team_bicgstab_kernel(TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  double red[2];
+  team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+    const double b = P.b[i];
+    P.x[i] = 0.0;
+    P.r[i] = b;
+    P.rhat[i] = b;
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+  });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  double rho = bb, rho_prev = 1.0, alpha = 1.0, omega = 1.0, beta = 0.0, res = 1.0;
+  int pa = 0;  // p_old/v_old in p0/v0 when pa == 0
+  bool converged = false, breakdown = false;
+  int it = 0;
+  for (it = 1; it <= T.max_iter; ++it) {
+    const bool first = (it == 1);
+    if (!first) beta = __dmul_rn(rho / rho_prev, alpha / omega);
+    // ---- phase 1
+    team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+      auto pnew = [&](const PartDev& Q, int64_t j) -> double {
+        const double r = Q.r[j];
+        if (first) return r;
+        const double po = pa ? Q.p1[j] : Q.p0[j];
+        const double vo = pa ? Q.v1[j] : Q.v0[j];
+        return __dadd_rn(r, __dmul_rn(beta, __dsub_rn(po, __dmul_rn(omega, vo))));
+      };
+      const double pi = pnew(P, i);
+      const double vi = row_spmv(P, parts, i, pnew);
+      (pa ? P.p0 : P.p1)[i] = pi;
+      (pa ? P.v0 : P.v1)[i] = vi;
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(P.rhat[i], vi));
+    });
+    if (team_failed(T)) break;
+    pa ^= 1;
+    const double rv = red[0];
+    if (rv == 0.0) {
+      breakdown = true;
+      break;
+    }
+    alpha = rho / rv;
+    // ---- phase 2
+    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+      auto sval = [&](const PartDev& Q, int64_t j) -> double {
+        const double v = pa ? Q.v1[j] : Q.v0[j];
+        return __dsub_rn(Q.r[j], __dmul_rn(alpha, v));
+      };
+      const double si = sval(P, i);
+      const double ti = row_spmv(P, parts, i, sval);
+      P.s[i] = si;
+      P.t[i] = ti;
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(ti, si));
+      acc[1] = __dadd_rn(acc[1], __dmul_rn(ti, ti));
+    });
+    if (team_failed(T)) break;
+    omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
+    // ---- phase 3
+    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+      const double p = (pa ? P.p1 : P.p0)[i];
+      const double s = P.s[i];
+      const double x = __dadd_rn(__dadd_rn(P.x[i], __dmul_rn(alpha, p)), __dmul_rn(omega, s));
+      const double r = __dsub_rn(s, __dmul_rn(omega, P.t[i]));
+      P.x[i] = x;
+      P.r[i] = r;
+      acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+      acc[1] = __dadd_rn(acc[1], __dmul_rn(P.rhat[i], r));
+    });
+    if (team_failed(T)) break;
+    const double rr = red[0];
+    rho_prev = rho;
+    rho = red[1];
+    const double rec = sqrt(rr) / bnorm;
+    if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
+    if (rec <= T.tol || it % 10 == 0) {
+      team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+        const double ax =
+            row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
+        const double d = __dsub_rn(P.b[i], ax);
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+      });
+      if (team_failed(T)) break;
+      res = sqrt(red[0]) / bnorm;
+      if (res <= T.tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      res = rec;
+    }
+    if (omega == 0.0 || rho == 0.0) {
+      breakdown = true;
+      break;
+    }
+  }
+  if (lead) {
+    out->iterations = it > T.max_iter ? T.max_iter : it;
+    out->converged = converged ? 1 : 0;
+    out->breakdown = breakdown ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+}  // namespace lrb

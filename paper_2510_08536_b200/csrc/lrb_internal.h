@@ -1,0 +1,119 @@
+// Internal structures shared by the host builder, the CUDA kernels and the C-ABI.
+// Not part of the public interface (see include/ldurepart_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace lrb {
+
+// ---------------------------------------------------------------------------
+// Device layout of one fused owner part ("GPU part k", repart.py:307-318).
+//
+// The fused matrix is stored once, in SELL-32: rows are grouped in slices of
+// 32 consecutive rows (one warp), each slice padded to its longest row and
+// laid out column-major (entry k of the slice's 32 rows are 32 consecutive
+// words).  A row's entries are its local entries in ascending column order
+// followed by its non-local entries in ascending halo order — exactly the
+// reference's row-major `local` then `non_local` order (solver.py:92-97), so a
+// per-row sequential product sum reproduces solver.spmv bit for bit.
+//   col[e] <  n         : part-local column
+//   col[e] >= n         : halo slot (col - n), resolved via hpart/hidx
+//   col[e] == -1        : padding (always at the end of a row)
+//   src[e]              : receive-buffer position scattered into val[e]
+// ---------------------------------------------------------------------------
+constexpr int kSlice = 32;
+
+struct PartDev {
+  int64_t n;          // owned rows
+  int64_t n_halo;
+  int64_t n_buf;      // receive-buffer length (= nnz, bijection)
+  int64_t n_slices;
+  const int64_t* slice_ptr;   // [n_slices+1] entry offsets
+  const int32_t* col;         // [E]
+  const int32_t* src;         // [E] scatter inverse (buffer position or -1)
+  const int8_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
+  const int32_t* hpart;       // [n_halo] team part that owns halo slot
+  const int32_t* hidx;        // [n_halo] row of that part
+  double* val;                // [E]
+  double* recv;               // [n_buf]
+  // Krylov vectors, [n] each
+  double *x, *r, *p0, *p1, *q, *b, *dinv;
+  double *rhat, *v0, *v1, *s, *t;
+  // tiling inside the team kernel
+  int64_t tile0;      // first tile of this part in its device's tile space
+  int64_t ntiles;
+};
+
+// Work decomposition of the persistent kernels: a tile is kTPB*kRPT rows of
+// one part.  The per-tile partial dot products are reduced in fixed order,
+// so results do not depend on grid size or scheduling.
+constexpr int kTPB = 256;
+constexpr int kRPT = 2;
+constexpr int kTile = kTPB * kRPT;
+constexpr int kMaxRed = 4;   // reductions fused into one barrier
+
+enum Method { kCG = 0, kPCG = 1, kBiCGStab = 2 };
+
+struct SolveOut {
+  int32_t iterations;
+  int32_t converged;
+  int32_t status;      // 0 ok, LRB_ENOTPD, LRB_ETIMEOUT
+  int32_t breakdown;
+  double residual;
+  double bnorm;
+};
+
+// Per-device team state, in device memory.
+struct TeamDev {
+  int32_t n_parts;          // team-wide
+  int32_t dev_rank;         // this device's rank in the team
+  int32_t n_dev;
+  int32_t part_begin;       // parts [part_begin, part_end) live on this device
+  int32_t part_end;
+  int32_t pad_;
+  int64_t n_tiles;          // tiles of this device
+  PartDev* parts;           // [n_parts] (remote parts carry peer pointers)
+  const int32_t* tile_part; // [n_tiles]
+  double* partials;         // [n_tiles * kMaxRed]
+  double* part_red;         // [n_parts * kMaxRed] every device holds all parts' values
+  double* red;              // [kMaxRed] team-reduced values (this device)
+  unsigned int* bar_count;
+  unsigned int* bar_gen;
+  unsigned long long* epoch;    // barrier epoch (this device)
+  unsigned long long* flags;    // [n_dev] arrival epochs written by peers
+  // peers' arrays (index = device rank), valid when n_dev > 1
+  unsigned long long** peer_flags;
+  double** peer_part_red;
+  SolveOut* out;
+  double* hist;             // [hist_cap] recurrence residual per iteration (nullable)
+  int32_t hist_cap;
+  int32_t max_iter;
+  double tol;
+  long long timeout_ns;
+};
+
+// ---------------------------------------------------------------------------
+// Host plan produced by the create path (plan.cpp).
+// ---------------------------------------------------------------------------
+struct Plan {
+  int64_t total = 0, lo = 0, hi = 0, n = 0, n_buf = 0;
+  std::vector<int64_t> loc_ptr, nl_ptr;     // [n+1]
+  std::vector<int32_t> loc_col, loc_src;    // part-local col, buffer pos
+  std::vector<int32_t> nl_col, nl_src;      // halo slot, buffer pos
+  std::vector<int64_t> halo_cols;           // ascending global
+  std::vector<int32_t> hpart, hidx;         // halo owner part / row in it
+  std::vector<int64_t> seg_off;             // receive offsets [n_src+1]
+  std::vector<int64_t> seg_rows;            // segment row ranges (part-local) [n_src+1]
+  // SELL
+  int64_t n_slices = 0;
+  std::vector<int64_t> slice_ptr;
+  std::vector<int32_t> sell_col, sell_src;
+  std::vector<int8_t> dpos;
+  int64_t sell_entries() const { return slice_ptr.empty() ? 0 : slice_ptr.back(); }
+};
+
+void set_error(const std::string& msg);
+
+}  // namespace lrb

@@ -1,0 +1,244 @@
+"""Device parts and teams: thin owners of native handles + PyTorch buffers.
+
+PyTorch allocates the memory (one device arena per part, one pinned host
+stage); everything else — layout, uploads, H2D copies, kernels — happens in
+libldurepart_b200.so behind the C ABI.
+"""
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _native as N
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("ldurepart_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+def device_count() -> int:
+    return _torch().cuda.device_count()
+
+
+class Plan:
+    """Host create-path artifact (lrb_plan): fused patterns + scatter inverse."""
+
+    def __init__(self, handle):
+        self.h = handle
+        info = np.zeros(10, dtype=np.int64)
+        N.check(N.lrb_plan_info(self.h, N.ptr(info)))
+        (self.n, self.nnz_local, self.nnz_nonlocal, self.n_halo, self.n_buf, self.n_slices,
+         self.sell_entries, self.max_row_len, self.n_seg, self.device_bytes) = (int(v) for v in info)
+        self._csr = None
+
+    @classmethod
+    def from_ldu(cls, total, lo, hi, src_rows, face_off, lower, upper, ifc_off, ifc_row, ifc_col,
+                 gpu_offsets, n_threads=0):
+        h = C.c_void_p()
+        arrs = [N.i64(a) for a in (src_rows, face_off, lower, upper, ifc_off, ifc_row, ifc_col,
+                                   gpu_offsets)]
+        src_rows, face_off, lower, upper, ifc_off, ifc_row, ifc_col, gpu_offsets = arrs
+        N.check(N.lrb_plan_build_ldu(total, lo, hi, len(src_rows) - 1, N.ptr(src_rows),
+                                     N.ptr(face_off), N.ptr(lower), N.ptr(upper), N.ptr(ifc_off),
+                                     N.ptr(ifc_row), N.ptr(ifc_col), len(gpu_offsets) - 1,
+                                     N.ptr(gpu_offsets), n_threads, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_coo(cls, total, lo, hi, buf_row, buf_col, seg_off=None, gpu_offsets=None):
+        h = C.c_void_p()
+        buf_row, buf_col = N.i64(buf_row), N.i64(buf_col)
+        seg = None if seg_off is None else N.i64(seg_off)
+        go = None if gpu_offsets is None else N.i64(gpu_offsets)
+        N.check(N.lrb_plan_build_coo(total, lo, hi, len(buf_row), N.ptr(buf_row), N.ptr(buf_col),
+                                     0 if seg is None else len(seg) - 1, N.ptr(seg),
+                                     0 if go is None else len(go) - 1, N.ptr(go), C.byref(h)))
+        return cls(h)
+
+    def csr(self):
+        """(loc_ptr, loc_col, nl_ptr, nl_col, halo_cols) int64, frozen."""
+        if self._csr is None:
+            out = (np.empty(self.n + 1, np.int64), np.empty(self.nnz_local, np.int64),
+                   np.empty(self.n + 1, np.int64), np.empty(self.nnz_nonlocal, np.int64),
+                   np.empty(self.n_halo, np.int64))
+            N.check(N.lrb_plan_export_csr(self.h, *(N.ptr(a) for a in out)))
+            for a in out:
+                a.setflags(write=False)
+            self._csr = out
+        return self._csr
+
+    def scatter(self):
+        to_local = np.empty(self.n_buf, np.uint8)
+        index = np.empty(self.n_buf, np.int64)
+        N.check(N.lrb_plan_export_scatter(self.h, N.ptr(to_local), N.ptr(index)))
+        return to_local.view(bool), index
+
+    def sell(self):
+        """Device layout as built on the host: (slice_ptr, col, src, dpos)."""
+        sp = np.empty(self.n_slices + 1, np.int64)
+        col = np.empty(self.sell_entries, np.int32)
+        src = np.empty(self.sell_entries, np.int32)
+        dpos = np.empty(self.n, np.int8)
+        N.check(N.lrb_plan_export_sell(self.h, N.ptr(sp), N.ptr(col), N.ptr(src), N.ptr(dpos)))
+        return sp, col, src, dpos
+
+    def halo_owners(self):
+        hp = np.empty(self.n_halo, np.int32)
+        hi = np.empty(self.n_halo, np.int32)
+        N.check(N.lrb_plan_export_halo(self.h, N.ptr(hp), N.ptr(hi)))
+        return hp, hi
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            N.lrb_plan_destroy(h)
+
+
+class DevicePart:
+    """One fused owner part on one GPU (lrb_part) with its PyTorch-owned memory."""
+
+    def __init__(self, plan: Plan, device: int):
+        torch = _torch()
+        self.plan = plan
+        self.device = int(device)
+        self.n = plan.n
+        self.n_buf = plan.n_buf
+        self.arena = torch.empty(plan.device_bytes + 256, dtype=torch.uint8,
+                                 device=f"cuda:{self.device}")
+        base = self.arena.data_ptr()
+        aligned = (base + 255) & ~255
+        self.stage = torch.empty(max(plan.n_buf, 1), dtype=torch.float64, pin_memory=True)
+        self.stage_np = self.stage.numpy()
+        h = C.c_void_p()
+        N.check(N.lrb_part_create(plan.h, self.device, aligned, plan.device_bytes,
+                                  self.stage.data_ptr(), plan.n_buf, C.byref(h)))
+        self.h = h
+        self._values_cache = None
+        self._version = 0
+        self._lock = threading.Lock()
+
+    # ---- update path -----------------------------------------------------
+    @staticmethod
+    def _pieces(pieces):
+        arrs = [np.ascontiguousarray(p, dtype=np.float64) for p in pieces]
+        ptrs = N.ptr_array([a.ctypes.data for a in arrs])
+        lens = np.array([len(a) for a in arrs], dtype=np.int64)
+        return arrs, ptrs, lens
+
+    def update_segment(self, seg, pieces):
+        arrs, ptrs, lens = self._pieces(pieces)
+        N.check(N.lrb_update_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
+        self._touch()
+
+    def stage_segment(self, seg, pieces):
+        arrs, ptrs, lens = self._pieces(pieces)
+        N.check(N.lrb_stage_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
+
+    def update_staged_from_stage(self):
+        ptrs = N.ptr_array([self.stage.data_ptr()])
+        lens = np.array([self.n_buf], dtype=np.int64)
+        N.check(N.lrb_update_staged(self.h, 1, ptrs, N.ptr(lens)))
+        self._touch()
+
+    def apply_scatter(self):
+        N.check(N.lrb_apply_scatter(self.h))
+        self._touch()
+
+    def fill(self, offset, values):
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        N.check(N.lrb_part_fill(self.h, int(offset), N.ptr(values), len(values)))
+
+    def read_buffer(self):
+        out = np.empty(self.n_buf, np.float64)
+        N.check(N.lrb_part_read_buffer(self.h, N.ptr(out)))
+        return out
+
+    def _touch(self):
+        with self._lock:
+            self._version += 1
+            self._values_cache = None
+
+    def read_values(self):
+        """(local vals, non-local vals) in the reference's row-major order."""
+        with self._lock:
+            if self._values_cache is None:
+                lv = np.empty(self.plan.nnz_local, np.float64)
+                nv = np.empty(self.plan.nnz_nonlocal, np.float64)
+                N.check(N.lrb_part_read_values(self.h, N.ptr(lv), N.ptr(nv)))
+                self._values_cache = (lv, nv)
+            lv, nv = self._values_cache
+        return {"local": lv.copy(), "non_local": nv.copy()}
+
+    def join(self):
+        N.check(N.lrb_part_join(self.h))
+
+    def sync(self):
+        N.check(N.lrb_part_sync(self.h))
+
+    def mark(self):
+        N.check(N.lrb_part_mark(self.h))
+
+    def elapsed_ms(self):
+        ms = C.c_float()
+        N.check(N.lrb_part_elapsed_ms(self.h, C.byref(ms)))
+        return float(ms.value)
+
+    def pointers(self):
+        arr = (C.c_void_p * 16)()
+        N.check(N.lrb_part_pointers(self.h, arr))
+        names = ("recv", "val", "x", "r", "p0", "p1", "q", "b", "dinv", "rhat", "v0", "v1", "s",
+                 "t", "col", "src")
+        return dict(zip(names, (int(p or 0) for p in arr)))
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            N.lrb_part_destroy(h)
+
+
+class Team:
+    """The owner parts of C_a; parts on one device share one persistent kernel."""
+
+    def __init__(self, parts, dev_ranks=None):
+        self.parts = list(parts)
+        arr = N.ptr_array([p.h.value for p in self.parts])
+        h = C.c_void_p()
+        if dev_ranks is None:
+            N.check(N.lrb_team_create(len(self.parts), arr, C.byref(h)))
+        else:
+            dr = np.ascontiguousarray(dev_ranks, dtype=np.int32)
+            N.check(N.lrb_team_create_ex(len(self.parts), arr, N.ptr(dr), C.byref(h)))
+        self.h = h
+        self._lock = threading.Lock()
+
+    def spmv(self, xs):
+        xs = [np.ascontiguousarray(x, dtype=np.float64) for x in xs]
+        ys = [np.empty(p.n, np.float64) for p in self.parts]
+        N.check(N.lrb_team_spmv(self.h, N.ptr_array([x.ctypes.data for x in xs]),
+                                N.ptr_array([y.ctypes.data for y in ys])))
+        return ys
+
+    def solve(self, method, bs, tol, max_iter, want_x=True, hist_cap=0):
+        """Run one Krylov solve; bs None = right-hand sides already on device."""
+        rep = N.Report()
+        bptr = None
+        if bs is not None:
+            bs = [np.ascontiguousarray(b, dtype=np.float64) for b in bs]
+            bptr = N.ptr_array([b.ctypes.data for b in bs])
+        xs = [np.empty(p.n, np.float64) for p in self.parts] if want_x else None
+        xptr = N.ptr_array([x.ctypes.data for x in xs]) if want_x else None
+        hist = np.zeros(max(hist_cap, 0), np.float64)
+        rc = N.lrb_team_solve(self.h, N.METHODS[method], bptr, xptr, float(tol), int(max_iter),
+                              C.byref(rep), N.ptr(hist) if hist_cap > 0 else None, int(hist_cap))
+        N.check(rc)
+        return xs, rep, hist[:max(min(rep.iterations, hist_cap), 0)]
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            N.lrb_team_destroy(h)
