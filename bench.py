@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""Benchmark: ms per timestep (matrix update + Krylov solve) on B200.
+
+Workload (BASELINE.json configs[2], "C3"): 3D cavity 200^3 (8M cells),
+``--rpg`` CPU assembly ranks per GPU (default 8) repartitioned onto N GPUs,
+pressure Jacobi-PCG to 1e-6 with b = ones, timesteps 2.. of the reference
+protocol (cli.py:181-272; step 1 = creation, excluded).  One timestep =
+update (all coefficients of every rank: H2D + gather-permute) + solve.
+
+* ``value``  device-resident: coefficients already in the receive buffer in
+  HBM, b resident; timed = scatter kernel + solve kernel (CUDA events).
+* ``e2e``    through the public API (``update`` from pinned host LDU arrays by
+  every rank thread, then ``cg_solve`` with b from host and x back to host).
+* ``--impl reference``: the reference CPU path (oracle port, oracle/) on the
+  host cores, bounded sample scaled to a full timestep.
+
+Inputs (1.5 GB PCG working set at N=1) are larger than L2, so no L2 flush is
+needed between timed steps.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/timestep (matrix update + CG solve) at 1/2/4/8 B200; % of HBM roofline"
+WORKLOADS = {
+    # name: (N, default rpg, method, description)
+    "c3": (200, 8, "pcg", "C3: 3D cavity 200^3 (8M cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "
+                          "(alpha {alpha}), pressure Jacobi-PCG to 1e-6, b=ones"),
+    "c2": (100, 8, "pcg", "C2: 3D cavity 100^3 (1M cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "
+                          "(alpha {alpha}), Jacobi-PCG to 1e-6"),
+    "c1": (32, 4, "pcg", "C1: 3D cavity 32^3, {n_cpu} CPU ranks -> {n_gpu} device(s) "
+                         "(alpha {alpha}), Jacobi-PCG to 1e-6"),
+}
+TOL, MAX_ITER = 1e-6, 2000
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:  # noqa: BLE001 - clocks are best effort
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7])
+                          if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# roofline accounting
+# ---------------------------------------------------------------------------
+def solve_bytes(n, nnz, h, iterations, checks, method):
+    """Algorithmic HBM bytes of one solve: CG it 12nnz+4(n+1)+88n+8h, PCG +16n,
+    true-residual check 12nnz+4(n+1)+16n+8h, init (b read, x r written) 24n."""
+    it = 12 * nnz + 4 * (n + 1) + 88 * n + 8 * h + (16 * n if method == "pcg" else 0)
+    chk = 12 * nnz + 4 * (n + 1) + 16 * n + 8 * h
+    return iterations * it + checks * chk + 24 * n
+
+
+def n_checks(history, iterations, tol):
+    c = 0
+    for it in range(1, iterations + 1):
+        rec = history[it - 1] if it - 1 < len(history) else 0.0
+        if rec <= tol or it % 10 == 0:
+            c += 1
+    return c
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# problem
+# ---------------------------------------------------------------------------
+class Problem:
+    """Per-rank LDU inputs whose value arrays live in pinned host memory."""
+
+    def __init__(self, N, n_cpu, ranks, pinned=True):
+        import paper_2510_08536_b200 as lrb
+        self.lrb = lrb
+        grid = lrb.StructuredGrid(N, N, N)
+        parts = lrb.decompose_slab(grid, n_cpu)
+        self.cells = [p.n_cells for p in parts]
+        self.base = {}
+        self.live = {}
+        for r in ranks:
+            m, ifs = lrb.assemble_poisson(parts[r])
+            self.base[r] = (m, ifs)
+            if pinned:
+                import torch
+                pin = lambda a: self._pin(torch, a)  # noqa: E731
+                diag = pin(m.diag)
+                mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, diag,
+                                   pin(m.lower_val), pin(m.upper_val))
+                ifp = [lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote, pin(b.values))
+                       for b in ifs]
+                self.live[r] = (mm, ifp, diag)
+            parts[r] = None   # drop the mesh (faces live on in the LDU matrix)
+        self.n_cells = grid.total_cells
+
+    @staticmethod
+    def _pin(torch, a):
+        t = torch.empty(len(a), dtype=torch.float64, pin_memory=True)
+        out = t.numpy()
+        out[:] = a
+        out._keep = t  # noqa: SLF001 - keep the pinned tensor alive
+        return out
+
+    def produce(self, r, step):
+        """Producer (outside the metric, like the reference's t_assemble):
+        write step's diag into the pinned array of rank r."""
+        m, ifs = self.base[r]
+        mm, ifp, diag = self.live[r]
+        self.lrb.perturb_diag_into(m.diag, step, diag)
+        return mm, ifp
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2510_08536_b200 as lrb
+    from paper_2510_08536_b200 import _native
+
+    rank, world, local_rank = dist_env()
+    if world > 1:
+        return run_ours_multi(args)
+    N, _, method_default, desc = WORKLOADS[args.workload]
+    method = args.method or method_default
+    n_gpu = args.gpus
+    n_cpu = args.rpg * n_gpu
+    alpha = args.rpg
+    torch.cuda.set_device(0)
+    t0 = time.monotonic()
+    prob = Problem(N, n_cpu, range(n_cpu))
+    pm = lrb.make_partition_map(prob.cells, alpha)
+    log(f"[bench] inputs {time.monotonic() - t0:.1f}s; n_cpu={n_cpu} alpha={alpha}")
+    n_steps = args.warmup + args.steps
+    steps = list(range(2, 2 + n_steps))
+    rec = {"e2e_ms": [], "wall_ms": [], "iters": [], "value_ms": [], "scatter_ms": [],
+           "solve_ms": [], "kernel_ms": [], "checks": [], "launches": 0, "create_s": 0.0}
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] or 0))
+
+    def program(ctx):
+        r = ctx.rank
+        m0, if0 = prob.base[r]
+        tc = time.monotonic()
+        system = lrb.repartition(m0, if0, pm, ctx)
+        ctx.barrier()
+        if r == 0:
+            rec["create_s"] = time.monotonic() - tc
+        b = np.ones(system.matrix.n_owned) if system.is_owner else None
+        # ---------------- e2e: public API, host buffers ----------------------
+        for i, step in enumerate(steps):
+            m_s, if_s = prob.produce(r, step)
+            ctx.barrier()
+            if r == 0:
+                if i == args.warmup:
+                    sampler.__enter__()
+                    rec["l0"] = _native.lrb_launch_count()
+                system.part.mark()
+                tw = time.perf_counter()
+            lrb.update(system, m_s, if_s, args.mode)
+            if system.is_owner:
+                x, rep = lrb.cg_solve(system.matrix, system.halo, b, TOL, MAX_ITER, system.comm,
+                                      method=method)
+            if r == 0:
+                system.part.mark()
+                wall = (time.perf_counter() - tw) * 1e3
+                if i >= args.warmup:
+                    rec["e2e_ms"].append(system.part.elapsed_ms())
+                    rec["wall_ms"].append(wall)
+                    rec["iters"].append(rep.iterations)
+                if i == n_steps - 1:
+                    rec["launches"] = _native.lrb_launch_count() - rec["l0"]
+        ctx.barrier()
+        if r == 0:
+            sampler.__exit__()
+        # ---------------- value: device-resident (HBM) inputs ---------------
+        for i, step in enumerate(steps):
+            m_s, if_s = prob.produce(r, step)
+            lrb.update(system, m_s, if_s, "direct")     # untimed: coefficients -> HBM
+            ctx.barrier()
+            if r == 0:
+                part, team = system.part, system.team
+                part.sync()
+                part.mark()
+                part.apply_scatter()
+                part.mark()
+                _, rep, hist = team.solve(method, None, TOL, MAX_ITER, want_x=False,
+                                          hist_cap=MAX_ITER)
+                t_sc = part.elapsed_ms()
+                part.mark()
+                part.sync()
+                if i >= args.warmup:
+                    rec["scatter_ms"].append(t_sc)
+                    rec["kernel_ms"].append(rep.device_ms)
+                    rec["value_ms"].append(t_sc + rep.device_ms)
+                    rec["checks"].append(n_checks(hist, rep.iterations, TOL))
+                    rec.setdefault("value_iters", []).append(rep.iterations)
+            ctx.barrier()
+        if r == 0:
+            p = system.part.plan
+            rec["plan"] = (p.n, p.nnz_local + p.nnz_nonlocal, p.n_halo, p.n_buf)
+        return None
+
+    lrb.run_world(n_cpu, program)
+    log(f"[bench] ours done ({time.monotonic() - t0:.1f}s)")
+    return finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha), N,
+                       n_cpu, alpha, sampler)
+
+
+def run_ours_multi(args):
+    raise SystemExit("multi-GPU bench path not built yet")
+
+
+def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
+    n, nnz, h, n_buf = rec["plan"]
+    value = float(np.mean(rec["value_ms"]))
+    peak, peak_kind = measured_peak()
+    alg = [solve_bytes(n, nnz, h, it, ck, method) for it, ck in zip(rec["value_iters"],
+                                                                    rec["checks"])]
+    achieved = float(np.mean([b / (ms * 1e-3) / 1e9 for b, ms in zip(alg, rec["kernel_ms"])]))
+    scatter_gbs = float(np.mean([20 * n_buf / (ms * 1e-3) / 1e9 for ms in rec["scatter_ms"]]))
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "ms/timestep",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(value, 4), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference cavity generator, "
+                                                    "closed form)",
+        "config": {"workload": desc, "n_cells": N ** 3, "n_cpu": n_cpu, "alpha": alpha,
+                   "mode": args.mode, "method": method, "tol": TOL,
+                   "timesteps": f"{2 + args.warmup}..{1 + args.warmup + args.steps}",
+                   "l2": "inputs larger than L2 (no flush needed)" if N >= 100 else
+                         "L2-resident (latency-bound)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "team_cg_kernel<JAC> (persistent, whole solve)",
+                     "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": int(np.mean(alg)),
+                     "kernel_ms": round(float(np.mean(rec["kernel_ms"])), 4)},
+        "e2e": {"value": round(float(np.mean(rec["e2e_ms"])), 4), "unit": "ms/timestep",
+                "h2d_bytes_per_step": int(8 * n_buf + 8 * n),
+                "d2h_bytes_per_step": int(8 * n),
+                "wall_ms": round(float(np.mean(rec["wall_ms"])), 4)},
+        "breakdown": {"scatter_ms": round(float(np.mean(rec["scatter_ms"])), 4),
+                      "scatter_gbs": round(scatter_gbs, 1),
+                      "solve_kernel_ms": round(float(np.mean(rec["kernel_ms"])), 4),
+                      "iterations": rec["value_iters"], "create_s": round(rec["create_s"], 2)},
+        "gpu_launches": int(rec["launches"]),
+        "clocks": sampler.summary(),
+    }
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                t = json.load(fh).get(args.workload)
+            if t:
+                line["roofline"]["traffic"] = t.get("dram_bytes_per_launch")
+                line["roofline"]["traffic_note"] = t.get("note")
+        except Exception:  # noqa: BLE001
+            pass
+    return line
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(args, iters_per_step=None):
+    from oracle import cavity as ocav
+    from oracle import krylov
+    from oracle.pipeline import OraclePipeline
+
+    N, _, method_default, desc = WORKLOADS[args.workload]
+    n_gpu = args.gpus
+    n_cpu = args.rpg * n_gpu
+    alpha = args.rpg
+    t0 = time.monotonic()
+    probs = ocav.cavity_problems((N, N, N), n_cpu)
+    offsets = np.concatenate(([0], np.cumsum([p.n for p in probs]))).astype(np.int64)
+    pipe = OraclePipeline(probs, offsets, alpha)
+    t_create = time.monotonic() - t0
+    table = iters_per_step or _iteration_table(N, n_cpu, alpha)
+    samples = []
+    steps = list(range(2, 2 + args.warmup + args.steps))
+    k_iter = 3
+    for i, step in enumerate(steps):
+        ps = [ocav.perturb(p, step) for p in probs]
+        ts = time.perf_counter()
+        pipe.update(ps)
+        t_up = time.perf_counter() - ts
+        S = pipe.system
+        bs = pipe.rhs_ones()
+        ts = time.perf_counter()
+        krylov.cg(S, bs, 1e-300, k_iter, jacobi=(method_default == "pcg"))
+        t_it = (time.perf_counter() - ts) / k_iter
+        ts = time.perf_counter()
+        S.spmv(bs)
+        t_spmv = time.perf_counter() - ts
+        if step in table:
+            its = table[step]
+            checks = its // 10 + (1 if its % 10 else 0)
+            ms = (t_up + its * t_it + checks * t_spmv) * 1e3
+        else:   # small case: just run the whole solve
+            ts = time.perf_counter()
+            krylov.cg(S, bs, TOL, MAX_ITER, jacobi=(method_default == "pcg"))
+            ms = (t_up + time.perf_counter() - ts) * 1e3
+        if i >= args.warmup:
+            samples.append(ms)
+        if time.monotonic() - t0 > args.cpu_budget_s and len(samples) >= 1:
+            break
+    return {"value": round(float(np.mean(samples)), 2), "unit": "ms/timestep", "cores": 1,
+            "kind": "port",
+            "sample": (f"oracle/ numpy port of the reference path, {N}^3 {n_cpu} ranks -> "
+                       f"{n_gpu} part(s): full update + {k_iter} timed "
+                       f"{'Jacobi-PCG' if method_default == 'pcg' else 'CG'} iterations + 1 SpMV "
+                       f"per step, scaled to the step's iteration count; create "
+                       f"{t_create:.1f}s excluded; {len(samples)} steps"),
+            "create_s": round(t_create, 1)}
+
+
+def _iteration_table(N, n_cpu, alpha):
+    path = os.path.join(ROOT, "tests", "golden", f"iters_{N}_r{n_cpu}_a{alpha}.json")
+    if not os.path.exists(path):
+        cand = [f for f in os.listdir(os.path.join(ROOT, "tests", "golden"))
+                if f.startswith(f"iters_{N}_")]
+        if not cand:
+            return {}
+        path = os.path.join(ROOT, "tests", "golden", cand[0])
+    with open(path) as fh:
+        return {row["step"]: row["iterations"] for row in json.load(fh)["steps"]}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    base = cpu_baseline(args)
+    N, _, method_default, desc = WORKLOADS[args.workload]
+    n_cpu = args.rpg * args.gpus
+    return {
+        "metric": METRIC, "value": base["value"], "unit": "ms/timestep", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["value"],
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": desc.format(n_cpu=n_cpu, n_gpu=args.gpus, alpha=args.rpg),
+                   "n_cells": N ** 3, "n_cpu": n_cpu, "alpha": args.rpg, "method": method_default,
+                   "tol": TOL},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": base["value"], "unit": "ms/timestep", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--rpg", type=int, default=None, help="CPU ranks per GPU (alpha)")
+    ap.add_argument("--mode", choices=("direct", "staged"), default="direct")
+    ap.add_argument("--method", choices=("cg", "pcg"), default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=60.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.rpg is None:
+        args.rpg = WORKLOADS[args.workload][1]
+    if args.impl == "reference":
+        line = run_reference(args)
+    else:
+        line = run_ours(args)
+        rank, world, _ = dist_env()
+        if line is not None and rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = {k: v for k, v in cpu_baseline(args, {
+                2 + args.warmup + i: it for i, it in enumerate(line["breakdown"]["iterations"])
+            }).items() if k != "create_s"}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

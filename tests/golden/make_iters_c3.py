@@ -48,7 +48,7 @@ def main():
                     print(rows[-1], file=sys.stderr, flush=True)
         return t_create
 
-    t_create = lr.run_world(n_cpu, program)
+    t_create = lr.run_world(n_cpu, program, timeout=1e6)
     out = os.path.join(os.path.dirname(os.path.abspath(__file__)),
                        f"iters_{n}_r{n_cpu}_a{alpha}.json")
     with open(out, "w") as fh:

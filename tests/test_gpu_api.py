@@ -1,0 +1,309 @@
+"""The reference's own hot-path tests (tests/test_repart.py, test_update.py,
+test_solver.py, test_acceptance.py 4-6) ported to the drop-in, plus BiCGStab
+against the oracle and the cross-device team protocol on one GPU."""
+
+import numpy as np
+import pytest
+
+import paper_2510_08536_b200 as lrb
+from helpers_b200 import cavity_case, chain_setup
+from oracle import cavity as ocav
+from oracle.pipeline import OraclePipeline
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def chain():
+    grid, parts, assembled, _ = chain_setup(4)
+    pm = lrb.make_partition_map([p.n_cells for p in parts], 2)
+    return grid, parts, assembled, pm
+
+
+def test_chain_alpha2_values(chain):
+    _, _, asm, pm = chain
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        if s.is_owner:
+            return s.matrix.local.vals.tolist(), s.matrix.non_local.vals.tolist()
+
+    res = lrb.run_world(4, program)
+    assert res[0] == ([2, -1, -1, 2, -1, -1, 2, -1, -1, 2], [-1])
+    assert res[2] == ([2, -1, -1, 2, -1, -1, 2, -1, -1, 2], [-1])
+
+
+def test_inactive_ranks_never_allocate(chain):
+    _, _, asm, pm = chain
+    world = lrb.World(4)
+    world.run(lambda ctx: lrb.repartition(*asm[ctx.rank], pm, ctx) and None)
+    assert world.device_allocations == [1, 0, 1, 0]
+
+
+def test_device_buffer_and_apply_scatter(chain):
+    _, _, asm, pm = chain
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        if s.is_owner:
+            buf = s.device.values()
+            s.device.fill(0, np.zeros(len(s.device)))
+            lrb.apply_scatter(s.device, s.scatter, s.matrix)
+            zero = (s.matrix.local.vals.tolist(), s.matrix.non_local.vals.tolist())
+            s.device.fill(0, buf)
+            lrb.apply_scatter(s.device, s.scatter, s.matrix)
+            return buf.tolist(), zero, s.matrix.local.vals.tolist()
+
+    res = lrb.run_world(4, program)
+    assert res[0][0] == [2, 2, -1, -1, -1, 2, 2, -1, -1, -1, -1]
+    assert res[0][1] == ([0.0] * 10, [0.0])
+    assert res[0][2] == [2, -1, -1, 2, -1, -1, 2, -1, -1, 2]
+
+
+def test_update_twenty_steps_match_fresh_repartition():
+    _, asm, pm = cavity_case((6, 6, 6), 4, 2)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        ok = True
+        for step in range(1, 21):
+            ms, ifs = lrb.perturb_coefficients(*asm[ctx.rank], step)
+            lrb.update(s, ms, ifs, "direct" if step % 2 else "staged")
+            fresh = lrb.repartition(ms, ifs, pm, ctx)
+            if s.is_owner:
+                ok &= np.array_equal(s.matrix.local.vals, fresh.matrix.local.vals)
+                ok &= np.array_equal(s.matrix.non_local.vals, fresh.matrix.non_local.vals)
+        return ok
+
+    assert all(lrb.run_world(4, program))
+
+
+@pytest.mark.parametrize("alpha", [2, 4])
+def test_transfer_counts_direct_vs_staged(alpha):
+    _, asm, pm = cavity_case((12, 12, 12), 8, alpha)
+
+    def program(ctx):
+        d = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        st = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        for step in (2, 3):
+            ms, ifs = lrb.perturb_coefficients(*asm[ctx.rank], step)
+            bd = d.device.transfer_count if d.is_owner else 0
+            lrb.update(d, ms, ifs, "direct")
+            bs = st.device.transfer_count if st.is_owner else 0
+            lrb.update(st, ms, ifs, "staged")
+            if d.is_owner:
+                assert d.device.transfer_count - bd == pm.alpha
+                assert st.device.transfer_count - bs == 1
+                assert np.array_equal(d.matrix.local.vals, st.matrix.local.vals)
+                assert np.array_equal(d.matrix.non_local.vals, st.matrix.non_local.vals)
+        return True
+
+    assert all(lrb.run_world(8, program))
+
+
+def test_pattern_drift_detected(chain):
+    _, _, asm, pm = chain
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        m, _ = asm[ctx.rank]
+        lrb.update(s, lrb.LduMatrix(m.n_cells, [], [], m.diag, [], []), [], "direct")
+
+    with pytest.raises(lrb.RankFailedError) as err:
+        lrb.run_world(4, program)
+    assert isinstance(err.value.cause, lrb.PatternDriftError)
+    assert "pattern drift" in str(err.value.cause)
+
+
+def test_pattern_arrays_never_rewritten(chain):
+    _, _, asm, pm = chain
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        before = s.matrix.local.rows if s.is_owner else None
+        ms, ifs = lrb.perturb_coefficients(*asm[ctx.rank], 2)
+        lrb.update(s, ms, ifs, "direct")
+        if s.is_owner:
+            assert s.matrix.local.rows is before
+            assert not s.matrix.local.rows.flags.writeable
+        return True
+
+    assert all(lrb.run_world(4, program))
+
+
+def test_unknown_mode_and_length_violation(chain):
+    _, _, asm, pm = chain
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        with pytest.raises(ValueError, match="mode"):
+            lrb.update(s, *asm[ctx.rank], "bogus")
+        return True
+
+    assert all(lrb.run_world(4, program))
+
+
+def test_spmv_row_sums_and_dimension_mismatch():
+    _, _, asm, pm = chain_setup(4, alpha=2)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        if s.is_owner:
+            y = lrb.spmv(s.matrix, s.halo, np.ones(s.matrix.n_owned), s.comm)
+            z = lrb.spmv(s.matrix, s.halo, np.zeros(s.matrix.n_owned), s.comm)
+            return y.tolist(), z.tolist()
+
+    res = lrb.run_world(4, program)
+    assert res[0] == ([1, 0, 0, 0], [0, 0, 0, 0]) and res[2] == ([0, 0, 0, 1], [0, 0, 0, 0])
+
+    def bad(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        if s.is_owner:
+            lrb.spmv(s.matrix, s.halo, np.zeros(3), s.comm)
+
+    with pytest.raises(lrb.RankFailedError, match="rank"):
+        lrb.run_world(4, bad)
+
+
+def solve_case(dims, n_cpu, alpha, tol=1e-10, b_value=1.0, max_iter=500, method="cg", step=None):
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+
+    def program(ctx):
+        m, ifs = asm[ctx.rank]
+        s = lrb.repartition(m, ifs, pm, ctx)
+        if step:
+            lrb.update(s, *lrb.perturb_coefficients(m, ifs, step), "direct")
+        if not s.is_owner:
+            return None
+        b = np.full(s.matrix.n_owned, b_value)
+        x, rep = lrb.cg_solve(s.matrix, s.halo, b, tol, max_iter, s.comm, method=method,
+                              history=True)
+        pieces = s.comm.gather(x, 0)
+        return (np.concatenate(pieces), rep) if pieces is not None else rep
+
+    return lrb.run_world(n_cpu, program)[0]
+
+
+@pytest.mark.parametrize("alpha", [1, 2, 4, 8])
+def test_chain8_cg_solution(alpha):
+    x, rep = solve_case((8, 1, 1), 8, alpha)
+    np.testing.assert_allclose(x, [4, 7, 9, 10, 10, 9, 7, 4], atol=1e-10)
+    assert rep.converged and rep.iterations <= 8
+
+
+def test_zero_rhs_and_max_iter():
+    x, rep = solve_case((8, 1, 1), 4, 2, b_value=0.0)
+    assert rep.iterations == 0 and rep.converged and (x == 0).all()
+    _, rep = solve_case((6, 6, 6), 4, 2, tol=1e-30, max_iter=40)
+    assert not rep.converged and rep.iterations == 40
+
+
+def test_converged_residual_is_true_residual():
+    from oracle.repart import build_owner  # noqa: F401  (oracle used as checker only)
+    grid, asm, pm = cavity_case((6, 6, 6), 4, 2)
+    x, rep = solve_case((6, 6, 6), 4, 2, tol=1e-8)
+    probs = ocav.cavity_problems((6, 6, 6), 4)
+    pipe = OraclePipeline(probs, pm.offsets, 2)
+    ys = pipe.system.spmv([x[p.lo:p.hi] for p in pipe.parts])
+    r = 1.0 - np.concatenate(ys)
+    true_res = np.linalg.norm(r) / np.sqrt(len(r))
+    assert rep.converged and true_res <= 1e-8
+    assert abs(true_res - rep.residual) <= 1e-12
+
+
+def test_solve_deterministic_and_alpha_invariant():
+    runs = [solve_case((12, 12, 12), 8, 2, tol=1e-9) for _ in range(3)]
+    for x, rep in runs[1:]:
+        assert np.array_equal(x, runs[0][0]) and rep.iterations == runs[0][1].iterations
+        assert rep.residual == runs[0][1].residual
+    # (2 ranks, alpha 1) and (4 ranks, alpha 2) give identical I_GPU at 12^3
+    xa, ra = solve_case((12, 12, 12), 2, 1, tol=1e-9)
+    xb, rb = solve_case((12, 12, 12), 4, 2, tol=1e-9)
+    assert np.array_equal(xa, xb) and ra.iterations == rb.iterations
+
+
+def test_not_positive_definite_raises():
+    grid = lrb.StructuredGrid(6, 6, 6)
+    parts = lrb.decompose_slab(grid, 2)
+    asm = []
+    for p in parts:
+        m, ifs = lrb.assemble_poisson(p)
+        asm.append((lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, -m.diag, m.lower_val,
+                                  m.upper_val), ifs))
+    pm = lrb.make_partition_map([p.n_cells for p in parts], 1)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), 1e-8, 100, s.comm)
+
+    with pytest.raises(lrb.RankFailedError) as err:
+        lrb.run_world(2, program)
+    assert "not positive definite" in str(err.value.cause)
+
+
+def _momentum(asm, seed=0):
+    """Non-symmetric, diagonally dominant LDU on the cavity addressing."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for m, ifs in asm:
+        eps_u = 0.05 * rng.random(m.n_faces)
+        eps_l = 0.05 * rng.random(m.n_faces)
+        mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, np.full(m.n_cells, 6.5),
+                           -1.0 - eps_l, -1.0 + eps_u)
+        out.append((mm, ifs))
+    return out
+
+
+@pytest.mark.parametrize("alpha", [1, 2, 4])
+def test_bicgstab_matches_oracle(alpha):
+    _, asm, pm = cavity_case((12, 12, 12), 4, alpha)
+    mom = _momentum(asm)
+
+    def program(ctx):
+        s = lrb.repartition(*mom[ctx.rank], pm, ctx)
+        if not s.is_owner:
+            return None
+        x, rep = lrb.bicgstab_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), 1e-10, 500,
+                                    s.comm, history=True)
+        pieces = s.comm.gather(x, 0)
+        return (np.concatenate(pieces), rep) if pieces is not None else rep
+
+    x, rep = lrb.run_world(4, program)[0]
+    probs = [ocav.RankProblem(m.n_cells, m.lower_addr, m.upper_addr, m.diag, m.lower_val,
+                              m.upper_val, tuple(ocav.Block(b.neighbor_rank, b.rows, b.cols_remote,
+                                                            b.values) for b in ifs))
+             for m, ifs in mom]
+    pipe = OraclePipeline(probs, pm.offsets, alpha)
+    xo, ro = pipe.solve("bicgstab", 1e-10, 500)
+    assert rep.converged and ro.converged
+    assert abs(rep.iterations - ro.iterations) <= 1
+    n = min(len(ro.history), len(rep.history))
+    np.testing.assert_allclose(rep.history[:n], ro.history[:n], rtol=1e-8)
+    np.testing.assert_allclose(x, np.concatenate(xo), rtol=1e-8, atol=1e-12)
+
+
+def test_cross_device_protocol_on_one_gpu():
+    """Parts split into separate 'device ranks' (separate kernels talking through
+    the peer-flag protocol) must give bit-identical results to one kernel."""
+    from paper_2510_08536_b200.device import Team
+    _, asm, pm = cavity_case((16, 16, 16), 4, 1)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        parts = s.comm.allgather(s.part)
+        if s.comm.group_rank == 0:
+            bs = [np.ones(p.n) for p in parts]
+            one = s.team.solve("cg", bs, 1e-9, 500)
+            split = Team(parts, dev_ranks=[0, 0, 1, 1]).solve("cg", bs, 1e-9, 500)
+            split4 = Team(parts, dev_ranks=[0, 1, 2, 3]).solve("pcg", bs, 1e-9, 500)
+            pcg = s.team.solve("pcg", bs, 1e-9, 500)
+            return one, split, split4, pcg
+        return None
+
+    one, split, split4, pcg = lrb.run_world(4, program)[0]
+    assert one[1].iterations == split[1].iterations
+    for a, b in zip(one[0], split[0]):
+        assert np.array_equal(a, b)
+    assert pcg[1].iterations == split4[1].iterations
+    for a, b in zip(pcg[0], split4[0]):
+        assert np.array_equal(a, b)

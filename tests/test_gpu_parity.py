@@ -1,0 +1,132 @@
+"""GPU parity of the drop-in API against the reference's golden outputs.
+
+Bar (BASELINE.json north_star): integer artifacts and scattered values
+bit-exact; SpMV bit-exact (same per-row order, no FMA); CG recurrence-residual
+history within 1e-10 relative of the reference with iterations within +-1.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2510_08536_b200 as lrb
+from golden_cases import case_config, case_meta, case_names, get, matches, spmv_inputs
+from helpers_b200 import golden_inputs
+
+pytestmark = pytest.mark.gpu
+
+CASES = case_names()
+SMALL = [c for c in CASES if c not in ("c2",)]
+HIST_RTOL = 1e-10
+
+
+def ref_history(log, iterations, tol):
+    """sqrt(rr)/|b| per iteration from the reference's allreduce log."""
+    bb = log[0]
+    out, i = [], 1
+    for it in range(1, iterations + 1):
+        rec = np.sqrt(log[i + 1]) / np.sqrt(bb)
+        out.append(rec)
+        i += 2
+        if rec <= tol or it % 10 == 0:
+            i += 1
+    return np.array(out)
+
+
+def run_case(name, mode="direct", solve=True, method="cg"):
+    pm, per_rank = golden_inputs(name)
+    cfg = case_config(name)
+    xs = spmv_inputs(name, pm.total_cells)
+
+    def program(ctx):
+        m, ifs = per_rank[ctx.rank]
+        system = lrb.repartition(m, ifs, pm, ctx)
+        out = {}
+        if system.is_owner:
+            mat = system.matrix
+            out["vals_1"] = (mat.local.vals, mat.non_local.vals)
+            out["rows"] = (mat.local.rows, mat.local.cols, mat.non_local.rows, mat.non_local.cols,
+                           mat.halo_cols)
+            if xs is not None:
+                lo, hi = pm.gpu_range(mat.owner_gpu_rank)
+                out["spmv"] = [lrb.spmv(mat, system.halo, x[lo:hi], system.comm) for x in xs]
+        for s in sorted(set(cfg["steps"]) | set(cfg["solve_steps"] if solve else ())):
+            if s >= 2:
+                ms, ifs_s = lrb.perturb_coefficients(m, ifs, s)
+                lrb.update(system, ms, ifs_s, mode)
+                if system.is_owner and s in cfg["steps"]:
+                    out[f"vals_{s}"] = (system.matrix.local.vals, system.matrix.non_local.vals)
+            if solve and s in cfg["solve_steps"] and system.is_owner:
+                b = np.ones(system.matrix.n_owned)
+                x, rep = lrb.cg_solve(system.matrix, system.halo, b, cfg["tol"], cfg["max_iter"],
+                                      system.comm, method=method, history=True)
+                out[f"cg_{s}"] = (x, rep)
+        return out
+
+    res = lrb.run_world(pm.n_cpu, program)
+    return pm, {k: res[pm.alpha * k] for k in range(pm.n_gpu)}
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_values_and_spmv_bit_exact(name):
+    pm, owners = run_case(name, solve=False)
+    cfg = case_config(name)
+    for k, out in owners.items():
+        lr, lc, nr, nc, halo = out["rows"]
+        assert matches(name, k, "local_rows", lr) and matches(name, k, "local_cols", lc)
+        assert matches(name, k, "nl_rows", nr) and matches(name, k, "nl_cols", nc)
+        assert matches(name, k, "halo_cols", halo)
+        assert matches(name, k, "vals_1_local", out["vals_1"][0])
+        assert matches(name, k, "vals_1_nl", out["vals_1"][1])
+        for s in cfg["steps"]:
+            assert matches(name, k, f"vals_{s}_local", out[f"vals_{s}"][0]), (k, s)
+            assert matches(name, k, f"vals_{s}_nl", out[f"vals_{s}"][1]), (k, s)
+        for i, y in enumerate(out.get("spmv", [])):
+            assert np.array_equal(y, get(name, k, f"spmv_{i}")), (name, k, i)
+
+
+@pytest.mark.parametrize("name", [c for c in SMALL if c.startswith("cav12") or c.startswith("chain4")])
+def test_staged_equals_direct(name):
+    _, direct = run_case(name, "direct", solve=False)
+    _, staged = run_case(name, "staged", solve=False)
+    for k in direct:
+        for key in direct[k]:
+            if key.startswith("vals_"):
+                assert np.array_equal(direct[k][key][0], staged[k][key][0])
+                assert np.array_equal(direct[k][key][1], staged[k][key][1])
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if case_config(c)["solve_steps"]])
+def test_cg_history_matches_reference(name):
+    pm, owners = run_case(name)
+    cfg = case_config(name)
+    for s in cfg["solve_steps"]:
+        it_ref, res_ref, conv_ref = get(name, 0, f"cg_{s}_rep")
+        ref = ref_history(get(name, 0, f"cg_{s}_log"), int(it_ref), cfg["tol"])
+        x0, rep = owners[0][f"cg_{s}"]
+        assert abs(rep.iterations - int(it_ref)) <= 1, (s, rep.iterations, it_ref)
+        assert rep.converged == bool(conv_ref)
+        n = min(len(ref), len(rep.history))
+        rel = np.abs(rep.history[:n] - ref[:n]) / ref[:n]
+        assert rel.max() <= HIST_RTOL, (s, rel.max())
+        # every owner reports the same team result
+        for k, out in owners.items():
+            assert out[f"cg_{s}"][1].iterations == rep.iterations
+        xref = get(name, 0, f"cg_{s}_x")
+        if xref is not None:
+            for k, out in owners.items():
+                np.testing.assert_allclose(out[f"cg_{s}"][0], get(name, k, f"cg_{s}_x"),
+                                           rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["c1", "cav12x12x12_r8_a2", "cav7x9x11_r6_a3"])
+def test_pcg_matches_reference_cg(name):
+    """Uniform cavity diagonal: Jacobi-PCG iterates equal CG's up to rounding."""
+    pm, owners = run_case(name, method="pcg")
+    cfg = case_config(name)
+    for s in cfg["solve_steps"]:
+        it_ref = int(get(name, 0, f"cg_{s}_rep")[0])
+        ref = ref_history(get(name, 0, f"cg_{s}_log"), it_ref, cfg["tol"])
+        _, rep = owners[0][f"cg_{s}"]
+        assert abs(rep.iterations - it_ref) <= 1
+        n = min(len(ref), len(rep.history))
+        assert (np.abs(rep.history[:n] - ref[:n]) / ref[:n]).max() <= HIST_RTOL
