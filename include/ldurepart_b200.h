@@ -133,6 +133,9 @@ int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_va
 /* Make the part's solve stream wait for all pending segment scatters. */
 int lrb_part_join(lrb_part* part);
 int lrb_part_sync(lrb_part* part);
+/* out[4] = pieces copied zero-copy from pinned memory, pageable pieces staged,
+ * H2D bytes, scatter launches (since create). */
+int lrb_part_stats(const lrb_part* part, int64_t* out);
 /* Device time (ms) between the last two lrb_part_mark() calls on the solve stream. */
 int lrb_part_mark(lrb_part* part);
 int lrb_part_elapsed_ms(lrb_part* part, float* ms);

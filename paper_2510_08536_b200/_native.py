@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libldurepart_b200.so")
+LIB_PATH = os.environ.get("LRB_LIB") or os.path.join(HERE, "libldurepart_b200.so")
 
 LRB_OK = 0
 LRB_EVALUE = -1
@@ -82,6 +82,7 @@ lrb_part_read_buffer = _sig("lrb_part_read_buffer", C.c_int, P, P)
 lrb_part_read_values = _sig("lrb_part_read_values", C.c_int, P, P, P)
 lrb_part_join = _sig("lrb_part_join", C.c_int, P)
 lrb_part_sync = _sig("lrb_part_sync", C.c_int, P)
+lrb_part_stats = _sig("lrb_part_stats", C.c_int, P, P)
 lrb_part_mark = _sig("lrb_part_mark", C.c_int, P)
 lrb_part_elapsed_ms = _sig("lrb_part_elapsed_ms", C.c_int, P, C.POINTER(C.c_float))
 lrb_team_create = _sig("lrb_team_create", C.c_int, I32, P, C.POINTER(P))
@@ -96,7 +97,7 @@ EXPORTED = [
     "lrb_plan_export_scatter", "lrb_plan_export_halo", "lrb_plan_export_sell", "lrb_plan_destroy", "lrb_part_create",
     "lrb_part_destroy", "lrb_part_pointers", "lrb_update_segment", "lrb_update_staged",
     "lrb_stage_segment", "lrb_apply_scatter", "lrb_part_fill", "lrb_part_read_buffer",
-    "lrb_part_read_values", "lrb_part_join", "lrb_part_sync", "lrb_part_mark",
+    "lrb_part_read_values", "lrb_part_join", "lrb_part_sync", "lrb_part_stats", "lrb_part_mark",
     "lrb_part_elapsed_ms", "lrb_team_create", "lrb_team_create_ex", "lrb_team_destroy",
     "lrb_team_spmv", "lrb_team_solve",
 ]

@@ -37,11 +37,13 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
+    """Compile the library; ``out``/``extra`` build tuning variants (e.g. -DLRB_MINB=3)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES],
-           "-o", LIB + ".tmp"]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES],
+           "-o", lib + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
@@ -51,8 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         fh.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -98,6 +98,9 @@ struct lrb_part {
   double* stage = nullptr;          // pinned, n_buf doubles (caller-owned)
   int64_t stage_len = 0;
   cudaEvent_t stage_free = nullptr; // last H2D from the whole-buffer stage
+  // [0] pinned pieces copied zero-copy, [1] pageable pieces staged,
+  // [2] H2D bytes, [3] scatter launches
+  std::atomic<int64_t> stats[4] = {0, 0, 0, 0};
   std::mutex mu;
 };
 
@@ -119,6 +122,7 @@ static int launch_scatter(lrb_part* P, int64_t r0, int64_t r1, cudaStream_t st) 
   const int64_t blocks = (threads + 255) / 256;
   scatter_rows_kernel<<<unsigned(blocks), 256, 0, st>>>(P->d, r0, r1);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  P->stats[3] += 1;
   LRB_CUDA(cudaGetLastError());
   return LRB_OK;
 }
@@ -297,6 +301,8 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
   for (int i = 0; i < n_pieces && all_pinned; ++i)
     if (piece_len[i]) all_pinned = is_pinned(pieces[i]);
   double* dst = part->d.recv + off;
+  part->stats[all_pinned ? 0 : 1] += n_pieces;
+  part->stats[2] += 8 * len;
   if (all_pinned) {
     int64_t o = 0;
     for (int i = 0; i < n_pieces; ++i) {
@@ -486,6 +492,15 @@ int lrb_part_sync(lrb_part* part) {
   return LRB_OK;
 }
 
+int lrb_part_stats(const lrb_part* part, int64_t* out) {
+  if (!part || !out) {
+    set_error("lrb_part_stats: null argument");
+    return LRB_EVALUE;
+  }
+  for (int i = 0; i < 4; ++i) out[i] = part->stats[i].load();
+  return LRB_OK;
+}
+
 int lrb_part_mark(lrb_part* part) {
   if (!part) {
     set_error("lrb_part_mark: null part");
@@ -521,7 +536,8 @@ struct TeamDevice {
   int rank = 0;         // device rank in the team
   std::vector<int> parts;
   int64_t n_tiles = 0;
-  int grid = 0;
+  int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
+  size_t smem[3] = {0, 0, 0};
   cudaStream_t stream = nullptr;  // main stream of the first local part
   void* ws = nullptr;             // device workspace (cudaMalloc, create time)
   TeamDev host{};                 // kernel argument
@@ -553,13 +569,25 @@ static int team_hist_capacity(TeamDevice& D, int cap) {
   return LRB_OK;
 }
 
+// Largest co-resident grid (one wave) for a persistent team kernel; the
+// dynamic shared memory holds the warp partials of the block's tiles.
 template <class K>
-static int max_grid(K kernel, int device, int64_t n_tiles, int n_share) {
+static int max_grid(K kernel, int device, int64_t n_tiles, int n_share, size_t* smem) {
   int sms = 0, per_sm = 0;
-  LRB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  LRB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTPB, 0));
-  int64_t cap = int64_t(sms) * std::max(per_sm, 1) / std::max(n_share, 1);
-  return int(std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(n_tiles, 1))));
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  const int64_t tiles = std::max<int64_t>(n_tiles, 1);
+  const int64_t slots = std::max<int64_t>(1, sms / std::max(n_share, 1));
+  const size_t smem_max = phase_smem_bytes((tiles + slots - 1) / slots);
+  if (smem_max > 200 * 1024) return -2;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)) !=
+      cudaSuccess)
+    return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTPB, smem_max) != cudaSuccess)
+    return -1;
+  const int64_t cap = int64_t(sms) * std::max(per_sm, 1) / std::max(n_share, 1);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, tiles)));
+  *smem = std::max(*smem, phase_smem_bytes((tiles + grid - 1) / grid));
+  return grid;
 }
 
 }  // namespace lrb
@@ -691,10 +719,14 @@ int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* d
     LRB_CUDA(cudaEventCreate(&D.t0));
     LRB_CUDA(cudaEventCreate(&D.t1));
     const int n_share = share[D.device];
-    int g1 = max_grid(team_cg_kernel<false>, D.device, D.n_tiles, n_share);
-    int g2 = max_grid(team_cg_kernel<true>, D.device, D.n_tiles, n_share);
-    int g3 = max_grid(team_bicgstab_kernel, D.device, D.n_tiles, n_share);
-    D.grid = std::min(g1, std::min(g2, g3));
+    D.grid[0] = max_grid(team_cg_kernel<false>, D.device, D.n_tiles, n_share, &D.smem[0]);
+    D.grid[1] = max_grid(team_cg_kernel<true>, D.device, D.n_tiles, n_share, &D.smem[1]);
+    D.grid[2] = max_grid(team_bicgstab_kernel, D.device, D.n_tiles, n_share, &D.smem[2]);
+    for (int m = 0; m < 3; ++m)
+      if (D.grid[m] <= 0) {
+        set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
+        return LRB_ERUNTIME;
+      }
   }
   // peer pointer tables
   std::vector<void*> pf(n_dev), pr(n_dev);
@@ -717,9 +749,10 @@ int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out) {
 
 void lrb_team_destroy(lrb_team* team) {
   if (!team) return;
+  // The parts (and their streams) may already be gone: Python finalizes the
+  // objects of a reference cycle in arbitrary order.  cudaFree synchronizes.
   for (auto& D : team->devs) {
     DeviceGuard g(D.device);
-    cudaStreamSynchronize(D.stream);
     if (D.ws) cudaFree(D.ws);
     if (D.hist_dev) cudaFree(D.hist_dev);
     if (D.t0) cudaEventDestroy(D.t0);
@@ -848,13 +881,15 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     void* fn = method == LRB_METHOD_CG    ? (void*)team_cg_kernel<false>
                : method == LRB_METHOD_PCG ? (void*)team_cg_kernel<true>
                                           : (void*)team_bicgstab_kernel;
+    const int grid = D.grid[method];
+    const size_t smem = D.smem[method];
     LRB_CUDA(cudaEventRecord(D.t0, D.stream));
     if (multi) {
       // co-residency across devices is guaranteed by separate GPUs; within a
       // device the grid fits one wave (max_grid)
-      LRB_CUDA(cudaLaunchKernel(fn, dim3(D.grid), dim3(kTPB), args, 0, D.stream));
+      LRB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));
     } else {
-      LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(D.grid), dim3(kTPB), args, 0, D.stream));
+      LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LRB_CUDA(cudaEventRecord(D.t1, D.stream));

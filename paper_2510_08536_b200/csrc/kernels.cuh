@@ -52,24 +52,53 @@ __device__ __forceinline__ RowRef row_ref(const PartDev& P, int64_t i) {
 
 // y_i = sum_k a_ik * f(col_k), reference order, no FMA.  f(Q, j) returns the
 // vector value at row j of part Q (local part or halo owner).
+//
+// Entries are processed in chunks of kChunk: all column loads of a chunk are
+// issued, then all value loads and vector gathers, then the products are
+// accumulated in entry order.  The slice width is warp-uniform, so the chunk
+// loop never diverges; padding (col -1) only predicates lanes off.  This keeps
+// ~3*kChunk independent loads in flight per thread instead of a dependent
+// col -> x -> add chain per entry.
+#ifndef LRB_CHUNK
+#define LRB_CHUNK 8
+#endif
+constexpr int kChunk = LRB_CHUNK;
+
+// Minimum resident blocks per SM requested from ptxas for the persistent
+// solvers (register cap 65536 / (256 * LRB_MINB)).
+#ifndef LRB_MINB
+#define LRB_MINB 2
+#endif
+
 template <class F>
 __device__ __forceinline__ double row_spmv(const PartDev& P, const PartDev* __restrict__ parts,
                                            int64_t i, F&& f) {
   const RowRef rr = row_ref(P, i);
+  const int n = int(P.n);
   double acc = 0.0;
-  for (int k = 0; k < rr.w; ++k) {
-    const int64_t e = rr.base + int64_t(k) * kSlice;
-    const int c = __ldg(P.col + e);
-    if (c < 0) break;
-    const double a = __ldg(P.val + e);
-    double xv;
-    if (c < P.n) {
-      xv = f(P, int64_t(c));
-    } else {
-      const int h = c - int(P.n);
-      xv = f(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+  for (int k0 = 0; k0 < rr.w; k0 += kChunk) {
+    int c[kChunk];
+    double a[kChunk], xv[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      c[u] = (k0 + u < rr.w) ? __ldg(P.col + rr.base + int64_t(k0 + u) * kSlice) : -1;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      a[u] = 0.0;
+      xv[u] = 0.0;
+      if (c[u] >= 0) {
+        a[u] = __ldg(P.val + rr.base + int64_t(k0 + u) * kSlice);
+        if (c[u] < n) {
+          xv[u] = f(P, int64_t(c[u]));
+        } else {
+          const int h = c[u] - n;
+          xv[u] = f(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+        }
+      }
     }
-    acc = __dadd_rn(acc, __dmul_rn(a, xv));
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(a[u], xv[u]));
   }
   return acc;
 }
@@ -85,13 +114,20 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(PartDev P, int64_t r0
   if (i < r0 || i >= r1) return;
   const RowRef rr = row_ref(P, i);
   const int dk = __ldg(P.dpos + i);
-  for (int k = 0; k < rr.w; ++k) {
-    const int64_t e = rr.base + int64_t(k) * kSlice;
-    const int b = __ldg(P.src + e);
-    if (b < 0) break;
-    const double v = __ldg(P.recv + b);
-    P.val[e] = v;
-    if (k == dk) P.dinv[i] = 1.0 / v;
+  for (int k0 = 0; k0 < rr.w; k0 += kChunk) {
+    int b[kChunk];
+    double v[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      b[u] = (k0 + u < rr.w) ? __ldg(P.src + rr.base + int64_t(k0 + u) * kSlice) : -1;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) v[u] = b[u] >= 0 ? __ldg(P.recv + b[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      if (b[u] < 0) continue;
+      P.val[rr.base + int64_t(k0 + u) * kSlice] = v[u];
+      if (k0 + u == dk) P.dinv[i] = 1.0 / v[u];
+    }
   }
 }
 
@@ -223,12 +259,23 @@ __device__ void team_sync(const TeamDev& T, double* red) {
 }
 
 // Tile-loop helper: runs body(P, i, acc) over every row of every tile of this
-// block, stores the per-tile partials, then team-syncs.  The row order inside
-// a tile and the reduction tree are fixed, so partials are deterministic.
+// block, then team-syncs.  Warps never wait for each other inside a phase:
+// each warp butterfly-reduces its share of a tile and parks it in shared
+// memory; after the last tile the block sums each tile's warp partials in
+// fixed warp order.  Row order, trees and orders are fixed, so the per-tile
+// partials are deterministic and independent of the grid size.
+constexpr int kWarps = kTPB / 32;
+
+__host__ __device__ constexpr size_t phase_smem_bytes(int64_t tiles_per_block) {
+  return size_t(tiles_per_block) * kWarps * kMaxRed * sizeof(double);
+}
+
 template <int NR, class Body>
 __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
-  __shared__ double sm[kTPB / 32][kMaxRed];
-  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) {
+  extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tl = 0;
+  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x, ++tl) {
     const int p = __ldg(T.tile_part + tile);
     const PartDev P = T.parts[p];  // by value: no aliasing with the vector stores
     const int64_t row0 = (tile - P.tile0) * kTile;
@@ -240,11 +287,21 @@ __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&&
       const int64_t i = row0 + m * kTPB + threadIdx.x;
       if (i < P.n) body(P, i, acc);
     }
-    block_sum<NR>(acc, sm);
-    if (threadIdx.x == 0) {
 #pragma unroll
-      for (int j = 0; j < NR; ++j) T.partials[tile * kMaxRed + j] = acc[j];
-    }
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) wsm[(tl * kWarps + warp) * kMaxRed + j] = acc[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < tl * NR; idx += kTPB) {
+    const int t = idx / NR, j = idx - t * NR;
+    double s = wsm[(t * kWarps) * kMaxRed + j];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsm[(t * kWarps + w) * kMaxRed + j]);
+    T.partials[(int64_t(blockIdx.x) + int64_t(t) * gridDim.x) * kMaxRed + j] = s;
   }
   team_sync<NR>(T, red);
 }
@@ -265,7 +322,7 @@ __device__ __forceinline__ bool team_failed(const TeamDev& T) {
 // p is double-buffered so phase A can read neighbours' p_old while writing p_new.
 // ---------------------------------------------------------------------------
 template <bool JAC>
-__global__ void __launch_bounds__(kTPB) team_cg_kernel(TeamDev T) {
+__global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
   // phase 0: x = 0, r = b, partial b.b (and r.z)
@@ -369,7 +426,7 @@ __global__ void __launch_bounds__(kTPB) team_cg_kernel(TeamDev T) {
 //  3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r
 // p and v are double-buffered.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTPB) team_bicgstab_kernel(TeamDev T) {
+__global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
   team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {

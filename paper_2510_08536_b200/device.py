@@ -180,6 +180,12 @@ class DevicePart:
     def sync(self):
         N.check(N.lrb_part_sync(self.h))
 
+    def stats(self):
+        out = np.zeros(4, np.int64)
+        N.check(N.lrb_part_stats(self.h, N.ptr(out)))
+        return dict(zip(("pinned_pieces", "pageable_pieces", "h2d_bytes", "scatters"),
+                        (int(v) for v in out)))
+
     def mark(self):
         N.check(N.lrb_part_mark(self.h))
 
@@ -230,7 +236,11 @@ class Team:
         if bs is not None:
             bs = [np.ascontiguousarray(b, dtype=np.float64) for b in bs]
             bptr = N.ptr_array([b.ctypes.data for b in bs])
-        xs = [np.empty(p.n, np.float64) for p in self.parts] if want_x else None
+        # solutions land in pinned host memory (torch's caching host allocator
+        # recycles the blocks); the ndarray keeps its tensor alive
+        torch = _torch()
+        xs = [torch.empty(max(p.n, 1), dtype=torch.float64, pin_memory=True).numpy()[:p.n]
+              for p in self.parts] if want_x else None
         xptr = N.ptr_array([x.ctypes.data for x in xs]) if want_x else None
         hist = np.zeros(max(hist_cap, 0), np.float64)
         rc = N.lrb_team_solve(self.h, N.METHODS[method], bptr, xptr, float(tol), int(max_iter),

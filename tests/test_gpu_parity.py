@@ -19,6 +19,16 @@ SMALL = [c for c in CASES if c not in ("c2",)]
 HIST_RTOL = 1e-10
 
 
+def history_ok(ours, ref, rtol=HIST_RTOL, floor=1e-12):
+    """Recurrence residuals within rtol relative; below the rounding floor
+    (tiny systems reach exact convergence, e.g. the 8-cell chain) both must
+    simply be negligible."""
+    n = min(len(ours), len(ref))
+    a, r = np.asarray(ours[:n]), np.asarray(ref[:n])
+    ok = (np.abs(a - r) <= rtol * r) | ((r < floor) & (a < floor))
+    return bool(ok.all()), n
+
+
 def ref_history(log, iterations, tol):
     """sqrt(rr)/|b| per iteration from the reference's allreduce log."""
     bb = log[0]
@@ -105,9 +115,8 @@ def test_cg_history_matches_reference(name):
         x0, rep = owners[0][f"cg_{s}"]
         assert abs(rep.iterations - int(it_ref)) <= 1, (s, rep.iterations, it_ref)
         assert rep.converged == bool(conv_ref)
-        n = min(len(ref), len(rep.history))
-        rel = np.abs(rep.history[:n] - ref[:n]) / ref[:n]
-        assert rel.max() <= HIST_RTOL, (s, rel.max())
+        ok, n = history_ok(rep.history, ref)
+        assert ok and n >= min(len(ref), rep.iterations) - 1, (s, rep.history, ref)
         # every owner reports the same team result
         for k, out in owners.items():
             assert out[f"cg_{s}"][1].iterations == rep.iterations
@@ -128,5 +137,4 @@ def test_pcg_matches_reference_cg(name):
         ref = ref_history(get(name, 0, f"cg_{s}_log"), it_ref, cfg["tol"])
         _, rep = owners[0][f"cg_{s}"]
         assert abs(rep.iterations - it_ref) <= 1
-        n = min(len(ref), len(rep.history))
-        assert (np.abs(rep.history[:n] - ref[:n]) / ref[:n]).max() <= HIST_RTOL
+        assert history_ok(rep.history, ref)[0]
