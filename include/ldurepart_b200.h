@@ -72,8 +72,9 @@ int lrb_plan_build_coo(int64_t total_cells, int64_t row_lo, int64_t row_hi, int6
                        const int64_t* seg_off, int32_t n_gpu, const int64_t* gpu_offsets,
                        lrb_plan** out);
 
-/* info[0..9] = n_rows, nnz_local, nnz_nonlocal, n_halo, n_buf, n_slices,
- *              sell_entries, max_row_len, n_seg, part_device_bytes */
+/* info[0..12] = n_rows, nnz_local, nnz_nonlocal, n_halo, n_buf, n_slices,
+ *               sell_entries, max_row_len, n_seg, part_device_bytes,
+ *               uniform (pattern) slices, n_patterns, entries in uniform slices */
 int lrb_plan_info(const lrb_plan* plan, int64_t* info);
 /* Reference DistributedCooMatrix patterns in CSR form (core.py:247-288):
  * loc_ptr/nl_ptr [n+1]; loc_col part-local; nl_col = index into halo_cols. */

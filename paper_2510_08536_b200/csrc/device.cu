@@ -50,7 +50,7 @@ static int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 
 // Arena layout of one part (all sections 256-byte aligned).
 struct Layout {
-  int64_t slice_ptr, col, src, dpos, hpart, hidx, val, recv, vec, total;
+  int64_t slice_ptr, slice_pat, pat_off, rmask, col, src, dpos, hpart, hidx, val, recv, vec, total;
   static constexpr int kVecs = 12;
 };
 
@@ -65,6 +65,9 @@ static Layout layout_of(const Plan& P) {
   const int64_t E = P.sell_entries();
   const int64_t h = int64_t(P.halo_cols.size());
   L.slice_ptr = take(8 * (P.n_slices + 1));
+  L.slice_pat = take(4 * P.n_slices);
+  L.pat_off = take(4 * int64_t(P.pat_off.size()));
+  L.rmask = take(2 * P.n);
   L.col = take(4 * E);
   L.src = take(4 * E);
   L.dpos = take(P.n);
@@ -87,7 +90,8 @@ using namespace lrb;
 struct lrb_part {
   int device = 0;
   PartDev d{};                      // device pointers (host copy)
-  std::vector<int64_t> seg_off, seg_rows, loc_ptr, nl_ptr, slice_ptr;
+  std::vector<int64_t> seg_off, seg_rows, slice_ptr;
+  std::vector<int32_t> loc_sell, nl_sell;  // SELL slot of each CSR entry (value mirror)
   int64_t nnz_l = 0, nnz_n = 0;
   cudaStream_t main = nullptr;
   std::vector<cudaStream_t> seg_stream;
@@ -170,6 +174,9 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   D.n_buf = P.n_buf;
   D.n_slices = P.n_slices;
   D.slice_ptr = reinterpret_cast<const int64_t*>(base + L.slice_ptr);
+  D.slice_pat = reinterpret_cast<const int32_t*>(base + L.slice_pat);
+  D.pat_off = reinterpret_cast<const int32_t*>(base + L.pat_off);
+  D.rmask = reinterpret_cast<const uint16_t*>(base + L.rmask);
   D.col = reinterpret_cast<const int32_t*>(base + L.col);
   D.src = reinterpret_cast<const int32_t*>(base + L.src);
   D.dpos = reinterpret_cast<const int8_t*>(base + L.dpos);
@@ -210,8 +217,8 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   LRB_CUDA(cudaEventCreate(&part->mark_b));
   part->seg_off = P.seg_off;
   part->seg_rows = P.seg_rows;
-  part->loc_ptr = P.loc_ptr;
-  part->nl_ptr = P.nl_ptr;
+  part->loc_sell = P.loc_sell;
+  part->nl_sell = P.nl_sell;
   part->slice_ptr = P.slice_ptr;
   part->nnz_l = int64_t(P.loc_col.size());
   part->nnz_n = int64_t(P.nl_col.size());
@@ -224,6 +231,13 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   LRB_CUDA(cudaMemsetAsync(dev_arena, 0, L.total, st));
   LRB_CUDA(cudaMemcpyAsync(base + L.slice_ptr, P.slice_ptr.data(), 8 * (P.n_slices + 1),
                            cudaMemcpyHostToDevice, st));
+  if (P.n_slices)
+    LRB_CUDA(cudaMemcpyAsync(base + L.slice_pat, P.slice_pat.data(), 4 * P.n_slices,
+                             cudaMemcpyHostToDevice, st));
+  LRB_CUDA(cudaMemcpyAsync(base + L.pat_off, P.pat_off.data(), 4 * P.pat_off.size(),
+                           cudaMemcpyHostToDevice, st));
+  if (P.n)
+    LRB_CUDA(cudaMemcpyAsync(base + L.rmask, P.rmask.data(), 2 * P.n, cudaMemcpyHostToDevice, st));
   if (E) {
     LRB_CUDA(cudaMemcpyAsync(base + L.col, P.sell_col.data(), 4 * E, cudaMemcpyHostToDevice, st));
     LRB_CUDA(cudaMemcpyAsync(base + L.src, P.sell_src.data(), 4 * E, cudaMemcpyHostToDevice, st));
@@ -468,14 +482,10 @@ int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_va
   std::vector<double> sell(E);
   if (E) LRB_CUDA(cudaMemcpyAsync(sell.data(), part->d.val, 8 * E, cudaMemcpyDeviceToHost, part->main));
   LRB_CUDA(cudaStreamSynchronize(part->main));
-  for (int64_t r = 0; r < part->d.n; ++r) {
-    const int64_t base = part->slice_ptr[r / kSlice] + (r % kSlice);
-    int64_t k = 0;
-    for (int64_t j = part->loc_ptr[r]; j < part->loc_ptr[r + 1]; ++j, ++k)
-      if (local_vals) local_vals[j] = sell[base + k * kSlice];
-    for (int64_t j = part->nl_ptr[r]; j < part->nl_ptr[r + 1]; ++j, ++k)
-      if (nonlocal_vals) nonlocal_vals[j] = sell[base + k * kSlice];
-  }
+  if (local_vals)
+    for (size_t j = 0; j < part->loc_sell.size(); ++j) local_vals[j] = sell[part->loc_sell[j]];
+  if (nonlocal_vals)
+    for (size_t j = 0; j < part->nl_sell.size(); ++j) nonlocal_vals[j] = sell[part->nl_sell[j]];
   return LRB_OK;
 }
 
@@ -536,6 +546,8 @@ struct TeamDevice {
   int rank = 0;         // device rank in the team
   std::vector<int> parts;
   int64_t n_tiles = 0;
+  bool inl = false;               // local part descriptors in the kernel parameter
+  const void* fn[3] = {nullptr, nullptr, nullptr};
   int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
   size_t smem[3] = {0, 0, 0};
   cudaStream_t stream = nullptr;  // main stream of the first local part
@@ -569,10 +581,20 @@ static int team_hist_capacity(TeamDevice& D, int cap) {
   return LRB_OK;
 }
 
+static const void* solve_kernel(int method, bool inl) {
+  switch (method) {
+    case LRB_METHOD_CG:
+      return inl ? (const void*)team_cg_kernel<false, true> : (const void*)team_cg_kernel<false, false>;
+    case LRB_METHOD_PCG:
+      return inl ? (const void*)team_cg_kernel<true, true> : (const void*)team_cg_kernel<true, false>;
+    default:
+      return inl ? (const void*)team_bicgstab_kernel<true> : (const void*)team_bicgstab_kernel<false>;
+  }
+}
+
 // Largest co-resident grid (one wave) for a persistent team kernel; the
 // dynamic shared memory holds the warp partials of the block's tiles.
-template <class K>
-static int max_grid(K kernel, int device, int64_t n_tiles, int n_share, size_t* smem) {
+static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t* smem) {
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   const int64_t tiles = std::max<int64_t>(n_tiles, 1);
@@ -719,9 +741,13 @@ int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* d
     LRB_CUDA(cudaEventCreate(&D.t0));
     LRB_CUDA(cudaEventCreate(&D.t1));
     const int n_share = share[D.device];
-    D.grid[0] = max_grid(team_cg_kernel<false>, D.device, D.n_tiles, n_share, &D.smem[0]);
-    D.grid[1] = max_grid(team_cg_kernel<true>, D.device, D.n_tiles, n_share, &D.smem[1]);
-    D.grid[2] = max_grid(team_bicgstab_kernel, D.device, D.n_tiles, n_share, &D.smem[2]);
+    D.inl = int(D.parts.size()) <= kInlineParts;
+    if (D.inl)
+      for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
+    for (int m = 0; m < 3; ++m) D.fn[m] = solve_kernel(m, D.inl);
+    D.grid[0] = max_grid(D.fn[0], D.device, D.n_tiles, n_share, &D.smem[0]);
+    D.grid[1] = max_grid(D.fn[1], D.device, D.n_tiles, n_share, &D.smem[1]);
+    D.grid[2] = max_grid(D.fn[2], D.device, D.n_tiles, n_share, &D.smem[2]);
     for (int m = 0; m < 3; ++m)
       if (D.grid[m] <= 0) {
         set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
@@ -878,9 +904,7 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
   for (auto& D : team->devs) {
     DeviceGuard g(D.device);
     void* args[] = {&D.host};
-    void* fn = method == LRB_METHOD_CG    ? (void*)team_cg_kernel<false>
-               : method == LRB_METHOD_PCG ? (void*)team_cg_kernel<true>
-                                          : (void*)team_bicgstab_kernel;
+    const void* fn = D.fn[method];
     const int grid = D.grid[method];
     const size_t smem = D.smem[method];
     LRB_CUDA(cudaEventRecord(D.t0, D.stream));

@@ -60,14 +60,16 @@ __device__ __forceinline__ RowRef row_ref(const PartDev& P, int64_t i) {
 // ~3*kChunk independent loads in flight per thread instead of a dependent
 // col -> x -> add chain per entry.
 #ifndef LRB_CHUNK
-#define LRB_CHUNK 8
+#define LRB_CHUNK 4
 #endif
 constexpr int kChunk = LRB_CHUNK;
 
 // Minimum resident blocks per SM requested from ptxas for the persistent
-// solvers (register cap 65536 / (256 * LRB_MINB)).
+// solvers (register cap 65536 / (256 * LRB_MINB)).  Measured on B200 at C3
+// (tools/variants.sh): occupancy beats spill-free code — MINB 6 / chunk 4
+// (40 regs, 75% occupancy) runs the PCG solve 2x faster than MINB 2 (111 regs).
 #ifndef LRB_MINB
-#define LRB_MINB 2
+#define LRB_MINB 6
 #endif
 
 template <class F>
@@ -75,13 +77,22 @@ __device__ __forceinline__ double row_spmv(const PartDev& P, const PartDev* __re
                                            int64_t i, F&& f) {
   const RowRef rr = row_ref(P, i);
   const int n = int(P.n);
+  const int pid = __ldg(P.slice_pat + (i >> 5));   // warp-uniform
+  const int32_t* poff = P.pat_off + pid * kPatW;
   double acc = 0.0;
   for (int k0 = 0; k0 < rr.w; k0 += kChunk) {
     int c[kChunk];
     double a[kChunk], xv[kChunk];
+    if (pid >= 0) {
+      const unsigned msk = __ldg(P.rmask + i);
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u)
-      c[u] = (k0 + u < rr.w) ? __ldg(P.col + rr.base + int64_t(k0 + u) * kSlice) : -1;
+      for (int u = 0; u < kChunk; ++u)
+        c[u] = (k0 + u < rr.w && ((msk >> (k0 + u)) & 1u)) ? int(i) + __ldg(poff + k0 + u) : -1;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        c[u] = (k0 + u < rr.w) ? __ldg(P.col + rr.base + int64_t(k0 + u) * kSlice) : -1;
+    }
 #pragma unroll
     for (int u = 0; u < kChunk; ++u) {
       a[u] = 0.0;
@@ -198,10 +209,25 @@ __device__ void team_sync(const TeamDev& T, double* red) {
       double acc[NR];
 #pragma unroll
       for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-      for (int64_t t = threadIdx.x; t < P.ntiles; t += kTPB) {
-        const double* src = T.partials + (P.tile0 + t) * kMaxRed;
+      // thread t sums tiles t, t+kTPB, ... in order; 8 tiles' loads in flight
+      // (L2, bypassing L1) before the ordered adds
+      const double2* base = reinterpret_cast<const double2*>(T.partials + P.tile0 * kMaxRed);
+      for (int64_t t0 = threadIdx.x; t0 < P.ntiles; t0 += 8 * kTPB) {
+        double2 v[8][(NR + 1) / 2];
 #pragma unroll
-        for (int j = 0; j < NR; ++j) acc[j] = __dadd_rn(acc[j], vload(src + j));
+        for (int u = 0; u < 8; ++u) {
+          const int64_t t = t0 + int64_t(u) * kTPB;
+#pragma unroll
+          for (int h = 0; h < (NR + 1) / 2; ++h)
+            v[u][h] = t < P.ntiles ? __ldcg(base + t * (kMaxRed / 2) + h) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (t0 + int64_t(u) * kTPB >= P.ntiles) break;
+#pragma unroll
+          for (int j = 0; j < NR; ++j)
+            acc[j] = __dadd_rn(acc[j], (j & 1) ? v[u][j / 2].y : v[u][j / 2].x);
+        }
       }
       block_sum<NR>(acc, sm);
       if (threadIdx.x == 0) {
@@ -271,21 +297,32 @@ __host__ __device__ constexpr size_t phase_smem_bytes(int64_t tiles_per_block) {
 }
 
 template <int NR, class Body>
+__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[NR],
+                                          Body&& body) {
+  const int64_t row0 = (tile - P.tile0) * kTile;
+#pragma unroll
+  for (int m = 0; m < kRPT; ++m) {
+    const int64_t i = row0 + m * kTPB + threadIdx.x;
+    if (i < P.n) body(P, i, acc);
+  }
+}
+
+// INL: local part descriptors come from the kernel parameter (T.lp).
+template <int NR, bool INL, class Body>
 __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
   extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tl = 0;
   for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x, ++tl) {
     const int p = __ldg(T.tile_part + tile);
-    const PartDev P = T.parts[p];  // by value: no aliasing with the vector stores
-    const int64_t row0 = (tile - P.tile0) * kTile;
     double acc[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-#pragma unroll
-    for (int m = 0; m < kRPT; ++m) {
-      const int64_t i = row0 + m * kTPB + threadIdx.x;
-      if (i < P.n) body(P, i, acc);
+    if constexpr (INL) {
+      tile_rows<NR>(T.lp[p - T.part_begin], tile, acc, body);
+    } else {
+      const PartDev P = T.parts[p];  // by value: no aliasing with the vector stores
+      tile_rows<NR>(P, tile, acc, body);
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j)
@@ -316,22 +353,27 @@ __device__ __forceinline__ bool team_failed(const TeamDev& T) {
 // Per iteration two fused phases (+ the true-residual phase every 10th
 // iteration or when the recurrence residual meets tol):
 //  A: p_new = z + beta*p_old computed on the fly for every row and neighbour
-//     (z = r, or dinv*r for PCG), q = A p_new, store p_new and q, partial p.q
-//  B: x += step*p, r -= step*q, partial r.r (and r.z for PCG)
+//     (z = r for CG; for PCG z = dinv*r was stored by phase B, so a neighbour
+//     costs two loads), q = A p_new, store p_new and q, partial p.q
+//  B: x += step*p, r -= step*q, partial r.r (PCG: z = dinv*r stored, r.z)
 //  C: y = A x, partial |b - y|^2
 // p is double-buffered so phase A can read neighbours' p_old while writing p_new.
 // ---------------------------------------------------------------------------
-template <bool JAC>
-__global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
+template <bool JAC, bool INL>
+__global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
   // phase 0: x = 0, r = b, partial b.b (and r.z)
-  team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+  team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
     const double b = P.b[i];
     P.x[i] = 0.0;
     P.r[i] = b;
     acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
-    if (JAC) acc[1] = __dadd_rn(acc[1], __dmul_rn(b, __dmul_rn(P.dinv[i], b)));
+    if (JAC) {
+      const double z = __dmul_rn(P.dinv[i], b);
+      P.s[i] = z;  // z = dinv * r lives in s for Jacobi-PCG
+      acc[1] = __dadd_rn(acc[1], __dmul_rn(b, z));
+    }
   });
   const double bb = red[0];
   SolveOut* out = T.out;
@@ -353,10 +395,9 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
   int it = 0;
   for (it = 1; it <= T.max_iter; ++it) {
     // ---- phase A: p_new, q = A p_new, p.q
-    team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+    team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
       auto pnew = [&](const PartDev& Q, int64_t j) -> double {
-        const double r = Q.r[j];
-        const double z = JAC ? __dmul_rn(Q.dinv[j], r) : r;
+        const double z = JAC ? Q.s[j] : Q.r[j];
         if (first) return z;
         const double po = pa ? Q.p1[j] : Q.p0[j];
         return __dadd_rn(z, __dmul_rn(beta, po));
@@ -376,14 +417,18 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
     const double step = rho / pq;
     pa ^= 1;  // p_new is now p_old for the elementwise phase and the next iteration
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
-    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       const double p = (pa ? P.p1 : P.p0)[i];
       const double x = __dadd_rn(P.x[i], __dmul_rn(step, p));
       const double r = __dsub_rn(P.r[i], __dmul_rn(step, P.q[i]));
       P.x[i] = x;
       P.r[i] = r;
       acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
-      if (JAC) acc[1] = __dadd_rn(acc[1], __dmul_rn(r, __dmul_rn(P.dinv[i], r)));
+      if (JAC) {
+        const double z = __dmul_rn(P.dinv[i], r);
+        P.s[i] = z;
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
+      }
     });
     if (team_failed(T)) break;
     const double rr_new = red[0];
@@ -392,7 +437,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
     if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
     if (rec <= T.tol || it % 10 == 0) {
       // ---- phase C: true residual |b - A x|
-      team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+      team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
         const double ax =
             row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
         const double d = __dsub_rn(P.b[i], ax);
@@ -426,10 +471,11 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(TeamDev T) {
 //  3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r
 // p and v are double-buffered.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T) {
+template <bool INL>
+__global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
-  team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+  team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
     const double b = P.b[i];
     P.x[i] = 0.0;
     P.r[i] = b;
@@ -457,7 +503,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T
     const bool first = (it == 1);
     if (!first) beta = __dmul_rn(rho / rho_prev, alpha / omega);
     // ---- phase 1
-    team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+    team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
       auto pnew = [&](const PartDev& Q, int64_t j) -> double {
         const double r = Q.r[j];
         if (first) return r;
@@ -480,7 +526,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T
     }
     alpha = rho / rv;
     // ---- phase 2
-    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       auto sval = [&](const PartDev& Q, int64_t j) -> double {
         const double v = pa ? Q.v1[j] : Q.v0[j];
         return __dsub_rn(Q.r[j], __dmul_rn(alpha, v));
@@ -495,7 +541,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T
     if (team_failed(T)) break;
     omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
     // ---- phase 3
-    team_phase<2>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       const double p = (pa ? P.p1 : P.p0)[i];
       const double s = P.s[i];
       const double x = __dadd_rn(__dadd_rn(P.x[i], __dmul_rn(alpha, p)), __dmul_rn(omega, s));
@@ -512,7 +558,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(TeamDev T
     const double rec = sqrt(rr) / bnorm;
     if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
     if (rec <= T.tol || it % 10 == 0) {
-      team_phase<1>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+      team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
         const double ax =
             row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
         const double d = __dsub_rn(P.b[i], ax);

@@ -25,12 +25,24 @@ namespace lrb {
 // ---------------------------------------------------------------------------
 constexpr int kSlice = 32;
 
+// Pattern dictionary: a full slice whose rows' column offsets (col - row) fit
+// in at most kPatW distinct values is laid out on the sorted union of those
+// offsets; its columns are not streamed from HBM but rebuilt as
+// row + pat_off[pid][slot] for the slots set in the row's rmask.  On the
+// cavity stencil nearly every slice qualifies, which removes 4 of the 12
+// matrix bytes per entry and the dependent col -> x load chain.
+constexpr int kPatW = 16;      // widest row a pattern may describe
+constexpr int kMaxPat = 1024;  // dictionary size
+
 struct PartDev {
   int64_t n;          // owned rows
   int64_t n_halo;
   int64_t n_buf;      // receive-buffer length (= nnz, bijection)
   int64_t n_slices;
   const int64_t* slice_ptr;   // [n_slices+1] entry offsets
+  const int32_t* slice_pat;   // [n_slices] pattern id or -1
+  const int32_t* pat_off;     // [n_pat * kPatW]
+  const uint16_t* rmask;      // [n] occupied pattern slots of each row
   const int32_t* col;         // [E]
   const int32_t* src;         // [E] scatter inverse (buffer position or -1)
   const int8_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
@@ -65,7 +77,12 @@ struct SolveOut {
   double bnorm;
 };
 
-// Per-device team state, in device memory.
+// Descriptors of up to kInlineParts local parts ride in the kernel parameter
+// space (__grid_constant__): their fields are warp-uniform constant-bank
+// operands, rematerialised instead of pinned in registers.
+constexpr int kInlineParts = 8;
+
+// Per-device team state, passed by value as the kernel parameter.
 struct TeamDev {
   int32_t n_parts;          // team-wide
   int32_t dev_rank;         // this device's rank in the team
@@ -92,6 +109,7 @@ struct TeamDev {
   int32_t max_iter;
   double tol;
   long long timeout_ns;
+  PartDev lp[kInlineParts];  // local parts [part_begin, part_end) when they fit
 };
 
 // ---------------------------------------------------------------------------
@@ -111,6 +129,11 @@ struct Plan {
   std::vector<int64_t> slice_ptr;
   std::vector<int32_t> sell_col, sell_src;
   std::vector<int8_t> dpos;
+  std::vector<int32_t> slice_pat;           // [n_slices]
+  std::vector<int32_t> pat_off;             // [n_pat * kPatW]
+  std::vector<uint16_t> rmask;              // [n] occupied slots of a pattern row
+  std::vector<int32_t> loc_sell, nl_sell;   // SELL slot of every CSR entry
+  int64_t n_pat() const { return int64_t(pat_off.size()) / kPatW; }
   int64_t sell_entries() const { return slice_ptr.empty() ? 0 : slice_ptr.back(); }
 };
 

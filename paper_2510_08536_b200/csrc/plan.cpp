@@ -15,7 +15,9 @@
 #include <atomic>
 #include <cstring>
 #include <functional>
+#include <iterator>
 #include <limits>
+#include <map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -312,16 +314,64 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
     if (ok) P.seg_rows = rows;
   }
 
-  // 6) SELL-32 layout: local entries then non-local entries per row
+  // 6) SELL-32 layout with a pattern dictionary (lrb_internal.h).  A row's
+  //    entries are (col - row) offsets in ascending order — local columns,
+  //    then halo columns encoded n + slot, which are always larger — so
+  //    laying a slice out on the sorted union of its rows' offsets keeps
+  //    every row in the reference's entry order; rows lacking an offset get a
+  //    hole (src -1, masked off).
   P.n_slices = (n + kSlice - 1) / kSlice;
-  P.slice_ptr.assign(P.n_slices + 1, 0);
-  for (int64_t s = 0; s < P.n_slices; ++s) {
-    int64_t w = 0;
-    for (int64_t r = s * kSlice; r < std::min<int64_t>(n, (s + 1) * kSlice); ++r)
-      w = std::max<int64_t>(w, (P.loc_ptr[r + 1] - P.loc_ptr[r]) + (P.nl_ptr[r + 1] - P.nl_ptr[r]));
-    P.slice_ptr[s + 1] = P.slice_ptr[s] + w * kSlice;
+  const int64_t ns = P.n_slices;
+  std::vector<std::vector<int32_t>> uni(ns);
+  std::vector<int32_t> maxlen(ns, 0);
+  auto row_off = [&](int64_t r, std::vector<int32_t>& out) {
+    out.clear();
+    for (int64_t i = P.loc_ptr[r]; i < P.loc_ptr[r + 1]; ++i) out.push_back(int32_t(P.loc_col[i] - r));
+    for (int64_t i = P.nl_ptr[r]; i < P.nl_ptr[r + 1]; ++i)
+      out.push_back(int32_t(n + P.nl_col[i] - r));
+  };
+  parallel_for(ns, n_threads, [&](int64_t s0, int64_t s1) {
+    std::vector<int32_t> ro, merged;
+    for (int64_t s = s0; s < s1; ++s) {
+      std::vector<int32_t>& u = uni[s];
+      u.clear();
+      bool ok = (s + 1) * kSlice <= n;  // only full slices
+      for (int64_t r = s * kSlice; r < std::min<int64_t>(n, (s + 1) * kSlice); ++r) {
+        row_off(r, ro);
+        maxlen[s] = std::max<int32_t>(maxlen[s], int32_t(ro.size()));
+        if (!ok) continue;
+        merged.clear();
+        std::set_union(u.begin(), u.end(), ro.begin(), ro.end(), std::back_inserter(merged));
+        u.swap(merged);
+        if (int64_t(u.size()) > kPatW) ok = false;
+      }
+      if (!ok) u.clear();
+    }
+  });
+  P.slice_ptr.assign(ns + 1, 0);
+  P.slice_pat.assign(ns, -1);
+  P.pat_off.clear();
+  {
+    std::map<std::vector<int32_t>, int32_t> ids;
+    for (int64_t s = 0; s < ns; ++s) {
+      int64_t w = maxlen[s];
+      if (!uni[s].empty()) {
+        auto it = ids.find(uni[s]);
+        if (it == ids.end() && int64_t(ids.size()) < kMaxPat) {
+          it = ids.emplace(uni[s], int32_t(ids.size())).first;
+          P.pat_off.resize(P.pat_off.size() + kPatW, 0);
+          std::copy(uni[s].begin(), uni[s].end(), P.pat_off.end() - kPatW);
+        }
+        if (it != ids.end()) {
+          P.slice_pat[s] = it->second;
+          w = int64_t(uni[s].size());
+        }
+      }
+      P.slice_ptr[s + 1] = P.slice_ptr[s] + w * kSlice;
+    }
+    if (P.pat_off.empty()) P.pat_off.assign(kPatW, 0);  // keep one (unused) row
   }
-  const int64_t E = P.slice_ptr[P.n_slices];
+  const int64_t E = P.slice_ptr[ns];
   if (E >= (int64_t(1) << 31) - 1) {
     set_error("part too large for 32-bit device indices");
     return LRB_EVALUE;
@@ -329,19 +379,38 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
   P.sell_col.assign(E, -1);
   P.sell_src.assign(E, -1);
   P.dpos.assign(n, -1);
+  P.rmask.assign(n, 0);
+  P.loc_sell.assign(nnz_l, 0);
+  P.nl_sell.assign(nnz_n, 0);
   parallel_for(n, n_threads, [&](int64_t r0, int64_t r1) {
+    std::vector<int32_t> ro;
     for (int64_t r = r0; r < r1; ++r) {
-      int64_t base = P.slice_ptr[r / kSlice] + (r % kSlice);
-      int64_t k = 0;
-      for (int64_t i = P.loc_ptr[r]; i < P.loc_ptr[r + 1]; ++i, ++k) {
-        P.sell_col[base + k * kSlice] = P.loc_col[i];
-        P.sell_src[base + k * kSlice] = P.loc_src[i];
-        if (P.loc_col[i] == r && k < 127) P.dpos[r] = int8_t(k);
+      const int64_t s = r / kSlice;
+      const int64_t base = P.slice_ptr[s] + (r % kSlice);
+      const int pid = P.slice_pat[s];
+      const std::vector<int32_t>& u = uni[s];
+      row_off(r, ro);
+      uint32_t mask = 0;
+      for (int64_t k = 0; k < int64_t(ro.size()); ++k) {
+        int64_t slot = k;
+        if (pid >= 0) slot = std::lower_bound(u.begin(), u.end(), ro[k]) - u.begin();
+        const int64_t e = base + slot * kSlice;
+        const int64_t nloc = P.loc_ptr[r + 1] - P.loc_ptr[r];
+        if (k < nloc) {
+          const int64_t j = P.loc_ptr[r] + k;
+          P.sell_col[e] = P.loc_col[j];
+          P.sell_src[e] = P.loc_src[j];
+          P.loc_sell[j] = int32_t(e);
+          if (P.loc_col[j] == r && slot < 127) P.dpos[r] = int8_t(slot);
+        } else {
+          const int64_t j = P.nl_ptr[r] + (k - nloc);
+          P.sell_col[e] = int32_t(n + P.nl_col[j]);
+          P.sell_src[e] = P.nl_src[j];
+          P.nl_sell[j] = int32_t(e);
+        }
+        mask |= 1u << (slot & 31);
       }
-      for (int64_t i = P.nl_ptr[r]; i < P.nl_ptr[r + 1]; ++i, ++k) {
-        P.sell_col[base + k * kSlice] = int32_t(n + P.nl_col[i]);
-        P.sell_src[base + k * kSlice] = P.nl_src[i];
-      }
+      if (pid >= 0) P.rmask[r] = uint16_t(mask);
     }
   });
   return LRB_OK;
@@ -447,6 +516,15 @@ extern "C" int lrb_plan_info(const lrb_plan* plan, int64_t* info) {
   info[7] = maxlen;
   info[8] = int64_t(P.seg_off.size()) - 1;
   info[9] = lrb::part_device_bytes(P);
+  int64_t uniform = 0, uniform_entries = 0;
+  for (int64_t s = 0; s < P.n_slices; ++s)
+    if (P.slice_pat[s] >= 0) {
+      ++uniform;
+      uniform_entries += P.slice_ptr[s + 1] - P.slice_ptr[s];
+    }
+  info[10] = uniform;
+  info[11] = P.n_pat();
+  info[12] = uniform_entries;
   return LRB_OK;
 }
 

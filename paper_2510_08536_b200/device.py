@@ -30,10 +30,11 @@ class Plan:
 
     def __init__(self, handle):
         self.h = handle
-        info = np.zeros(10, dtype=np.int64)
+        info = np.zeros(13, dtype=np.int64)
         N.check(N.lrb_plan_info(self.h, N.ptr(info)))
         (self.n, self.nnz_local, self.nnz_nonlocal, self.n_halo, self.n_buf, self.n_slices,
-         self.sell_entries, self.max_row_len, self.n_seg, self.device_bytes) = (int(v) for v in info)
+         self.sell_entries, self.max_row_len, self.n_seg, self.device_bytes,
+         self.uniform_slices, self.n_patterns, self.uniform_entries) = (int(v) for v in info)
         self._csr = None
 
     @classmethod
