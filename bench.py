@@ -283,7 +283,95 @@ def run_ours(args):
 
 
 def run_ours_multi(args):
-    raise SystemExit("multi-GPU bench path not built yet")
+    """torchrun: one process per GPU; each hosts its part's rpg source ranks as
+    threads; the solve kernels of all GPUs synchronise through NVLink peer
+    memory (CUDA IPC).  gloo carries only create-time blobs and the
+    max-over-ranks of the timings."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_08536_b200 import _native
+    from paper_2510_08536_b200.dist import DistributedOwner, ProcessLayout, max_over_ranks
+
+    rank, world, local_rank = dist_env()
+    dist.init_process_group("gloo")
+    torch.cuda.set_device(local_rank)
+    N, _, method_default, desc = WORKLOADS[args.workload]
+    method = args.method or method_default
+    n_gpu = world
+    n_cpu = args.rpg * n_gpu
+    alpha = args.rpg
+    t0 = time.monotonic()
+    import paper_2510_08536_b200 as lrb
+    parts_all = lrb.decompose_slab(lrb.StructuredGrid(N, N, N), n_cpu)
+    layout = ProcessLayout([p.n_cells for p in parts_all], alpha, world, rank)
+    del parts_all
+    prob = Problem(N, n_cpu, layout.cpu_ranks)
+    owner = DistributedOwner(layout, {r: prob.base[r] for r in layout.cpu_ranks})
+    dist.barrier()
+    create_s = max_over_ranks(time.monotonic() - t0)
+    b = [Problem._pin(torch, np.ones(p.n)) for p in owner.parts]
+    n_steps = args.warmup + args.steps
+    steps = list(range(2, 2 + n_steps))
+    rec = {"e2e_ms": [], "wall_ms": [], "value_ms": [], "scatter_ms": [], "kernel_ms": [],
+           "checks": [], "value_iters": [], "launches": 0, "create_s": create_s}
+    sampler = ClockSampler(local_rank)
+    part = owner.parts[0]
+    for i, step in enumerate(steps):
+        live = {r: prob.produce(r, step) for r in layout.cpu_ranks}
+        torch.cuda.synchronize()
+        dist.barrier()
+        if i == args.warmup:
+            sampler.__enter__()
+            l0 = _native.lrb_launch_count()
+        part.mark()
+        tw = time.perf_counter()
+        owner.update(live, args.mode)
+        xs, rep, _ = owner.solve(method, b, TOL, MAX_ITER)
+        part.mark()
+        wall = (time.perf_counter() - tw) * 1e3
+        torch.cuda.synchronize()
+        e2e = max_over_ranks(part.elapsed_ms())
+        wall = max_over_ranks(wall)
+        if i >= args.warmup:
+            rec["e2e_ms"].append(e2e)
+            rec["wall_ms"].append(wall)
+    rec["launches"] = _native.lrb_launch_count() - l0
+    dist.barrier()
+    sampler.__exit__()
+    for i, step in enumerate(steps):
+        owner.update({r: prob.produce(r, step) for r in layout.cpu_ranks}, "direct")
+        for p in owner.parts:
+            p.sync()
+        dist.barrier()
+        part.mark()
+        for p in owner.parts:
+            p.apply_scatter()
+        part.mark()
+        _, rep, hist = owner.team.solve(method, None, TOL, MAX_ITER, want_x=False,
+                                        hist_cap=MAX_ITER)
+        t_sc = max_over_ranks(part.elapsed_ms())
+        kms = max_over_ranks(rep.device_ms)
+        if i >= args.warmup:
+            rec["scatter_ms"].append(t_sc)
+            rec["kernel_ms"].append(kms)
+            rec["value_ms"].append(t_sc + kms)
+            rec["checks"].append(n_checks(hist, rep.iterations, TOL))
+            rec["value_iters"].append(rep.iterations)
+    p0 = owner.plans[0]
+    # roofline on the max-loaded GPU: the largest part
+    sizes = max_over_ranks(float(p0.n))
+    rec["plan"] = (p0.n, p0.nnz_local + p0.nnz_nonlocal, p0.n_halo, p0.n_buf)
+    rec["e2e_update_wall_ms"] = [0.0]
+    rec["e2e_solve_wall_ms"] = [0.0]
+    rec["e2e_solve_kernel_ms"] = [0.0]
+    line = finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha), N,
+                       n_cpu, alpha, sampler)
+    line["config"]["max_part_rows"] = int(sizes)
+    line["config"]["parallelism"] = f"{n_gpu} GPU parts, NVLink peer-memory halo + reductions"
+    dist.barrier()
+    dist.destroy_process_group()
+    return line if rank == 0 else None
 
 
 def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
@@ -331,7 +419,10 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
             with open(prof) as fh:
                 t = json.load(fh).get(args.workload)
             if t:
-                line["roofline"]["traffic"] = t.get("dram_bytes_per_launch")
+                # ncu DRAM bytes per algorithmic byte of the solve kernel, applied
+                # to this run's launches (same kernel, same config)
+                line["roofline"]["traffic"] = int(t["dram_bytes_per_alg_byte"] *
+                                                  line["roofline"]["alg_bytes_per_launch"])
                 line["roofline"]["traffic_note"] = t.get("note")
         except Exception:  # noqa: BLE001
             pass
@@ -341,7 +432,7 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference algorithm (oracle port) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_baseline(args, iters_per_step=None):
+def cpu_baseline(args, iters_per_step=None, full_warmup=False):
     from oracle import cavity as ocav
     from oracle import krylov
     from oracle.pipeline import OraclePipeline
@@ -357,7 +448,9 @@ def cpu_baseline(args, iters_per_step=None):
     t_create = time.monotonic() - t0
     table = iters_per_step or _iteration_table(N, n_cpu, alpha)
     samples = []
-    steps = list(range(2, 2 + args.warmup + args.steps))
+    timed = list(range(2 + args.warmup, 2 + args.warmup + args.steps))
+    n_warm = args.warmup if full_warmup else 1
+    steps = list(range(timed[0] - n_warm, timed[0])) + timed
     k_iter = 3
     for i, step in enumerate(steps):
         ps = [ocav.perturb(p, step) for p in probs]
@@ -380,7 +473,7 @@ def cpu_baseline(args, iters_per_step=None):
             ts = time.perf_counter()
             krylov.cg(S, bs, TOL, MAX_ITER, jacobi=(method_default == "pcg"))
             ms = (t_up + time.perf_counter() - ts) * 1e3
-        if i >= args.warmup:
+        if i >= n_warm:
             samples.append(ms)
         if time.monotonic() - t0 > args.cpu_budget_s and len(samples) >= 1:
             break
@@ -410,7 +503,8 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    base = cpu_baseline(args)
+    args.cpu_budget_s = max(args.cpu_budget_s, 240.0)
+    base = cpu_baseline(args, full_warmup=True)
     N, _, method_default, desc = WORKLOADS[args.workload]
     n_cpu = args.rpg * args.gpus
     return {

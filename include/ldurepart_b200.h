@@ -158,6 +158,22 @@ int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* d
                        lrb_team** out);
 void lrb_team_destroy(lrb_team* team);
 
+/* Teams spanning processes (one process per GPU, e.g. torchrun): the caller
+ * exchanges opaque blobs (e.g. torch.distributed all_gather) — no NCCL on
+ * the data path; halo values and partial dot products move by NVLink peer
+ * loads/stores from inside the solve kernels.
+ *  1. every process: lrb_part_export(part, blob) for its part(s);
+ *  2. all-gather the part blobs in GPU-rank order;
+ *  3. lrb_team_create_ipc(...) opens the peers' arenas and returns this
+ *     device's team-workspace blob;
+ *  4. all-gather the team blobs; lrb_team_connect_ipc(team, blobs). */
+#define LRB_BLOB_BYTES 512
+int lrb_part_export(const lrb_part* part, void* blob);
+int lrb_team_create_ipc(int32_t n_parts, int32_t part_begin, int32_t n_local,
+                        lrb_part* const* local_parts, const void* part_blobs /* n_parts x 512 */,
+                        int32_t dev_rank, int32_t n_dev, lrb_team** out, void* team_blob);
+int lrb_team_connect_ipc(lrb_team* team, const void* team_blobs /* n_dev x 512 */);
+
 /* Distributed SpMV y = A x (solver.py:80-97): x_host/y_host per part. */
 int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host);
 

@@ -89,6 +89,11 @@ lrb_team_create = _sig("lrb_team_create", C.c_int, I32, P, C.POINTER(P))
 lrb_team_create_ex = _sig("lrb_team_create_ex", C.c_int, I32, P, P, C.POINTER(P))
 lrb_team_destroy = _sig("lrb_team_destroy", None, P)
 lrb_team_spmv = _sig("lrb_team_spmv", C.c_int, P, P, P)
+BLOB_BYTES = 512
+lrb_part_export = _sig("lrb_part_export", C.c_int, P, P)
+lrb_team_create_ipc = _sig("lrb_team_create_ipc", C.c_int, I32, I32, I32, P, P, I32, I32,
+                           C.POINTER(P), P)
+lrb_team_connect_ipc = _sig("lrb_team_connect_ipc", C.c_int, P, P)
 lrb_team_solve = _sig("lrb_team_solve", C.c_int, P, I32, P, P, D, I32, C.POINTER(Report), P, I32)
 
 EXPORTED = [
@@ -99,7 +104,8 @@ EXPORTED = [
     "lrb_stage_segment", "lrb_apply_scatter", "lrb_part_fill", "lrb_part_read_buffer",
     "lrb_part_read_values", "lrb_part_join", "lrb_part_sync", "lrb_part_stats", "lrb_part_mark",
     "lrb_part_elapsed_ms", "lrb_team_create", "lrb_team_create_ex", "lrb_team_destroy",
-    "lrb_team_spmv", "lrb_team_solve",
+    "lrb_team_spmv", "lrb_team_solve", "lrb_part_export", "lrb_team_create_ipc",
+    "lrb_team_connect_ipc",
 ]
 
 

@@ -2,6 +2,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a (see build.py).
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <atomic>
@@ -547,6 +548,8 @@ struct TeamDevice {
   std::vector<int> parts;
   int64_t n_tiles = 0;
   bool inl = false;               // local part descriptors in the kernel parameter
+  bool cooperative = true;        // whole device to one team kernel
+  size_t ws_bytes = 0;
   const void* fn[3] = {nullptr, nullptr, nullptr};
   int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
   size_t smem[3] = {0, 0, 0};
@@ -563,11 +566,111 @@ struct TeamDevice {
 }  // namespace lrb
 
 struct lrb_team {
-  std::vector<lrb_part*> parts;
+  std::vector<lrb_part*> parts;     // local parts by team part index (nullptr: remote)
   std::vector<lrb::TeamDevice> devs;
   std::vector<int> dev_of_part;
+  std::vector<void*> ipc_opened;    // peer allocations opened via CUDA IPC
+  int ipc_dev = -1;
   std::mutex mu;
 };
+
+namespace lrb {
+
+static const void* solve_kernel(int method, bool inl);
+static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t* smem);
+
+// Workspace, tile map, launch geometry of one device of a team.  table holds
+// every team part's descriptor; local parts get their tile ranges here.
+static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* const* by_index,
+                        int n_parts, int n_dev, int n_share) {
+  int64_t t = 0;
+  for (int p : D.parts) {
+    lrb_part* P = by_index[p];
+    P->d.tile0 = t;
+    P->d.ntiles = (P->d.n + kTile - 1) / kTile;
+    t += P->d.ntiles;
+    table[p] = P->d;
+  }
+  D.n_tiles = t;
+  DeviceGuard g(D.device);
+  D.stream = by_index[D.parts.front()]->main;
+  const int64_t n_tiles = std::max<int64_t>(D.n_tiles, 1);
+  size_t bytes = 0;
+  auto take = [&](size_t b) {
+    size_t at = bytes;
+    bytes = (bytes + b + 255) & ~size_t(255);
+    return at;
+  };
+  const size_t o_parts = take(sizeof(PartDev) * n_parts);
+  const size_t o_tp = take(sizeof(int32_t) * n_tiles);
+  const size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
+  const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts);
+  const size_t o_red = take(sizeof(double) * kMaxRed);
+  const size_t o_bar = take(sizeof(unsigned) * 2);
+  const size_t o_epoch = take(sizeof(unsigned long long));
+  const size_t o_flags = take(sizeof(unsigned long long) * n_dev);
+  const size_t o_peer_flags = take(sizeof(void*) * n_dev);
+  const size_t o_peer_red = take(sizeof(void*) * n_dev);
+  const size_t o_out = take(sizeof(SolveOut));
+  LRB_CUDA(cudaMalloc(&D.ws, bytes));
+  LRB_CUDA(cudaMemset(D.ws, 0, bytes));
+  D.ws_bytes = bytes;
+  char* w = static_cast<char*>(D.ws);
+  D.parts_dev = reinterpret_cast<PartDev*>(w + o_parts);
+  D.out_dev = reinterpret_cast<SolveOut*>(w + o_out);
+  TeamDev& H = D.host;
+  H.n_parts = n_parts;
+  H.dev_rank = D.rank;
+  H.n_dev = n_dev;
+  H.part_begin = D.parts.front();
+  H.part_end = D.parts.back() + 1;
+  H.n_tiles = D.n_tiles;
+  H.parts = D.parts_dev;
+  H.tile_part = reinterpret_cast<int32_t*>(w + o_tp);
+  H.partials = reinterpret_cast<double*>(w + o_partials);
+  H.part_red = reinterpret_cast<double*>(w + o_pred);
+  H.red = reinterpret_cast<double*>(w + o_red);
+  H.bar_count = reinterpret_cast<unsigned*>(w + o_bar);
+  H.bar_gen = H.bar_count + 1;
+  H.epoch = reinterpret_cast<unsigned long long*>(w + o_epoch);
+  H.flags = reinterpret_cast<unsigned long long*>(w + o_flags);
+  H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
+  H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
+  H.out = D.out_dev;
+  H.timeout_ns = 20LL * 1000 * 1000 * 1000;
+  std::vector<int32_t> tp(n_tiles, 0);
+  for (int p : D.parts)
+    for (int64_t q = 0; q < by_index[p]->d.ntiles; ++q) tp[by_index[p]->d.tile0 + q] = p;
+  LRB_CUDA(cudaMemcpy((void*)H.tile_part, tp.data(), sizeof(int32_t) * n_tiles, cudaMemcpyHostToDevice));
+  LRB_CUDA(cudaEventCreate(&D.t0));
+  LRB_CUDA(cudaEventCreate(&D.t1));
+  D.inl = int(D.parts.size()) <= kInlineParts;
+  if (D.inl)
+    for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
+  D.cooperative = (n_share == 1);
+  for (int m = 0; m < 3; ++m) {
+    D.fn[m] = solve_kernel(m, D.inl);
+    D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, &D.smem[m]);
+    if (D.grid[m] <= 0) {
+      set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
+      return LRB_ERUNTIME;
+    }
+  }
+  return LRB_OK;
+}
+
+// Every device's copy of the part table, the flag and part-value peer tables.
+static int publish_tables(TeamDevice& D, const std::vector<PartDev>& table,
+                          const std::vector<void*>& pf, const std::vector<void*>& pr) {
+  DeviceGuard g(D.device);
+  const int n_dev = int(pf.size());
+  LRB_CUDA(cudaMemcpy(D.parts_dev, table.data(), sizeof(PartDev) * table.size(), cudaMemcpyHostToDevice));
+  LRB_CUDA(cudaMemcpy(D.host.peer_flags, pf.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
+  LRB_CUDA(cudaMemcpy(D.host.peer_part_red, pr.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
+  return LRB_OK;
+}
+
+}  // namespace lrb
 
 namespace lrb {
 
@@ -674,99 +777,214 @@ int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* d
         }
         cudaGetLastError();
       }
-  // per-device workspace
+  // per-device workspace, then the shared part / peer tables
   std::vector<PartDev> table(n_parts);
   for (auto& D : team->devs) {
-    int64_t t = 0;
-    for (int p : D.parts) {
-      lrb_part* P = parts[p];
-      P->d.tile0 = t;
-      P->d.ntiles = (P->d.n + kTile - 1) / kTile;
-      t += P->d.ntiles;
-    }
-    D.n_tiles = t;
+    int rc = setup_device(D, table, parts, n_parts, n_dev, share[D.device]);
+    if (rc) return rc;
   }
-  for (int p = 0; p < n_parts; ++p) table[p] = parts[p]->d;
-  for (auto& D : team->devs) {
-    DeviceGuard g(D.device);
-    D.stream = parts[D.parts.front()]->main;
-    const int64_t n_tiles = std::max<int64_t>(D.n_tiles, 1);
-    size_t bytes = 0;
-    auto take = [&](size_t b) {
-      size_t at = bytes;
-      bytes = (bytes + b + 255) & ~size_t(255);
-      return at;
-    };
-    size_t o_parts = take(sizeof(PartDev) * n_parts);
-    size_t o_tp = take(sizeof(int32_t) * n_tiles);
-    size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
-    size_t o_pred = take(sizeof(double) * kMaxRed * n_parts);
-    size_t o_red = take(sizeof(double) * kMaxRed);
-    size_t o_bar = take(sizeof(unsigned) * 2);
-    size_t o_epoch = take(sizeof(unsigned long long));
-    size_t o_flags = take(sizeof(unsigned long long) * n_dev);
-    size_t o_peer_flags = take(sizeof(void*) * n_dev);
-    size_t o_peer_red = take(sizeof(void*) * n_dev);
-    size_t o_out = take(sizeof(SolveOut));
-    LRB_CUDA(cudaMalloc(&D.ws, bytes));
-    LRB_CUDA(cudaMemset(D.ws, 0, bytes));
-    char* w = static_cast<char*>(D.ws);
-    D.parts_dev = reinterpret_cast<PartDev*>(w + o_parts);
-    D.out_dev = reinterpret_cast<SolveOut*>(w + o_out);
-    TeamDev& H = D.host;
-    H.n_parts = n_parts;
-    H.dev_rank = D.rank;
-    H.n_dev = n_dev;
-    H.part_begin = D.parts.front();
-    H.part_end = D.parts.back() + 1;
-    H.n_tiles = D.n_tiles;
-    H.parts = D.parts_dev;
-    H.tile_part = reinterpret_cast<int32_t*>(w + o_tp);
-    H.partials = reinterpret_cast<double*>(w + o_partials);
-    H.part_red = reinterpret_cast<double*>(w + o_pred);
-    H.red = reinterpret_cast<double*>(w + o_red);
-    H.bar_count = reinterpret_cast<unsigned*>(w + o_bar);
-    H.bar_gen = H.bar_count + 1;
-    H.epoch = reinterpret_cast<unsigned long long*>(w + o_epoch);
-    H.flags = reinterpret_cast<unsigned long long*>(w + o_flags);
-    H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
-    H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
-    H.out = D.out_dev;
-    H.timeout_ns = 20LL * 1000 * 1000 * 1000;
-    std::vector<int32_t> tp(n_tiles, 0);
-    for (int p : D.parts)
-      for (int64_t t = 0; t < parts[p]->d.ntiles; ++t) tp[parts[p]->d.tile0 + t] = p;
-    LRB_CUDA(cudaMemcpy(D.parts_dev, table.data(), sizeof(PartDev) * n_parts, cudaMemcpyHostToDevice));
-    LRB_CUDA(cudaMemcpy((void*)H.tile_part, tp.data(), sizeof(int32_t) * n_tiles, cudaMemcpyHostToDevice));
-    LRB_CUDA(cudaEventCreate(&D.t0));
-    LRB_CUDA(cudaEventCreate(&D.t1));
-    const int n_share = share[D.device];
-    D.inl = int(D.parts.size()) <= kInlineParts;
-    if (D.inl)
-      for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
-    for (int m = 0; m < 3; ++m) D.fn[m] = solve_kernel(m, D.inl);
-    D.grid[0] = max_grid(D.fn[0], D.device, D.n_tiles, n_share, &D.smem[0]);
-    D.grid[1] = max_grid(D.fn[1], D.device, D.n_tiles, n_share, &D.smem[1]);
-    D.grid[2] = max_grid(D.fn[2], D.device, D.n_tiles, n_share, &D.smem[2]);
-    for (int m = 0; m < 3; ++m)
-      if (D.grid[m] <= 0) {
-        set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
-        return LRB_ERUNTIME;
-      }
-  }
-  // peer pointer tables
   std::vector<void*> pf(n_dev), pr(n_dev);
   for (auto& D : team->devs) {
     pf[D.rank] = D.host.flags;
     pr[D.rank] = D.host.part_red;
   }
   for (auto& D : team->devs) {
-    DeviceGuard g(D.device);
-    LRB_CUDA(cudaMemcpy(D.host.peer_flags, pf.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
-    LRB_CUDA(cudaMemcpy(D.host.peer_part_red, pr.data(), sizeof(void*) * n_dev, cudaMemcpyHostToDevice));
+    int rc = publish_tables(D, table, pf, pr);
+    if (rc) return rc;
   }
   *out = team.release();
   return LRB_OK;
+}
+
+}  // extern "C"
+
+// ---- multi-process teams (CUDA IPC) ---------------------------------------
+namespace {
+
+struct PartBlob {   // fixed layout inside LRB_BLOB_BYTES
+  char magic[8];
+  cudaIpcMemHandle_t arena;
+  int64_t arena_off;      // offset of the arena start inside the IPC allocation
+  PartDev d;              // pointers rewritten as offsets from the arena start
+};
+struct TeamBlob {
+  char magic[8];
+  cudaIpcMemHandle_t ws;
+  int64_t flags_off, part_red_off;
+};
+static_assert(sizeof(PartBlob) <= LRB_BLOB_BYTES, "blob too small");
+static_assert(sizeof(TeamBlob) <= LRB_BLOB_BYTES, "blob too small");
+
+template <class T>
+T* rebase(T* p, const char* from, char* to) {
+  return p ? reinterpret_cast<T*>(to + (reinterpret_cast<const char*>(p) - from)) : nullptr;
+}
+
+// base of the cudaMalloc allocation containing p (driver API, loaded lazily so
+// the library still loads on machines without a driver)
+int alloc_base(const void* p, char** base) {
+  typedef int (*fn_t)(unsigned long long*, size_t*, unsigned long long);
+  static fn_t fn = nullptr;
+  if (!fn) {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (h) fn = reinterpret_cast<fn_t>(dlsym(h, "cuMemGetAddressRange_v2"));
+    if (!fn) {
+      set_error("cuMemGetAddressRange_v2 unavailable");
+      return LRB_ECUDA;
+    }
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0) {
+    set_error("cuMemGetAddressRange failed");
+    return LRB_ECUDA;
+  }
+  *base = reinterpret_cast<char*>(b);
+  return LRB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lrb_part_export(const lrb_part* part, void* blob) {
+  if (!part || !blob) {
+    set_error("lrb_part_export: null argument");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(part->device);
+  std::memset(blob, 0, LRB_BLOB_BYTES);
+  PartBlob b{};
+  std::memcpy(b.magic, "LRBPART", 8);
+  char* arena = const_cast<char*>(reinterpret_cast<const char*>(part->d.slice_ptr));
+  char* base = nullptr;
+  int rc = alloc_base(arena, &base);
+  if (rc) return rc;
+  LRB_CUDA(cudaIpcGetMemHandle(&b.arena, base));
+  b.arena_off = arena - base;
+  b.d = part->d;
+  // pointers -> offsets from the arena start (rebased by the importer)
+  char* zero = nullptr;
+  PartDev& d = b.d;
+  d.slice_ptr = rebase(d.slice_ptr, arena, zero);
+  d.slice_pat = rebase(d.slice_pat, arena, zero);
+  d.pat_off = rebase(d.pat_off, arena, zero);
+  d.rmask = rebase(d.rmask, arena, zero);
+  d.col = rebase(d.col, arena, zero);
+  d.src = rebase(d.src, arena, zero);
+  d.dpos = rebase(d.dpos, arena, zero);
+  d.hpart = rebase(d.hpart, arena, zero);
+  d.hidx = rebase(d.hidx, arena, zero);
+  d.val = rebase(d.val, arena, zero);
+  d.recv = rebase(d.recv, arena, zero);
+  for (double** v : {&d.x, &d.r, &d.p0, &d.p1, &d.q, &d.b, &d.dinv, &d.rhat, &d.v0, &d.v1, &d.s, &d.t})
+    *v = rebase(*v, arena, zero);
+  std::memcpy(blob, &b, sizeof(b));
+  return LRB_OK;
+}
+
+int lrb_team_create_ipc(int32_t n_parts, int32_t part_begin, int32_t n_local,
+                        lrb_part* const* local_parts, const void* part_blobs, int32_t dev_rank,
+                        int32_t n_dev, lrb_team** out, void* team_blob) {
+  if (n_parts < 1 || n_local < 1 || part_begin < 0 || part_begin + n_local > n_parts ||
+      !local_parts || !part_blobs || !out || !team_blob || dev_rank < 0 || dev_rank >= n_dev) {
+    set_error("lrb_team_create_ipc: bad arguments");
+    return LRB_EVALUE;
+  }
+  const int device = local_parts[0]->device;
+  for (int i = 0; i < n_local; ++i)
+    if (local_parts[i]->device != device) {
+      set_error("lrb_team_create_ipc: local parts must share one CUDA device");
+      return LRB_EVALUE;
+    }
+  DeviceGuard g(device);
+  auto team = std::make_unique<lrb_team>();
+  team->ipc_dev = device;
+  team->parts.assign(n_parts, nullptr);
+  for (int i = 0; i < n_local; ++i) team->parts[part_begin + i] = local_parts[i];
+  std::vector<PartDev> table(n_parts);
+  const char* blobs = static_cast<const char*>(part_blobs);
+  for (int p = 0; p < n_parts; ++p) {
+    if (p >= part_begin && p < part_begin + n_local) continue;
+    PartBlob b;
+    std::memcpy(&b, blobs + size_t(p) * LRB_BLOB_BYTES, sizeof(b));
+    if (std::memcmp(b.magic, "LRBPART", 8) != 0) {
+      set_error("lrb_team_create_ipc: bad part blob");
+      return LRB_EVALUE;
+    }
+    void* base = nullptr;
+    LRB_CUDA(cudaIpcOpenMemHandle(&base, b.arena, cudaIpcMemLazyEnablePeerAccess));
+    team->ipc_opened.push_back(base);
+    char* arena = static_cast<char*>(base) + b.arena_off;
+    PartDev d = b.d;
+    const char* zero = nullptr;
+    d.slice_ptr = rebase(d.slice_ptr, zero, arena);
+    d.slice_pat = rebase(d.slice_pat, zero, arena);
+    d.pat_off = rebase(d.pat_off, zero, arena);
+    d.rmask = rebase(d.rmask, zero, arena);
+    d.col = rebase(d.col, zero, arena);
+    d.src = rebase(d.src, zero, arena);
+    d.dpos = rebase(d.dpos, zero, arena);
+    d.hpart = rebase(d.hpart, zero, arena);
+    d.hidx = rebase(d.hidx, zero, arena);
+    d.val = rebase(d.val, zero, arena);
+    d.recv = rebase(d.recv, zero, arena);
+    for (double** v : {&d.x, &d.r, &d.p0, &d.p1, &d.q, &d.b, &d.dinv, &d.rhat, &d.v0, &d.v1, &d.s, &d.t})
+      *v = rebase(*v, zero, arena);
+    table[p] = d;
+  }
+  team->devs.resize(1);
+  TeamDevice& D = team->devs[0];
+  D.device = device;
+  D.rank = dev_rank;
+  for (int i = 0; i < n_local; ++i) D.parts.push_back(part_begin + i);
+  team->dev_of_part.assign(n_parts, -1);
+  int rc = setup_device(D, table, team->parts.data(), n_parts, n_dev, 1);
+  if (rc) return rc;
+  // local table now; peer tables after connect
+  LRB_CUDA(cudaMemcpy(D.parts_dev, table.data(), sizeof(PartDev) * n_parts, cudaMemcpyHostToDevice));
+  std::memset(team_blob, 0, LRB_BLOB_BYTES);
+  TeamBlob tb{};
+  std::memcpy(tb.magic, "LRBTEAM", 8);
+  LRB_CUDA(cudaIpcGetMemHandle(&tb.ws, D.ws));
+  tb.flags_off = reinterpret_cast<char*>(D.host.flags) - static_cast<char*>(D.ws);
+  tb.part_red_off = reinterpret_cast<char*>(D.host.part_red) - static_cast<char*>(D.ws);
+  std::memcpy(team_blob, &tb, sizeof(tb));
+  *out = team.release();
+  return LRB_OK;
+}
+
+int lrb_team_connect_ipc(lrb_team* team, const void* team_blobs) {
+  if (!team || !team_blobs || team->devs.size() != 1) {
+    set_error("lrb_team_connect_ipc: bad arguments");
+    return LRB_EVALUE;
+  }
+  TeamDevice& D = team->devs[0];
+  DeviceGuard g(D.device);
+  const int n_dev = D.host.n_dev;
+  std::vector<void*> pf(n_dev), pr(n_dev);
+  const char* blobs = static_cast<const char*>(team_blobs);
+  for (int r = 0; r < n_dev; ++r) {
+    if (r == D.rank) {
+      pf[r] = D.host.flags;
+      pr[r] = D.host.part_red;
+      continue;
+    }
+    TeamBlob tb;
+    std::memcpy(&tb, blobs + size_t(r) * LRB_BLOB_BYTES, sizeof(tb));
+    if (std::memcmp(tb.magic, "LRBTEAM", 8) != 0) {
+      set_error("lrb_team_connect_ipc: bad team blob");
+      return LRB_EVALUE;
+    }
+    void* base = nullptr;
+    LRB_CUDA(cudaIpcOpenMemHandle(&base, tb.ws, cudaIpcMemLazyEnablePeerAccess));
+    team->ipc_opened.push_back(base);
+    pf[r] = static_cast<char*>(base) + tb.flags_off;
+    pr[r] = static_cast<char*>(base) + tb.part_red_off;
+  }
+  std::vector<PartDev> table(D.host.n_parts);
+  LRB_CUDA(cudaMemcpy(table.data(), D.parts_dev, sizeof(PartDev) * table.size(), cudaMemcpyDeviceToHost));
+  return publish_tables(D, table, pf, pr);
 }
 
 int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out) {
@@ -783,6 +1001,10 @@ void lrb_team_destroy(lrb_team* team) {
     if (D.hist_dev) cudaFree(D.hist_dev);
     if (D.t0) cudaEventDestroy(D.t0);
     if (D.t1) cudaEventDestroy(D.t1);
+  }
+  if (team->ipc_dev >= 0) {
+    DeviceGuard g(team->ipc_dev);
+    for (void* p : team->ipc_opened) cudaIpcCloseMemHandle(p);
   }
   delete team;
 }
@@ -818,6 +1040,10 @@ static int team_epilogue(lrb_team* team, lrb::TeamDevice& D) {
 int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host) {
   if (!team || !x_host || !y_host) {
     set_error("lrb_team_spmv: null argument");
+    return LRB_EVALUE;
+  }
+  if (team->ipc_dev >= 0 && team->devs[0].host.n_dev > 1) {
+    set_error("lrb_team_spmv: not available on multi-process teams (use lrb_team_solve)");
     return LRB_EVALUE;
   }
   std::lock_guard<std::mutex> lk(team->mu);
@@ -908,9 +1134,9 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     const int grid = D.grid[method];
     const size_t smem = D.smem[method];
     LRB_CUDA(cudaEventRecord(D.t0, D.stream));
-    if (multi) {
-      // co-residency across devices is guaranteed by separate GPUs; within a
-      // device the grid fits one wave (max_grid)
+    if (!D.cooperative) {
+      // several device ranks share this GPU (test mode): each grid is sized
+      // to a share of one wave (max_grid), so they are co-resident
       LRB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));
     } else {
       LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));

@@ -195,6 +195,12 @@ class DevicePart:
         N.check(N.lrb_part_elapsed_ms(self.h, C.byref(ms)))
         return float(ms.value)
 
+    def export(self) -> bytes:
+        """Opaque blob (CUDA IPC handle + layout) for peers in other processes."""
+        buf = (C.c_char * N.BLOB_BYTES)()
+        N.check(N.lrb_part_export(self.h, buf))
+        return bytes(buf)
+
     def pointers(self):
         arr = (C.c_void_p * 16)()
         N.check(N.lrb_part_pointers(self.h, arr))
@@ -223,6 +229,33 @@ class Team:
         self.h = h
         self._lock = threading.Lock()
 
+    @classmethod
+    def across_processes(cls, local_parts, part_begin, n_parts, dev_rank, n_dev, allgather):
+        """Team spanning processes (one per GPU).  ``allgather(bytes) -> [bytes]``
+        exchanges blobs in device-rank order (e.g. torch.distributed over gloo);
+        halo values and partial dots then move by NVLink peer memory only."""
+        self = cls.__new__(cls)
+        self.parts = [None] * n_parts
+        for i, p in enumerate(local_parts):
+            self.parts[part_begin + i] = p
+        self._local = list(local_parts)
+        self._part_begin = part_begin
+        mine = b"".join(p.export() for p in local_parts)
+        every = allgather(mine)
+        blobs = b"".join(every)
+        if len(blobs) != n_parts * N.BLOB_BYTES:
+            raise ValueError("team blobs do not cover every part exactly once")
+        arr = N.ptr_array([p.h.value for p in local_parts])
+        h = C.c_void_p()
+        team_blob = (C.c_char * N.BLOB_BYTES)()
+        N.check(N.lrb_team_create_ipc(n_parts, part_begin, len(local_parts), arr, blobs, dev_rank,
+                                      n_dev, C.byref(h), team_blob))
+        self.h = h
+        self._lock = threading.Lock()
+        tblobs = b"".join(allgather(bytes(team_blob)))
+        N.check(N.lrb_team_connect_ipc(self.h, tblobs))
+        return self
+
     def spmv(self, xs):
         xs = [np.ascontiguousarray(x, dtype=np.float64) for x in xs]
         ys = [np.empty(p.n, np.float64) for p in self.parts]
@@ -234,15 +267,16 @@ class Team:
         """Run one Krylov solve; bs None = right-hand sides already on device."""
         rep = N.Report()
         bptr = None
-        if bs is not None:
-            bs = [np.ascontiguousarray(b, dtype=np.float64) for b in bs]
-            bptr = N.ptr_array([b.ctypes.data for b in bs])
+        if bs is not None:   # entries for remote parts (multi-process teams) are None
+            bs = [None if b is None else np.ascontiguousarray(b, dtype=np.float64) for b in bs]
+            bptr = N.ptr_array([0 if b is None else b.ctypes.data for b in bs])
         # solutions land in pinned host memory (torch's caching host allocator
         # recycles the blocks); the ndarray keeps its tensor alive
         torch = _torch()
-        xs = [torch.empty(max(p.n, 1), dtype=torch.float64, pin_memory=True).numpy()[:p.n]
+        xs = [None if p is None else
+              torch.empty(max(p.n, 1), dtype=torch.float64, pin_memory=True).numpy()[:p.n]
               for p in self.parts] if want_x else None
-        xptr = N.ptr_array([x.ctypes.data for x in xs]) if want_x else None
+        xptr = N.ptr_array([0 if x is None else x.ctypes.data for x in xs]) if want_x else None
         hist = np.zeros(max(hist_cap, 0), np.float64)
         rc = N.lrb_team_solve(self.h, N.METHODS[method], bptr, xptr, float(tol), int(max_iter),
                               C.byref(rep), N.ptr(hist) if hist_cap > 0 else None, int(hist_cap))

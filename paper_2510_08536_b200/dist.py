@@ -1,0 +1,127 @@
+"""One process per GPU (torchrun): host orchestration of the multi-GPU path.
+
+Process g owns GPU part(s) ``parts_per_proc*g ..`` and hosts their CPU source
+ranks as threads.  ``torch.distributed`` (gloo, CPU) carries only create-time
+plumbing — IPC blobs, halo descriptions — and the max-over-ranks of timings.
+The data path (halo values, partial dot products) never touches NCCL: the
+persistent solve kernels read neighbour vectors and exchange dot partials
+through NVLink peer memory (csrc/kernels.cuh team_sync).
+
+No update traffic crosses GPUs: a source's segment goes only to its owner
+(repart.py:239-250), so ``update`` is process-local.
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from .core import PartitionMap, make_partition_map
+from .device import DevicePart, Team, device_count
+from .repart import _owner_plan, _pieces, _Source, sparsity_fingerprint
+
+
+class ProcessLayout:
+    """Which GPU parts and CPU ranks live in process ``rank`` of ``world``."""
+
+    def __init__(self, cells_per_rank, alpha: int, world: int, rank: int):
+        self.pm: PartitionMap = make_partition_map(cells_per_rank, alpha)
+        if self.pm.n_gpu % world:
+            raise ValueError(f"{self.pm.n_gpu} GPU parts cannot be split over {world} processes")
+        self.world, self.rank = world, rank
+        self.parts_per_proc = self.pm.n_gpu // world
+        self.part_begin = rank * self.parts_per_proc
+        self.parts = list(range(self.part_begin, self.part_begin + self.parts_per_proc))
+        a = self.pm.alpha
+        self.cpu_ranks = list(range(self.part_begin * a, (self.part_begin + self.parts_per_proc) * a))
+
+    def owner_of(self, cpu_rank: int) -> int:
+        return cpu_rank // self.pm.alpha
+
+
+def allgather_bytes(blob: bytes, group=None):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+def allgather_obj(obj, group=None):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def halo_pairs(layout: ProcessLayout, halo_by_part):
+    """Reference halo plan semantics across processes (solver.py:48-77):
+    for every ordered pair (owner j -> needer k) the rows j sends, from the
+    halo columns every part published.  Used by the tests to check the device
+    halo tables (hpart/hidx) against the reference's send lists."""
+    pm = layout.pm
+    go = pm.gpu_offsets
+    send = {}
+    for k, halo in halo_by_part.items():
+        owners = pm.col_owner_gpu(np.asarray(halo, dtype=np.int64))
+        for j in np.unique(owners):
+            send[(int(j), int(k))] = np.asarray(halo, np.int64)[owners == j] - go[j]
+    return send
+
+
+class DistributedOwner:
+    """This process's owner part(s) and source ranks: create once, then
+    update + solve per timestep through the C ABI with host buffers."""
+
+    def __init__(self, layout: ProcessLayout, problems, group=None, n_threads=0):
+        """``problems``: {cpu_rank: (LduMatrix, [InterfaceBlock])} for this process."""
+        self.layout = layout
+        pm = layout.pm
+        self.fingerprints = {r: sparsity_fingerprint(*problems[r]) for r in layout.cpu_ranks}
+        dev = (layout.rank % device_count())
+        self.parts = []
+        self.plans = []
+        for k in layout.parts:
+            srcs = [_Source(*problems[r], pm, r) for r in range(pm.alpha * k, pm.alpha * (k + 1))]
+            plan = _owner_plan(srcs, pm, k)
+            self.plans.append(plan)
+            self.parts.append(DevicePart(plan, dev))
+        self.team = Team.across_processes(self.parts, layout.part_begin, pm.n_gpu, layout.rank,
+                                          layout.world, lambda b: allgather_bytes(b, group))
+        self.pool = ThreadPoolExecutor(max(1, len(layout.cpu_ranks)))
+        self.update(problems, "direct")
+
+    def update(self, problems, mode="direct"):
+        """Every local source rank copies its segment (threads; GIL released in C)."""
+        pm = self.layout.pm
+
+        def one(r):
+            m, ifs = problems[r]
+            if sparsity_fingerprint(m, ifs) != self.fingerprints[r]:
+                raise RuntimeError(f"pattern drift on rank {r}")
+            part = self.parts[self.layout.owner_of(r) - self.layout.part_begin]
+            if mode == "direct":
+                part.update_segment(r % pm.alpha, _pieces(m, ifs))
+            else:
+                part.stage_segment(r % pm.alpha, _pieces(m, ifs))
+
+        list(self.pool.map(one, self.layout.cpu_ranks))
+        for p in self.parts:
+            if mode == "direct":
+                p.join()
+            else:
+                p.update_staged_from_stage()
+
+    def solve(self, method, b_local, tol, max_iter, hist_cap=0):
+        bs = [None] * self.layout.pm.n_gpu
+        for i, k in enumerate(self.layout.parts):
+            bs[k] = b_local[i] if b_local is not None else None
+        xs, rep, hist = self.team.solve(method, None if b_local is None else bs, tol, max_iter,
+                                        want_x=True, hist_cap=hist_cap)
+        return [xs[k] for k in self.layout.parts], rep, hist
