@@ -295,6 +295,9 @@ def run_ours_multi(args):
 
     rank, world, local_rank = dist_env()
     dist.init_process_group("gloo")
+    # one GPU per process; on a 1-GPU box the ranks share it (time-sliced,
+    # correctness only — the protocol is the same as over NVLink)
+    local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     N, _, method_default, desc = WORKLOADS[args.workload]
     method = args.method or method_default

@@ -173,6 +173,12 @@ int lrb_team_create_ipc(int32_t n_parts, int32_t part_begin, int32_t n_local,
                         lrb_part* const* local_parts, const void* part_blobs /* n_parts x 512 */,
                         int32_t dev_rank, int32_t n_dev, lrb_team** out, void* team_blob);
 int lrb_team_connect_ipc(lrb_team* team, const void* team_blobs /* n_dev x 512 */);
+/* Diagnostics: copy n doubles of vector `vec` (index as in lrb_part_pointers,
+ * 2 = x ... 13 = t) of team part `part` — local or a peer's, through the
+ * team's own pointer table — into host memory; and this device's barrier
+ * state: out[0] = epoch, out[1..n_dev] = arrival flags written by peers. */
+int lrb_team_read_vector(lrb_team* team, int32_t part, int32_t vec, int64_t n, double* out);
+int lrb_team_debug(lrb_team* team, int64_t* out);
 
 /* Distributed SpMV y = A x (solver.py:80-97): x_host/y_host per part. */
 int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host);

@@ -604,7 +604,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_parts = take(sizeof(PartDev) * n_parts);
   const size_t o_tp = take(sizeof(int32_t) * n_tiles);
   const size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
-  const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts);
+  const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts * 2);  // epoch parity
   const size_t o_red = take(sizeof(double) * kMaxRed);
   const size_t o_bar = take(sizeof(unsigned) * 2);
   const size_t o_epoch = take(sizeof(unsigned long long));
@@ -637,7 +637,11 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
   H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
   H.out = D.out_dev;
-  H.timeout_ns = 20LL * 1000 * 1000 * 1000;
+  {
+    const char* env = getenv("LRB_BARRIER_TIMEOUT_S");
+    const double s = env ? atof(env) : 20.0;
+    H.timeout_ns = (long long)((s > 0 ? s : 20.0) * 1e9);
+  }
   std::vector<int32_t> tp(n_tiles, 0);
   for (int p : D.parts)
     for (int64_t q = 0; q < by_index[p]->d.ntiles; ++q) tp[by_index[p]->d.tile0 + q] = p;
@@ -985,6 +989,41 @@ int lrb_team_connect_ipc(lrb_team* team, const void* team_blobs) {
   std::vector<PartDev> table(D.host.n_parts);
   LRB_CUDA(cudaMemcpy(table.data(), D.parts_dev, sizeof(PartDev) * table.size(), cudaMemcpyDeviceToHost));
   return publish_tables(D, table, pf, pr);
+}
+
+int lrb_team_read_vector(lrb_team* team, int32_t part, int32_t vec, int64_t n, double* out) {
+  if (!team || !out || vec < 2 || vec > 13 || part < 0) {
+    set_error("lrb_team_read_vector: bad arguments");
+    return LRB_EVALUE;
+  }
+  TeamDevice& D = team->devs[0];
+  if (part >= D.host.n_parts) {
+    set_error("lrb_team_read_vector: bad part");
+    return LRB_EVALUE;
+  }
+  DeviceGuard g(D.device);
+  PartDev P;
+  LRB_CUDA(cudaMemcpy(&P, D.parts_dev + part, sizeof(PartDev), cudaMemcpyDeviceToHost));
+  double* v[12] = {P.x, P.r, P.p0, P.p1, P.q, P.b, P.dinv, P.rhat, P.v0, P.v1, P.s, P.t};
+  if (n > P.n) n = P.n;
+  LRB_CUDA(cudaMemcpy(out, v[vec - 2], 8 * n, cudaMemcpyDefault));
+  return LRB_OK;
+}
+
+int lrb_team_debug(lrb_team* team, int64_t* out) {
+  if (!team || !out) {
+    set_error("lrb_team_debug: null argument");
+    return LRB_EVALUE;
+  }
+  TeamDevice& D = team->devs[0];
+  DeviceGuard g(D.device);
+  unsigned long long e = 0;
+  std::vector<unsigned long long> f(D.host.n_dev);
+  LRB_CUDA(cudaMemcpy(&e, D.host.epoch, sizeof(e), cudaMemcpyDeviceToHost));
+  LRB_CUDA(cudaMemcpy(f.data(), D.host.flags, 8 * f.size(), cudaMemcpyDeviceToHost));
+  out[0] = int64_t(e);
+  for (size_t i = 0; i < f.size(); ++i) out[1 + i] = int64_t(f[i]);
+  return LRB_OK;
 }
 
 int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out) {

@@ -204,6 +204,12 @@ __device__ void team_sync(const TeamDev& T, double* red) {
   __syncthreads();
   if (s_last) {
     __threadfence();
+    // Part values are double-buffered by epoch parity: a fast peer may already
+    // publish epoch e+1 into our buffer while we still read epoch e (it only
+    // needs our flag for e, which we raise before summing).  It cannot reach
+    // e+2 before our flag for e+1, i.e. before we finished reading e.
+    const unsigned long long e_next = (T.n_dev > 1) ? *(volatile unsigned long long*)T.epoch + 1 : 0;
+    const int64_t pbuf = int64_t(e_next & 1) * T.n_parts * kMaxRed;
     for (int p = T.part_begin; p < T.part_end; ++p) {
       const PartDev& P = T.parts[p];
       double acc[NR];
@@ -233,16 +239,17 @@ __device__ void team_sync(const TeamDev& T, double* red) {
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          T.part_red[p * kMaxRed + j] = acc[j];
+          T.part_red[pbuf + p * kMaxRed + j] = acc[j];
           for (int d = 0; d < T.n_dev; ++d)
-            if (d != T.dev_rank) T.peer_part_red[d][p * kMaxRed + j] = acc[j];
+            if (d != T.dev_rank) T.peer_part_red[d][pbuf + p * kMaxRed + j] = acc[j];
         }
       }
     }
     if (threadIdx.x == 0) {
       if (T.n_dev > 1) {
         __threadfence_system();
-        const unsigned long long e = ++(*T.epoch);
+        const unsigned long long e = e_next;
+        *T.epoch = e;
         for (int d = 0; d < T.n_dev; ++d)
           if (d != T.dev_rank) st_release_sys(T.peer_flags[d] + T.dev_rank, e);
         const long long t0 = global_ns();
@@ -260,8 +267,9 @@ __device__ void team_sync(const TeamDev& T, double* red) {
       }
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        double s = vload(T.part_red + j);
-        for (int p = 1; p < T.n_parts; ++p) s = __dadd_rn(s, vload(T.part_red + p * kMaxRed + j));
+        double s = vload(T.part_red + pbuf + j);
+        for (int p = 1; p < T.n_parts; ++p)
+          s = __dadd_rn(s, vload(T.part_red + pbuf + p * kMaxRed + j));
         T.red[j] = s;
       }
       *T.bar_count = 0;

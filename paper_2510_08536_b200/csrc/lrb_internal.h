@@ -94,7 +94,7 @@ struct TeamDev {
   PartDev* parts;           // [n_parts] (remote parts carry peer pointers)
   const int32_t* tile_part; // [n_tiles]
   double* partials;         // [n_tiles * kMaxRed]
-  double* part_red;         // [n_parts * kMaxRed] every device holds all parts' values
+  double* part_red;         // [2][n_parts][kMaxRed] all parts' values, by epoch parity
   double* red;              // [kMaxRed] team-reduced values (this device)
   unsigned int* bar_count;
   unsigned int* bar_gen;

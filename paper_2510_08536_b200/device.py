@@ -256,6 +256,21 @@ class Team:
         N.check(N.lrb_team_connect_ipc(self.h, tblobs))
         return self
 
+    VECS = {"x": 2, "r": 3, "p0": 4, "p1": 5, "q": 6, "b": 7, "dinv": 8, "rhat": 9, "v0": 10,
+            "v1": 11, "s": 12, "t": 13}
+
+    def read_vector(self, part, name, n):
+        """Read a vector of any team part through the team's pointer table
+        (peer memory for remote parts) — diagnostics and tests."""
+        out = np.empty(n, np.float64)
+        N.check(N.lrb_team_read_vector(self.h, part, self.VECS[name], n, N.ptr(out)))
+        return out
+
+    def debug(self, n_dev):
+        out = np.zeros(1 + n_dev, np.int64)
+        N.check(N.lrb_team_debug(self.h, N.ptr(out)))
+        return out
+
     def spmv(self, xs):
         xs = [np.ascontiguousarray(x, dtype=np.float64) for x in xs]
         ys = [np.empty(p.n, np.float64) for p in self.parts]

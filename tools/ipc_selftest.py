@@ -41,16 +41,41 @@ def worker(rank, world, port, out):
     lay = ProcessLayout([p.n_cells for p in parts], ALPHA, world, rank)
     probs = {r: lrb.assemble_poisson(parts[r]) for r in lay.cpu_ranks}
     owner = DistributedOwner(lay, probs)
+    for p in owner.parts:
+        p.sync()
+    dist.barrier()
+    # 1) peer pointers: read the OTHER process's part (dinv = 1/diag after the
+    #    initial scatter) through this process's team table (CUDA IPC mapping)
+    other = 1 - rank
+    n_other = parts[2 * other].n_cells + parts[2 * other + 1].n_cells
+    diag = np.concatenate([lrb.assemble_poisson(parts[r])[0].diag for r in (2 * other, 2 * other + 1)])
+    got = owner.team.read_vector(other, "dinv", n_other)
+    peer_ok = bool(np.array_equal(got, 1.0 / diag))
+    print(f"[rank {rank}] peer read ok={peer_ok}", file=sys.stderr, flush=True)
+    dist.barrier()
     t0 = time.time()
-    xs, rep, hist = owner.solve("pcg", [np.ones(p.n) for p in owner.parts], 1e-9, 500,
-                                hist_cap=500)
+    try:
+        xs, rep, hist = owner.solve("pcg", [np.ones(p.n) for p in owner.parts], 1e-9, 500,
+                                    hist_cap=500)
+        err = None
+    except Exception as exc:  # noqa: BLE001
+        xs, rep, hist, err = [np.zeros(p.n) for p in owner.parts], None, [], repr(exc)
+        print(f"[rank {rank}] solve failed: {err}; barrier state {owner.team.debug(world)}",
+              file=sys.stderr, flush=True)
     dt = time.time() - t0
-    xs_all = allgather_obj((rank, [x.copy() for x in xs], rep.iterations, list(hist)))
+    mine = {"rank": rank, "peer_ok": peer_ok, "error": err, "seconds": dt,
+            "debug": owner.team.debug(world).tolist(),
+            "iterations": None if rep is None else rep.iterations,
+            "x": np.concatenate(xs).tolist(), "hist": [float(h) for h in hist]}
+    every = sorted(allgather_obj(mine), key=lambda d: d["rank"])
     if rank == 0:
+        res = {"ranks": [{k: v for k, v in d.items() if k not in ("x", "hist")} for d in every],
+               "peer_ok": all(d["peer_ok"] for d in every),
+               "error": next((d["error"] for d in every if d["error"]), None),
+               "iterations": every[0]["iterations"], "seconds": max(d["seconds"] for d in every),
+               "x": [sum((d["x"] for d in every), [])], "hist": every[0]["hist"]}
         with open(out, "w") as fh:
-            json.dump({"iterations": rep.iterations, "seconds": dt,
-                       "x": [np.concatenate([np.concatenate(v[1]) for v in sorted(xs_all)]).tolist()],
-                       "hist": list(hist)}, fh)
+            json.dump(res, fh)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -61,6 +86,9 @@ def main():
     os.makedirs(os.path.dirname(out), exist_ok=True)
     mp.spawn(worker, args=(2, _port(), out), nprocs=2, join=True)
     res = json.load(open(out))
+    if res.get("error"):
+        print(json.dumps({k: v for k, v in res.items() if k not in ("x", "hist")}))
+        sys.exit(2)
     # single-process reference run of the same team
     import paper_2510_08536_b200 as lrb
     parts = lrb.decompose_slab(lrb.StructuredGrid(*DIMS), NCPU)
