@@ -51,7 +51,8 @@ static int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 
 // Arena layout of one part (all sections 256-byte aligned).
 struct Layout {
-  int64_t slice_ptr, slice_pat, pat_off, rmask, col, src, dpos, hpart, hidx, val, recv, vec, total;
+  int64_t slice_ptr, slice_pat, pat_off, rmask, tile_win, col, src, dpos, hpart, hidx, val, recv,
+      vec, total;
   static constexpr int kVecs = 12;
 };
 
@@ -69,6 +70,7 @@ static Layout layout_of(const Plan& P) {
   L.slice_pat = take(4 * P.n_slices);
   L.pat_off = take(4 * int64_t(P.pat_off.size()));
   L.rmask = take(2 * P.n);
+  L.tile_win = take(4 * int64_t(P.tile_win.size()));
   L.col = take(4 * E);
   L.src = take(4 * E);
   L.dpos = take(P.n);
@@ -178,6 +180,8 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   D.slice_pat = reinterpret_cast<const int32_t*>(base + L.slice_pat);
   D.pat_off = reinterpret_cast<const int32_t*>(base + L.pat_off);
   D.rmask = reinterpret_cast<const uint16_t*>(base + L.rmask);
+  D.tile_win = reinterpret_cast<const int32_t*>(base + L.tile_win);
+  D.max_stage = P.max_stage;
   D.col = reinterpret_cast<const int32_t*>(base + L.col);
   D.src = reinterpret_cast<const int32_t*>(base + L.src);
   D.dpos = reinterpret_cast<const int8_t*>(base + L.dpos);
@@ -239,6 +243,9 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
                            cudaMemcpyHostToDevice, st));
   if (P.n)
     LRB_CUDA(cudaMemcpyAsync(base + L.rmask, P.rmask.data(), 2 * P.n, cudaMemcpyHostToDevice, st));
+  if (!P.tile_win.empty())
+    LRB_CUDA(cudaMemcpyAsync(base + L.tile_win, P.tile_win.data(), 4 * P.tile_win.size(),
+                             cudaMemcpyHostToDevice, st));
   if (E) {
     LRB_CUDA(cudaMemcpyAsync(base + L.col, P.sell_col.data(), 4 * E, cudaMemcpyHostToDevice, st));
     LRB_CUDA(cudaMemcpyAsync(base + L.src, P.sell_src.data(), 4 * E, cudaMemcpyHostToDevice, st));
@@ -577,7 +584,8 @@ struct lrb_team {
 namespace lrb {
 
 static const void* solve_kernel(int method, bool inl);
-static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t* smem);
+static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share,
+                    int64_t stage_doubles, size_t* smem);
 
 // Workspace, tile map, launch geometry of one device of a team.  table holds
 // every team part's descriptor; local parts get their tile ranges here.
@@ -652,9 +660,12 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   if (D.inl)
     for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
   D.cooperative = (n_share == 1);
+  int64_t stage = 0;   // staged-operand shared memory: the largest local part's
+  if (LRB_STAGE)
+    for (int p : D.parts) stage = std::max<int64_t>(stage, by_index[p]->d.max_stage);
   for (int m = 0; m < 3; ++m) {
     D.fn[m] = solve_kernel(m, D.inl);
-    D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, &D.smem[m]);
+    D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
     if (D.grid[m] <= 0) {
       set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
       return LRB_ERUNTIME;
@@ -701,22 +712,31 @@ static const void* solve_kernel(int method, bool inl) {
 
 // Largest co-resident grid (one wave) for a persistent team kernel; the
 // dynamic shared memory holds the warp partials of the block's tiles.
-static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t* smem) {
-  int sms = 0, per_sm = 0;
+static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share,
+                    int64_t stage_doubles, size_t* smem) {
+  int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   const int64_t tiles = std::max<int64_t>(n_tiles, 1);
-  const int64_t slots = std::max<int64_t>(1, sms / std::max(n_share, 1));
-  const size_t smem_max = phase_smem_bytes((tiles + slots - 1) / slots);
-  if (smem_max > 200 * 1024) return -2;
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_max)) !=
+  const size_t stage = size_t(stage_doubles) * sizeof(double);
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
       cudaSuccess)
     return -1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTPB, smem_max) != cudaSuccess)
-    return -1;
-  const int64_t cap = int64_t(sms) * std::max(per_sm, 1) / std::max(n_share, 1);
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, tiles)));
-  *smem = std::max(*smem, phase_smem_bytes((tiles + grid - 1) / grid));
-  return grid;
+  // start from the register-limited occupancy, shrink until the shared memory
+  // of the resulting tiles-per-block fits as well
+  for (int per_sm = 32; per_sm >= 1; --per_sm) {
+    const int64_t cap = int64_t(sms) * per_sm / std::max(n_share, 1);
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cap, tiles)));
+    const size_t need = phase_smem_bytes((tiles + grid - 1) / grid) + stage;
+    if (need > 200 * 1024) continue;
+    int fit = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kernel, kTPB, need) != cudaSuccess)
+      return -1;
+    if (int64_t(fit) * sms / std::max(n_share, 1) >= grid) {   // one co-resident wave
+      *smem = std::max(*smem, need);
+      return grid;
+    }
+  }
+  return -2;
 }
 
 }  // namespace lrb

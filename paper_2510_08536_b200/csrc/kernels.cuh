@@ -71,6 +71,24 @@ constexpr int kChunk = LRB_CHUNK;
 #ifndef LRB_MINB
 #define LRB_MINB 6
 #endif
+#ifndef LRB_SPLITB
+#define LRB_SPLITB 0
+#endif
+// Shared-memory staging of the SpMV operand (tile_win).  Measured slower than
+// the L1-cached gathers on the 7-point stencil (13.4 vs 11.9 ms, C3): the
+// +-1 / +-d0 neighbours already hit L1, staging routes them through L2 and
+// adds two block barriers per tile.  Kept for irregular patterns.
+#ifndef LRB_STAGE
+#define LRB_STAGE 0
+#endif
+// Tiles of a phase: grid-strided (default: the whole grid sweeps the rows as
+// one wavefront, so a row's +-plane neighbours are fetched into L2 by another
+// block at about the same time) or contiguous per block (measured 11% slower
+// at C3).  Partials are per tile either way: results do not depend on the
+// choice or on the grid size.
+#ifndef LRB_CONTIG
+#define LRB_CONTIG 0
+#endif
 
 template <class F>
 __device__ __forceinline__ double row_spmv(const PartDev& P, const PartDev* __restrict__ parts,
@@ -113,6 +131,68 @@ __device__ __forceinline__ double row_spmv(const PartDev& P, const PartDev* __re
   }
   return acc;
 }
+
+// Same, with the local-column operand from floc(c) (staged in shared memory
+// for pattern tiles) and halo columns from fhalo(owner part, row).
+template <class FL, class FH>
+__device__ __forceinline__ double row_spmv2(const PartDev& P, const PartDev* __restrict__ parts,
+                                            int64_t i, FL&& floc, FH&& fhalo) {
+  const RowRef rr = row_ref(P, i);
+  const int n = int(P.n);
+  const int pid = __ldg(P.slice_pat + (i >> 5));   // warp-uniform
+  const int32_t* poff = P.pat_off + pid * kPatW;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < rr.w; k0 += kChunk) {
+    int c[kChunk];
+    double a[kChunk], xv[kChunk];
+    if (pid >= 0) {
+      const unsigned msk = __ldg(P.rmask + i);
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        c[u] = (k0 + u < rr.w && ((msk >> (k0 + u)) & 1u)) ? int(i) + __ldg(poff + k0 + u) : -1;
+    } else {
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u)
+        c[u] = (k0 + u < rr.w) ? __ldg(P.col + rr.base + int64_t(k0 + u) * kSlice) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      a[u] = 0.0;
+      xv[u] = 0.0;
+      if (c[u] >= 0) {
+        a[u] = __ldg(P.val + rr.base + int64_t(k0 + u) * kSlice);
+        if (c[u] < n) {
+          xv[u] = floc(int64_t(c[u]));
+        } else {
+          const int h = c[u] - n;
+          xv[u] = fhalo(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(a[u], xv[u]));
+  }
+  return acc;
+}
+
+// Staged operand of one tile (lrb_internal.h, tile_win): position of local
+// column c in the shared-memory windows, or -1.
+struct Stage {
+  const double* sm;
+  int64_t row0;
+  int s0, l0, s1, l1, s2, l2;
+  __device__ __forceinline__ int pos(int64_t c) const {
+    const int rel = int(c - row0);
+    unsigned a = unsigned(rel - s0);
+    if (a < unsigned(l0)) return int(a);
+    a = unsigned(rel - s1);
+    if (a < unsigned(l1)) return l0 + int(a);
+    a = unsigned(rel - s2);
+    if (a < unsigned(l2)) return l0 + l1 + int(a);
+    return -1;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Update: gather-permute one segment's rows from the receive buffer
@@ -177,6 +257,17 @@ __device__ __forceinline__ void block_sum(double (&acc)[NR], double (*sm)[kMaxRe
     }
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ int64_t tile_first(const TeamDev& T) {
+  return LRB_CONTIG ? int64_t(blockIdx.x) * T.n_tiles / gridDim.x : int64_t(blockIdx.x);
+}
+__device__ __forceinline__ int64_t tile_end(const TeamDev& T) {
+  return LRB_CONTIG ? (int64_t(blockIdx.x) + 1) * T.n_tiles / gridDim.x : T.n_tiles;
+}
+__device__ __forceinline__ int64_t tile_step() { return LRB_CONTIG ? 1 : int64_t(gridDim.x); }
+__device__ __forceinline__ int64_t tile_of(const TeamDev& T, int t) {
+  return tile_first(T) + int64_t(t) * tile_step();
 }
 
 __device__ void team_fail(const TeamDev& T, int code) {
@@ -315,13 +406,125 @@ __device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double
   }
 }
 
+// Elementwise phases: every row's loads of the tile are issued first
+// (load(P, i) -> L), then the updates (apply(P, i, L, acc)) — the stores of
+// one row cannot hold back the loads of the next (no aliasing proof needed).
+template <int NR, class Load, class Apply>
+struct SplitBody {
+  Load load;
+  Apply apply;
+};
+
+template <int NR, class Load, class Apply>
+__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[NR],
+                                          SplitBody<NR, Load, Apply>& body) {
+  const int64_t row0 = (tile - P.tile0) * kTile;
+  decltype(body.load(P, int64_t(0))) v[kRPT];
+#pragma unroll
+  for (int m = 0; m < kRPT; ++m) {
+    const int64_t i = row0 + m * kTPB + threadIdx.x;
+    if (i < P.n) v[m] = body.load(P, i);
+  }
+#pragma unroll
+  for (int m = 0; m < kRPT; ++m) {
+    const int64_t i = row0 + m * kTPB + threadIdx.x;
+    if (i < P.n) body.apply(P, i, v[m], acc);
+  }
+}
+
+template <int NR, class Load, class Apply>
+__device__ __forceinline__ SplitBody<NR, Load, Apply> split_body(Load&& l, Apply&& a) {
+  return SplitBody<NR, Load, Apply>{l, a};
+}
+
+// SpMV tile with the operand staged in shared memory when the tile allows it:
+// the block computes vecf(P, j) once per window element with coalesced loads,
+// then body(P, i, acc, floc) reads floc(c) from shared memory.
+template <int NR, class VecF, class Body>
+__device__ __forceinline__ void tile_rows_staged(const PartDev& P, int64_t tile, double (&acc)[NR],
+                                                 double* stage, VecF&& vecf, Body&& body) {
+  const int64_t lt = tile - P.tile0;
+  const int64_t row0 = lt * kTile;
+  const int32_t* tw = P.tile_win + lt * kWinStride;
+  const int nw = LRB_STAGE ? __ldg(tw) : 0;   // block-uniform
+  Stage S{stage, row0, 0, 0, 0, 0, 0, 0};
+  if (nw > 0) {
+    S.s0 = __ldg(tw + 2);
+    S.l0 = __ldg(tw + 3);
+    if (nw > 1) {
+      S.s1 = __ldg(tw + 4);
+      S.l1 = __ldg(tw + 5);
+    }
+    if (nw > 2) {
+      S.s2 = __ldg(tw + 6);
+      S.l2 = __ldg(tw + 7);
+    }
+    for (int q = threadIdx.x; q < S.l0; q += kTPB) stage[q] = vecf(P, row0 + S.s0 + q);
+    for (int q = threadIdx.x; q < S.l1; q += kTPB) stage[S.l0 + q] = vecf(P, row0 + S.s1 + q);
+    for (int q = threadIdx.x; q < S.l2; q += kTPB)
+      stage[S.l0 + S.l1 + q] = vecf(P, row0 + S.s2 + q);
+    __syncthreads();
+  }
+  auto floc = [&](int64_t c) -> double {
+    if (nw > 0) {
+      const int q = S.pos(c);
+      if (q >= 0) return S.sm[q];
+    }
+    return vecf(P, c);
+  };
+#pragma unroll
+  for (int m = 0; m < kRPT; ++m) {
+    const int64_t i = row0 + m * kTPB + threadIdx.x;
+    if (i < P.n) body(P, i, acc, floc);
+  }
+  if (nw > 0) __syncthreads();   // the next tile overwrites the stage
+}
+
+template <int NR, bool INL, class VecF, class Body>
+__device__ __forceinline__ void team_phase_spmv(const TeamDev& T, double* red, VecF&& vecf,
+                                                Body&& body) {
+  extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed] | stage
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tpb = (T.n_tiles + gridDim.x - 1) / gridDim.x;
+  double* stage = wsm + tpb * kWarps * kMaxRed;
+  int tl = 0;
+  for (int64_t tile = tile_first(T); tile < tile_end(T); tile += tile_step(), ++tl) {
+    const int p = __ldg(T.tile_part + tile);
+    double acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    if constexpr (INL) {
+      tile_rows_staged<NR>(T.lp[p - T.part_begin], tile, acc, stage, vecf, body);
+    } else {
+      const PartDev P = T.parts[p];
+      tile_rows_staged<NR>(P, tile, acc, stage, vecf, body);
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) wsm[(tl * kWarps + warp) * kMaxRed + j] = acc[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < tl * NR; idx += kTPB) {
+    const int t = idx / NR, j = idx - t * NR;
+    double s = wsm[(t * kWarps) * kMaxRed + j];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsm[(t * kWarps + w) * kMaxRed + j]);
+    T.partials[tile_of(T, t) * kMaxRed + j] = s;
+  }
+  team_sync<NR>(T, red);
+}
+
 // INL: local part descriptors come from the kernel parameter (T.lp).
 template <int NR, bool INL, class Body>
 __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
   extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tl = 0;
-  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x, ++tl) {
+  for (int64_t tile = tile_first(T); tile < tile_end(T); tile += tile_step(), ++tl) {
     const int p = __ldg(T.tile_part + tile);
     double acc[NR];
 #pragma unroll
@@ -346,7 +549,7 @@ __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&&
     double s = wsm[(t * kWarps) * kMaxRed + j];
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsm[(t * kWarps + w) * kMaxRed + j]);
-    T.partials[(int64_t(blockIdx.x) + int64_t(t) * gridDim.x) * kMaxRed + j] = s;
+    T.partials[tile_of(T, t) * kMaxRed + j] = s;
   }
   team_sync<NR>(T, red);
 }
@@ -403,15 +606,16 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
   int it = 0;
   for (it = 1; it <= T.max_iter; ++it) {
     // ---- phase A: p_new, q = A p_new, p.q
-    team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
-      auto pnew = [&](const PartDev& Q, int64_t j) -> double {
-        const double z = JAC ? Q.s[j] : Q.r[j];
-        if (first) return z;
-        const double po = pa ? Q.p1[j] : Q.p0[j];
-        return __dadd_rn(z, __dmul_rn(beta, po));
-      };
-      const double pi = pnew(P, i);
-      const double qi = row_spmv(P, parts, i, pnew);
+    auto pnew = [&](const PartDev& Q, int64_t j) -> double {
+      const double z = JAC ? Q.s[j] : Q.r[j];
+      if (first) return z;
+      const double po = pa ? Q.p1[j] : Q.p0[j];
+      return __dadd_rn(z, __dmul_rn(beta, po));
+    };
+    team_phase_spmv<1, INL>(T, red, pnew,
+                            [&](const PartDev& P, int64_t i, double (&acc)[1], auto&& floc) {
+      const double pi = floc(i);
+      const double qi = row_spmv2(P, parts, i, floc, pnew);
       (pa ? P.p0 : P.p1)[i] = pi;
       P.q[i] = qi;
       acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
@@ -425,19 +629,32 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
     const double step = rho / pq;
     pa ^= 1;  // p_new is now p_old for the elementwise phase and the next iteration
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
+    struct BIn {
+      double p, x, r, q, d;
+    };
+    auto phase_b = split_body<2>(
+        [&](const PartDev& P, int64_t i) -> BIn {
+          return BIn{(pa ? P.p1 : P.p0)[i], P.x[i], P.r[i], P.q[i], JAC ? P.dinv[i] : 0.0};
+        },
+        [&](const PartDev& P, int64_t i, const BIn& v, double (&acc)[2]) {
+          const double x = __dadd_rn(v.x, __dmul_rn(step, v.p));
+          const double r = __dsub_rn(v.r, __dmul_rn(step, v.q));
+          P.x[i] = x;
+          P.r[i] = r;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+          if (JAC) {
+            const double z = __dmul_rn(v.d, r);
+            P.s[i] = z;
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
+          }
+        });
+#if LRB_SPLITB
+    team_phase<2, INL>(T, red, phase_b);
+#else
     team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
-      const double p = (pa ? P.p1 : P.p0)[i];
-      const double x = __dadd_rn(P.x[i], __dmul_rn(step, p));
-      const double r = __dsub_rn(P.r[i], __dmul_rn(step, P.q[i]));
-      P.x[i] = x;
-      P.r[i] = r;
-      acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
-      if (JAC) {
-        const double z = __dmul_rn(P.dinv[i], r);
-        P.s[i] = z;
-        acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
-      }
+      phase_b.apply(P, i, phase_b.load(P, i), acc);
     });
+#endif
     if (team_failed(T)) break;
     const double rr_new = red[0];
     const double rho_new = JAC ? red[1] : rr_new;
@@ -445,9 +662,10 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
     if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
     if (rec <= T.tol || it % 10 == 0) {
       // ---- phase C: true residual |b - A x|
-      team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
-        const double ax =
-            row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
+      auto xval = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
+      team_phase_spmv<1, INL>(T, red, xval,
+                              [&](const PartDev& P, int64_t i, double (&acc)[1], auto&& floc) {
+        const double ax = row_spmv2(P, parts, i, floc, xval);
         const double d = __dsub_rn(P.b[i], ax);
         acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
       });

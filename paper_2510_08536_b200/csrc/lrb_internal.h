@@ -34,6 +34,18 @@ constexpr int kSlice = 32;
 constexpr int kPatW = 16;      // widest row a pattern may describe
 constexpr int kMaxPat = 1024;  // dictionary size
 
+// Shared-memory staging of the SpMV operand for pattern tiles: a tile's rows
+// read the vector only at row + {pattern offsets}; those indices form at most
+// kMaxWin contiguous windows (on the 7-point stencil: -plane, [-d0, d0], +plane
+// around the tile).  The block stages the windows with coalesced loads once
+// (computing p_new = z + beta*p_old once per element) and the rows read shared
+// memory instead of 14 dependent gathers each.  tile_win[t] = {n_win, total,
+// start0, len0, start1, len1, start2, len2} (starts relative to the tile's
+// first row, clipped to [0, n)); n_win = 0: no staging for that tile.
+constexpr int kMaxWin = 3;
+constexpr int kWinStride = 2 + 2 * kMaxWin;
+constexpr int kMaxStage = 4096;   // doubles of staged operand per block
+
 struct PartDev {
   int64_t n;          // owned rows
   int64_t n_halo;
@@ -43,6 +55,8 @@ struct PartDev {
   const int32_t* slice_pat;   // [n_slices] pattern id or -1
   const int32_t* pat_off;     // [n_pat * kPatW]
   const uint16_t* rmask;      // [n] occupied pattern slots of each row
+  const int32_t* tile_win;    // [ntiles_part * kWinStride] staging windows
+  int64_t max_stage;          // max staged doubles over this part's tiles
   const int32_t* col;         // [E]
   const int32_t* src;         // [E] scatter inverse (buffer position or -1)
   const int8_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
@@ -62,7 +76,10 @@ struct PartDev {
 // one part.  The per-tile partial dot products are reduced in fixed order,
 // so results do not depend on grid size or scheduling.
 constexpr int kTPB = 256;
-constexpr int kRPT = 2;
+#ifndef LRB_RPT
+#define LRB_RPT 2
+#endif
+constexpr int kRPT = LRB_RPT;
 constexpr int kTile = kTPB * kRPT;
 constexpr int kMaxRed = 4;   // reductions fused into one barrier
 
@@ -133,6 +150,8 @@ struct Plan {
   std::vector<int32_t> pat_off;             // [n_pat * kPatW]
   std::vector<uint16_t> rmask;              // [n] occupied slots of a pattern row
   std::vector<int32_t> loc_sell, nl_sell;   // SELL slot of every CSR entry
+  std::vector<int32_t> tile_win;            // [ntiles * kWinStride]
+  int64_t max_stage = 0;
   int64_t n_pat() const { return int64_t(pat_off.size()) / kPatW; }
   int64_t sell_entries() const { return slice_ptr.empty() ? 0 : slice_ptr.back(); }
 };

@@ -131,6 +131,55 @@ struct BuildError {
   }
 };
 
+// Staging windows per tile (lrb_internal.h): the union over the tile's
+// pattern slices of [row0 + off, row0 + off + rows) for every local offset,
+// clipped to [0, n), merged into at most kMaxWin sorted intervals.
+void build_tile_windows(Plan& P) {
+  const int64_t n = P.n;
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  P.tile_win.assign(ntiles * kWinStride, 0);
+  P.max_stage = 0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int64_t row0 = t * kTile, rows = std::min<int64_t>(kTile, n - row0);
+    std::vector<int32_t> offs;
+    bool ok = true;
+    for (int64_t s = row0 / kSlice; s < (row0 + rows + kSlice - 1) / kSlice && ok; ++s) {
+      const int pid = P.slice_pat[s];
+      if (pid < 0) {
+        ok = false;
+        break;
+      }
+      const int64_t w = (P.slice_ptr[s + 1] - P.slice_ptr[s]) / kSlice;
+      for (int64_t k = 0; k < w; ++k) offs.push_back(P.pat_off[pid * kPatW + k]);
+    }
+    if (!ok) continue;
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    std::vector<std::pair<int64_t, int64_t>> iv;  // [a, b) relative to row0
+    for (int32_t o : offs) {
+      int64_t a = std::max<int64_t>(row0 + o, 0), b = std::min<int64_t>(row0 + o + rows, n);
+      if (a >= b) continue;  // halo column (col >= n) or outside the part
+      a -= row0;
+      b -= row0;
+      if (!iv.empty() && a <= iv.back().second)
+        iv.back().second = std::max(iv.back().second, b);
+      else
+        iv.emplace_back(a, b);
+    }
+    int64_t total = 0;
+    for (auto& x : iv) total += x.second - x.first;
+    if (iv.empty() || int64_t(iv.size()) > kMaxWin || total > kMaxStage) continue;
+    int32_t* tw = &P.tile_win[t * kWinStride];
+    tw[0] = int32_t(iv.size());
+    tw[1] = int32_t(total);
+    for (size_t w = 0; w < iv.size(); ++w) {
+      tw[2 + 2 * w] = int32_t(iv[w].first);
+      tw[3 + 2 * w] = int32_t(iv[w].second - iv[w].first);
+    }
+    P.max_stage = std::max(P.max_stage, total);
+  }
+}
+
 template <class Gen>
 int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
           const std::vector<int64_t>& seg_off, const Gen& gen, int32_t n_gpu,
@@ -413,6 +462,7 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
       if (pid >= 0) P.rmask[r] = uint16_t(mask);
     }
   });
+  build_tile_windows(P);
   return LRB_OK;
 }
 
