@@ -179,6 +179,25 @@ int lrb_team_connect_ipc(lrb_team* team, const void* team_blobs /* n_dev x 512 *
  * state: out[0] = epoch, out[1..n_dev] = arrival flags written by peers. */
 int lrb_team_read_vector(lrb_team* team, int32_t part, int32_t vec, int64_t n, double* out);
 int lrb_team_debug(lrb_team* team, int64_t* out);
+/* Launch geometry of the solve kernel of `method` on device rank 0:
+ * out[0] = 1 streaming (bulk-copy, stream.cuh) / 0 classic (kernels.cuh),
+ * out[1] = grid, out[2] = block, out[3] = ring stages, out[4] = stage bytes,
+ * out[5] = dynamic shared memory bytes.  LRB_SOLVER=classic at team creation
+ * selects the classic kernels. */
+int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out);
+/* Phase profiling (diagnostics): with cap > 0 every later solve records the
+ * globaltimer (ns) at each team-barrier release, up to cap entries (cap = 0
+ * turns it off).  lrb_team_profile_read copies the last solve's timestamps of
+ * device rank 0 and returns their count (negative: error).  Phase order:
+ * init, then per iteration A (SpMV + p.q), B (update + r.r), [C (true
+ * residual)]. */
+int lrb_team_profile(lrb_team* team, int32_t cap);
+int lrb_team_profile_read(lrb_team* team, int64_t* out, int32_t cap);
+/* Streaming solvers with profiling on: per-CTA SM-cycle counters of the last
+ * solve of `method`, 16 per CTA = [phase kind: init, A, B, C][consumer data
+ * wait, consumer barrier, producer stage wait, team barrier]; returns the
+ * number of values copied (0: not streaming / profiling off). */
+int lrb_team_profile_counters(lrb_team* team, int32_t method, int64_t* out, int32_t cap);
 
 /* Distributed SpMV y = A x (solver.py:80-97): x_host/y_host per part. */
 int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_host);

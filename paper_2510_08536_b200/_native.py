@@ -96,6 +96,10 @@ lrb_team_create_ipc = _sig("lrb_team_create_ipc", C.c_int, I32, I32, I32, P, P, 
 lrb_team_connect_ipc = _sig("lrb_team_connect_ipc", C.c_int, P, P)
 lrb_team_read_vector = _sig("lrb_team_read_vector", C.c_int, P, I32, I32, I64, P)
 lrb_team_debug = _sig("lrb_team_debug", C.c_int, P, P)
+lrb_team_kernel_info = _sig("lrb_team_kernel_info", C.c_int, P, I32, P)
+lrb_team_profile = _sig("lrb_team_profile", C.c_int, P, I32)
+lrb_team_profile_read = _sig("lrb_team_profile_read", C.c_int, P, P, I32)
+lrb_team_profile_counters = _sig("lrb_team_profile_counters", C.c_int, P, I32, P, I32)
 lrb_team_solve = _sig("lrb_team_solve", C.c_int, P, I32, P, P, D, I32, C.POINTER(Report), P, I32)
 
 EXPORTED = [
@@ -107,7 +111,8 @@ EXPORTED = [
     "lrb_part_read_values", "lrb_part_join", "lrb_part_sync", "lrb_part_stats", "lrb_part_mark",
     "lrb_part_elapsed_ms", "lrb_team_create", "lrb_team_create_ex", "lrb_team_destroy",
     "lrb_team_spmv", "lrb_team_solve", "lrb_part_export", "lrb_team_create_ipc",
-    "lrb_team_connect_ipc", "lrb_team_read_vector", "lrb_team_debug",
+    "lrb_team_connect_ipc", "lrb_team_read_vector", "lrb_team_debug", "lrb_team_kernel_info",
+    "lrb_team_profile", "lrb_team_profile_read", "lrb_team_profile_counters",
 ]
 
 

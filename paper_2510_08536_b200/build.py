@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libldurepart_b200.so")
 SOURCES = ["plan.cpp", "device.cu"]
-HEADERS = ["lrb_internal.h", "kernels.cuh"]
+HEADERS = ["lrb_internal.h", "kernels.cuh", "stream.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",

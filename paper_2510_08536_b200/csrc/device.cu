@@ -14,7 +14,7 @@
 #include <vector>
 
 #include "../../include/ldurepart_b200.h"
-#include "kernels.cuh"
+#include "stream.cuh"
 #include "lrb_internal.h"
 
 struct lrb_plan;
@@ -94,6 +94,8 @@ struct lrb_part {
   int device = 0;
   PartDev d{};                      // device pointers (host copy)
   std::vector<int64_t> seg_off, seg_rows, slice_ptr;
+  std::vector<int32_t> tile_win;           // host copies (stage headers of the streaming solvers)
+  std::vector<int32_t> slice_pat_host;
   std::vector<int32_t> loc_sell, nl_sell;  // SELL slot of each CSR entry (value mirror)
   int64_t nnz_l = 0, nnz_n = 0;
   cudaStream_t main = nullptr;
@@ -225,6 +227,8 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   part->loc_sell = P.loc_sell;
   part->nl_sell = P.nl_sell;
   part->slice_ptr = P.slice_ptr;
+  part->tile_win = P.tile_win;
+  part->slice_pat_host = P.slice_pat;
   part->nnz_l = int64_t(P.loc_col.size());
   part->nnz_n = int64_t(P.nl_col.size());
   part->stage = host_stage;
@@ -560,6 +564,8 @@ struct TeamDevice {
   const void* fn[3] = {nullptr, nullptr, nullptr};
   int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
   size_t smem[3] = {0, 0, 0};
+  int block[3] = {kTPB, kTPB, kTPB};
+  bool streaming[3] = {false, false, false};  // streaming (bulk-copy) kernel for this method
   cudaStream_t stream = nullptr;  // main stream of the first local part
   void* ws = nullptr;             // device workspace (cudaMalloc, create time)
   TeamDev host{};                 // kernel argument
@@ -567,6 +573,8 @@ struct TeamDevice {
   SolveOut* out_dev = nullptr;
   double* hist_dev = nullptr;
   int hist_cap = 0;
+  long long* prof_dev = nullptr;  // phase timestamps (lrb_team_profile), [0] holds the count
+  int prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 
@@ -584,6 +592,12 @@ struct lrb_team {
 namespace lrb {
 
 static const void* solve_kernel(int method, bool inl);
+static const void* stream_kernel(int method, bool inl);
+static int stream_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t smem);
+static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, int* n_stages);
+static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, int stage_bytes,
+                                std::vector<StageHdr>& out);
+static int solver_choice();
 static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share,
                     int64_t stage_doubles, size_t* smem);
 
@@ -620,6 +634,13 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_peer_flags = take(sizeof(void*) * n_dev);
   const size_t o_peer_red = take(sizeof(void*) * n_dev);
   const size_t o_out = take(sizeof(SolveOut));
+  // streaming solvers: stage size from the largest stageable tile, and the
+  // per-tile stage headers
+  const bool want_stream = solver_choice() != 1;
+  int n_stages = 0;
+  const int stage_bytes = want_stream ? stream_stage_bytes(D, by_index, &n_stages) : 0;
+  const bool use_stream = want_stream && n_stages >= 2;
+  const size_t o_hdr = use_stream ? take(sizeof(StageHdr) * n_tiles) : 0;
   LRB_CUDA(cudaMalloc(&D.ws, bytes));
   LRB_CUDA(cudaMemset(D.ws, 0, bytes));
   D.ws_bytes = bytes;
@@ -660,12 +681,28 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   if (D.inl)
     for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
   D.cooperative = (n_share == 1);
-  int64_t stage = 0;   // staged-operand shared memory: the largest local part's
-  if (LRB_STAGE)
-    for (int p : D.parts) stage = std::max<int64_t>(stage, by_index[p]->d.max_stage);
+  const int64_t stage = 0;   // classic kernels: no staged operand
+  H.stage_bytes = stage_bytes;
+  H.n_stages = n_stages;
+  H.tile_hdr = nullptr;
+  if (use_stream) {
+    std::vector<StageHdr> hdr;
+    build_stage_headers(D, by_index, stage_bytes, hdr);
+    H.tile_hdr = w + o_hdr;
+    LRB_CUDA(cudaMemcpy(w + o_hdr, hdr.data(), sizeof(StageHdr) * hdr.size(), cudaMemcpyHostToDevice));
+  }
   for (int m = 0; m < 3; ++m) {
-    D.fn[m] = solve_kernel(m, D.inl);
-    D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
+    const void* sfn = use_stream ? stream_kernel(m, D.inl) : nullptr;
+    if (sfn) {
+      D.fn[m] = sfn;
+      D.block[m] = kStreamThreads;
+      D.streaming[m] = true;
+      D.smem[m] = stream_smem_bytes(stage_bytes, n_stages);
+      D.grid[m] = stream_grid(sfn, D.device, D.n_tiles, n_share, D.smem[m]);
+    } else {
+      D.fn[m] = solve_kernel(m, D.inl);
+      D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
+    }
     if (D.grid[m] <= 0) {
       set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
       return LRB_ERUNTIME;
@@ -737,6 +774,112 @@ static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share
     }
   }
   return -2;
+}
+
+// LRB_SOLVER=classic selects the per-thread-gather kernels (kernels.cuh);
+// default: the streaming kernels (stream.cuh) where a method has one.
+static int solver_choice() {
+  const char* e = getenv("LRB_SOLVER");
+  if (e && std::strcmp(e, "classic") == 0) return 1;
+  return 0;
+}
+
+static const void* stream_kernel(int method, bool inl) {
+  switch (method) {
+    case LRB_METHOD_CG:
+      return inl ? (const void*)team_cg_stream_kernel<false, true>
+                 : (const void*)team_cg_stream_kernel<false, false>;
+    case LRB_METHOD_PCG:
+      return inl ? (const void*)team_cg_stream_kernel<true, true>
+                 : (const void*)team_cg_stream_kernel<true, false>;
+    default:
+      return nullptr;
+  }
+}
+
+// Geometry of one tile as the streaming producer stages it (StageHdr without
+// the staging decision); need = the largest stage any phase asks for.
+static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int64_t dev_tile,
+                             StageHdr& h) {
+  std::memset(&h, 0, sizeof(h));
+  const int64_t n = P->d.n;
+  const int64_t row0 = lt * kTile, rows = std::min<int64_t>(kTile, n - row0);
+  const int64_t s0 = row0 / kSlice, s1 = (row0 + rows + kSlice - 1) / kSlice;
+  h.row0 = row0;
+  h.rows = int32_t(rows);
+  h.part = part_index;
+  h.tile = int32_t(dev_tile);
+  h.e0 = P->slice_ptr[s0];
+  h.vbytes = int32_t(8 * (P->slice_ptr[s1] - P->slice_ptr[s0]));
+  for (int64_t s = s0; s <= s1; ++s) h.sp[s - s0] = int32_t(P->slice_ptr[s] - P->slice_ptr[s0]);
+  const bool have_win = int64_t(P->tile_win.size()) >= (lt + 1) * kWinStride;
+  const int32_t* tw = have_win ? &P->tile_win[lt * kWinStride] : nullptr;
+  h.nw = tw ? tw[0] : 0;
+  int64_t wtot = 0;
+  for (int w = 0; w < h.nw; ++w) {
+    const int64_t a = row0 + tw[2 + 2 * w], l = tw[3 + 2 * w];
+    const int64_t a2 = a & ~int64_t(1), b2 = (a + l + 1) & ~int64_t(1);
+    h.wa[w] = a2;
+    h.wl[w] = int32_t(b2 - a2);
+    h.woff[w] = int32_t(wtot);
+    wtot += b2 - a2;
+  }
+  h.wtot = int32_t(wtot);
+  if (h.nw <= 0) return 0;
+  const int64_t base = kHdrBytes + h.vbytes + kMaskBytes;
+  return std::max(base + 2 * wtot * 8, base + wtot * 8 + kVecTileBytes);
+}
+
+// Largest stage any phase needs for a stageable tile of this device's parts,
+// and how many stages fit in shared memory (at least two, else no streaming).
+static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, int* n_stages) {
+  int dev_smem = 0;
+  cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, D.device);
+  const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - 1024;
+  const int64_t cap = budget / 2;   // at least double-buffered
+  int64_t best = kHdrBytes + 5 * kVecTileBytes;   // elementwise phases
+  StageHdr h;
+  for (int p : D.parts) {
+    const lrb_part* P = by_index[p];
+    const int64_t ntiles = (P->d.n + kTile - 1) / kTile;
+    for (int64_t lt = 0; lt < ntiles; ++lt) {
+      const int64_t need = tile_geometry(P, lt, p, 0, h);
+      if (need > 0 && need <= cap) best = std::max(best, need);
+    }
+  }
+  best = (best + 127) & ~int64_t(127);
+  *n_stages = int(std::min<int64_t>(kStreamMaxStages, budget / best));
+  return int(best);
+}
+
+// One StageHdr per device tile; tiles without windows, or larger than a
+// stage, are marked for the consumers' direct-load path (tma = 0).
+static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, int stage_bytes,
+                                std::vector<StageHdr>& out) {
+  out.assign(size_t(std::max<int64_t>(D.n_tiles, 1)), StageHdr{});
+  for (int p : D.parts) {
+    const lrb_part* P = by_index[p];
+    for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
+      StageHdr& h = out[P->d.tile0 + lt];
+      const int64_t need = tile_geometry(P, lt, p, P->d.tile0 + lt, h);
+      h.tma = (need > 0 && need <= stage_bytes) ? 1 : 0;
+      const int64_t s0 = h.row0 / kSlice, nsl = (h.rows + kSlice - 1) / kSlice;
+      for (int64_t s = 0; s < nsl; ++s) h.pat[s] = P->slice_pat_host[s0 + s];
+    }
+  }
+}
+
+static int stream_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t smem) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    return -1;
+  int fit = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kernel, kStreamThreads, smem) != cudaSuccess ||
+      fit < 1)
+    return -2;
+  const int64_t cap = int64_t(sms) * fit / std::max(n_share, 1);
+  return int(std::max<int64_t>(1, std::min<int64_t>(cap, std::max<int64_t>(n_tiles, 1))));
 }
 
 }  // namespace lrb
@@ -1046,6 +1189,82 @@ int lrb_team_debug(lrb_team* team, int64_t* out) {
   return LRB_OK;
 }
 
+int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out) {
+  if (!team || !out || method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+    set_error("lrb_team_kernel_info: bad arguments");
+    return LRB_EVALUE;
+  }
+  const TeamDevice& D = team->devs[0];
+  out[0] = D.streaming[method] ? 1 : 0;
+  out[1] = D.grid[method];
+  out[2] = D.block[method];
+  out[3] = D.streaming[method] ? D.host.n_stages : 0;
+  out[4] = D.streaming[method] ? D.host.stage_bytes : 0;
+  out[5] = int64_t(D.smem[method]);
+  return LRB_OK;
+}
+
+int lrb_team_profile(lrb_team* team, int32_t cap) {
+  if (!team || cap < 0) {
+    set_error("lrb_team_profile: bad arguments");
+    return LRB_EVALUE;
+  }
+  std::lock_guard<std::mutex> lk(team->mu);
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    if (D.prof_dev) cudaFree(D.prof_dev);
+    D.prof_dev = nullptr;
+    D.prof_cap = 0;
+    D.host.prof = nullptr;
+    D.host.prof_n = nullptr;
+    D.host.prof_cap = 0;
+    D.host.prof_cta = nullptr;
+    if (cap > 0) {
+      const size_t extra = size_t(*std::max_element(D.grid, D.grid + 3)) * kCnt;
+      const size_t words = size_t(cap) + 1 + extra;
+      LRB_CUDA(cudaMalloc(&D.prof_dev, sizeof(long long) * words));
+      LRB_CUDA(cudaMemset(D.prof_dev, 0, sizeof(long long) * words));
+      D.prof_cap = cap;
+      D.host.prof = D.prof_dev + 1;
+      D.host.prof_cta = D.prof_dev + 1 + cap;
+      D.host.prof_n = reinterpret_cast<int32_t*>(D.prof_dev);
+      D.host.prof_cap = cap;
+    }
+  }
+  return LRB_OK;
+}
+
+int lrb_team_profile_read(lrb_team* team, int64_t* out, int32_t cap) {
+  if (!team || !out || cap < 0) {
+    set_error("lrb_team_profile_read: bad arguments");
+    return LRB_EVALUE;
+  }
+  const TeamDevice& D = team->devs[0];
+  if (!D.prof_dev) return 0;
+  DeviceGuard g(D.device);
+  std::vector<long long> buf(size_t(D.prof_cap) + 1);
+  LRB_CUDA(cudaMemcpy(buf.data(), D.prof_dev, sizeof(long long) * buf.size(), cudaMemcpyDeviceToHost));
+  const int n = std::min<int>(int(*reinterpret_cast<int32_t*>(buf.data())), std::min(cap, D.prof_cap));
+  for (int i = 0; i < n; ++i) out[i] = int64_t(buf[1 + i]);
+  return n;
+}
+
+int lrb_team_profile_counters(lrb_team* team, int32_t method, int64_t* out, int32_t cap) {
+  if (!team || !out || method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+    set_error("lrb_team_profile_counters: bad arguments");
+    return LRB_EVALUE;
+  }
+  const TeamDevice& D = team->devs[0];
+  if (!D.prof_dev || !D.streaming[method]) return 0;
+  DeviceGuard g(D.device);
+  const int n = std::min(cap, D.grid[method] * kCnt);
+  std::vector<long long> buf(size_t(std::max(n, 0)));
+  if (n > 0)
+    LRB_CUDA(cudaMemcpy(buf.data(), D.host.prof_cta, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) out[i] = int64_t(buf[i]);
+  return n;
+}
+
 int lrb_team_create(int32_t n_parts, lrb_part* const* parts, lrb_team** out) {
   return lrb_team_create_ex(n_parts, parts, nullptr, out);
 }
@@ -1058,6 +1277,7 @@ void lrb_team_destroy(lrb_team* team) {
     DeviceGuard g(D.device);
     if (D.ws) cudaFree(D.ws);
     if (D.hist_dev) cudaFree(D.hist_dev);
+    if (D.prof_dev) cudaFree(D.prof_dev);
     if (D.t0) cudaEventDestroy(D.t0);
     if (D.t1) cudaEventDestroy(D.t1);
   }
@@ -1173,6 +1393,7 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
           LRB_CUDA(cudaMemcpyAsync(P->d.b, b_host[p], 8 * P->d.n, cudaMemcpyHostToDevice, D.stream));
       }
     LRB_CUDA(cudaMemsetAsync(D.out_dev, 0, sizeof(SolveOut), D.stream));
+    if (D.prof_dev) LRB_CUDA(cudaMemsetAsync(D.prof_dev, 0, sizeof(long long), D.stream));
     TeamDev& H = D.host;
     H.tol = tol;
     H.max_iter = max_iter;
@@ -1196,9 +1417,9 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     if (!D.cooperative) {
       // several device ranks share this GPU (test mode): each grid is sized
       // to a share of one wave (max_grid), so they are co-resident
-      LRB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));
+      LRB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(D.block[method]), args, smem, D.stream));
     } else {
-      LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kTPB), args, smem, D.stream));
+      LRB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(D.block[method]), args, smem, D.stream));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     LRB_CUDA(cudaEventRecord(D.t1, D.stream));

@@ -74,13 +74,6 @@ constexpr int kChunk = LRB_CHUNK;
 #ifndef LRB_SPLITB
 #define LRB_SPLITB 0
 #endif
-// Shared-memory staging of the SpMV operand (tile_win).  Measured slower than
-// the L1-cached gathers on the 7-point stencil (13.4 vs 11.9 ms, C3): the
-// +-1 / +-d0 neighbours already hit L1, staging routes them through L2 and
-// adds two block barriers per tile.  Kept for irregular patterns.
-#ifndef LRB_STAGE
-#define LRB_STAGE 0
-#endif
 // Tiles of a phase: grid-strided (default: the whole grid sweeps the rows as
 // one wavefront, so a row's +-plane neighbours are fetched into L2 by another
 // block at about the same time) or contiguous per block (measured 11% slower
@@ -176,24 +169,6 @@ __device__ __forceinline__ double row_spmv2(const PartDev& P, const PartDev* __r
   return acc;
 }
 
-// Staged operand of one tile (lrb_internal.h, tile_win): position of local
-// column c in the shared-memory windows, or -1.
-struct Stage {
-  const double* sm;
-  int64_t row0;
-  int s0, l0, s1, l1, s2, l2;
-  __device__ __forceinline__ int pos(int64_t c) const {
-    const int rel = int(c - row0);
-    unsigned a = unsigned(rel - s0);
-    if (a < unsigned(l0)) return int(a);
-    a = unsigned(rel - s1);
-    if (a < unsigned(l1)) return l0 + int(a);
-    a = unsigned(rel - s2);
-    if (a < unsigned(l2)) return l0 + l1 + int(a);
-    return -1;
-  }
-};
-
 // ---------------------------------------------------------------------------
 // Update: gather-permute one segment's rows from the receive buffer
 // (apply_scatter, update.py:105-112).  One thread per row; a warp covers one
@@ -237,23 +212,69 @@ __global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ p
 // ---------------------------------------------------------------------------
 // Team barrier with fused deterministic reduction.
 // ---------------------------------------------------------------------------
-template <int NR>
-__device__ __forceinline__ void block_sum(double (&acc)[NR], double (*sm)[kMaxRed]) {
+// Part value from its tile partials (canonical order, both solver families):
+// kRedLanes virtual lanes; lane v sums tiles v, v + kRedLanes, ... in order
+// (from 0.0); each group of 32 lanes is butterfly-reduced and the group sums
+// are added in group order.  A block runs it with LPT lanes per thread
+// (v = tid + q * kRedLanes / LPT): the classic kernels (256 threads) LPT = 2,
+// the streaming kernels (512 consumer threads) LPT = 1.  Loads are issued in
+// batches so a lane's chain costs ceil(tiles / kRedLanes / batch) L2 trips.
+constexpr int kRedLanes = 512;
+constexpr int kRedGroups = kRedLanes / 32;
+
+template <int NR, int LPT>
+__device__ __forceinline__ void part_value(const double* __restrict__ partials, int64_t ntiles,
+                                           double (*gs)[kMaxRed], double* out) {
+  constexpr int kThreads = kRedLanes / LPT;
+  constexpr int kBatch = NR <= 2 ? 16 : 8;
+  constexpr int kH = (NR + 1) / 2;
+  double acc[LPT][NR];
 #pragma unroll
-  for (int j = 0; j < NR; ++j)
+  for (int q = 0; q < LPT; ++q)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
+    for (int j = 0; j < NR; ++j) acc[q][j] = 0.0;
+  if (threadIdx.x < kThreads) {
+    const double2* base = reinterpret_cast<const double2*>(partials);
 #pragma unroll
-    for (int j = 0; j < NR; ++j) sm[w][j] = acc[j];
+    for (int q = 0; q < LPT; ++q) {
+      const int64_t v = threadIdx.x + int64_t(q) * kThreads;
+      for (int64_t t0 = v; t0 < ntiles; t0 += int64_t(kBatch) * kRedLanes) {
+        double2 x[kBatch][kH];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int64_t t = t0 + int64_t(u) * kRedLanes;
+#pragma unroll
+          for (int h = 0; h < kH; ++h)
+            x[u][h] = t < ntiles ? __ldcg(base + t * (kMaxRed / 2) + h) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          if (t0 + int64_t(u) * kRedLanes >= ntiles) break;
+#pragma unroll
+          for (int j = 0; j < NR; ++j) acc[q][j] = __dadd_rn(acc[q][j], (j & 1) ? x[u][j / 2].y : x[u][j / 2].x);
+        }
+      }
+    }
+  }
+  // all warps shuffle (the extra producer warp with zeros), only lane groups vote
+#pragma unroll
+  for (int q = 0; q < LPT; ++q) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q][j] = __dadd_rn(acc[q][j], __shfl_xor_sync(0xffffffffu, acc[q][j], o));
+    const int g = int(threadIdx.x >> 5) + q * (kThreads / 32);
+    if ((threadIdx.x & 31) == 0 && threadIdx.x < kThreads)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) gs[g][j] = acc[q][j];
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      double s = sm[0][j];
-      for (int q = 1; q < kTPB / 32; ++q) s = __dadd_rn(s, sm[q][j]);
-      acc[j] = s;
+      double s = gs[0][j];
+      for (int g = 1; g < kRedGroups; ++g) s = __dadd_rn(s, gs[g][j]);
+      out[j] = s;
     }
   }
   __syncthreads();
@@ -278,10 +299,11 @@ __device__ void team_fail(const TeamDev& T, int code) {
 // every local part in fixed order, exchanges part values with the peer devices
 // (NVLink peer stores + release/acquire flags), sums all parts in ascending
 // GPU rank and releases everybody.  Returns the team-reduced values in red[].
-template <int NR>
+template <int NR, int LPT>
 __device__ void team_sync(const TeamDev& T, double* red) {
   __shared__ unsigned s_last, s_gen;
-  __shared__ double sm[kTPB / 32][kMaxRed];
+  __shared__ double gs[kRedGroups][kMaxRed];
+  __shared__ double pv[kMaxRed];
   __syncthreads();
   if (threadIdx.x == 0) {
     s_gen = vload(T.bar_gen);
@@ -303,36 +325,13 @@ __device__ void team_sync(const TeamDev& T, double* red) {
     const int64_t pbuf = int64_t(e_next & 1) * T.n_parts * kMaxRed;
     for (int p = T.part_begin; p < T.part_end; ++p) {
       const PartDev& P = T.parts[p];
-      double acc[NR];
-#pragma unroll
-      for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-      // thread t sums tiles t, t+kTPB, ... in order; 8 tiles' loads in flight
-      // (L2, bypassing L1) before the ordered adds
-      const double2* base = reinterpret_cast<const double2*>(T.partials + P.tile0 * kMaxRed);
-      for (int64_t t0 = threadIdx.x; t0 < P.ntiles; t0 += 8 * kTPB) {
-        double2 v[8][(NR + 1) / 2];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t t = t0 + int64_t(u) * kTPB;
-#pragma unroll
-          for (int h = 0; h < (NR + 1) / 2; ++h)
-            v[u][h] = t < P.ntiles ? __ldcg(base + t * (kMaxRed / 2) + h) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (t0 + int64_t(u) * kTPB >= P.ntiles) break;
-#pragma unroll
-          for (int j = 0; j < NR; ++j)
-            acc[j] = __dadd_rn(acc[j], (j & 1) ? v[u][j / 2].y : v[u][j / 2].x);
-        }
-      }
-      block_sum<NR>(acc, sm);
+      part_value<NR, LPT>(T.partials + P.tile0 * kMaxRed, P.ntiles, gs, pv);
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          T.part_red[pbuf + p * kMaxRed + j] = acc[j];
+          T.part_red[pbuf + p * kMaxRed + j] = pv[j];
           for (int d = 0; d < T.n_dev; ++d)
-            if (d != T.dev_rank) T.peer_part_red[d][pbuf + p * kMaxRed + j] = acc[j];
+            if (d != T.dev_rank) T.peer_part_red[d][pbuf + p * kMaxRed + j] = pv[j];
         }
       }
     }
@@ -363,6 +362,7 @@ __device__ void team_sync(const TeamDev& T, double* red) {
           s = __dadd_rn(s, vload(T.part_red + pbuf + p * kMaxRed + j));
         T.red[j] = s;
       }
+      if (T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
       *T.bar_count = 0;
       __threadfence();
       atomicAdd(T.bar_gen, 1u);
@@ -383,26 +383,37 @@ __device__ void team_sync(const TeamDev& T, double* red) {
   for (int j = 0; j < NR; ++j) red[j] = vload(T.red + j);
 }
 
-// Tile-loop helper: runs body(P, i, acc) over every row of every tile of this
-// block, then team-syncs.  Warps never wait for each other inside a phase:
-// each warp butterfly-reduces its share of a tile and parks it in shared
-// memory; after the last tile the block sums each tile's warp partials in
-// fixed warp order.  Row order, trees and orders are fixed, so the per-tile
-// partials are deterministic and independent of the grid size.
+// Tile partials.  Canonical tree (shared by the classic and the streaming
+// solvers, stream.cuh): a tile's kTile rows form kGroups groups of 32
+// consecutive rows; each group's row values are butterfly-reduced (xor 16, 8,
+// 4, 2, 1) and the tile partial is the sum of the group sums in group order.
+// Warps never wait for each other inside a phase: group sums are parked in
+// shared memory and summed per tile after the block's last tile.  Row order,
+// trees and orders are fixed, so the per-tile partials are deterministic and
+// independent of the grid size and of the kernel family.
 constexpr int kWarps = kTPB / 32;
+constexpr int kGroups = kTile / 32;
 
 __host__ __device__ constexpr size_t phase_smem_bytes(int64_t tiles_per_block) {
-  return size_t(tiles_per_block) * kWarps * kMaxRed * sizeof(double);
+  return size_t(tiles_per_block) * kGroups * kMaxRed * sizeof(double);
+}
+
+template <int NR>
+__device__ __forceinline__ void group_reduce(double (&acc)[NR]) {
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
 }
 
 template <int NR, class Body>
-__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[NR],
+__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[kRPT][NR],
                                           Body&& body) {
   const int64_t row0 = (tile - P.tile0) * kTile;
 #pragma unroll
   for (int m = 0; m < kRPT; ++m) {
     const int64_t i = row0 + m * kTPB + threadIdx.x;
-    if (i < P.n) body(P, i, acc);
+    if (i < P.n) body(P, i, acc[m]);
   }
 }
 
@@ -416,7 +427,7 @@ struct SplitBody {
 };
 
 template <int NR, class Load, class Apply>
-__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[NR],
+__device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double (&acc)[kRPT][NR],
                                           SplitBody<NR, Load, Apply>& body) {
   const int64_t row0 = (tile - P.tile0) * kTile;
   decltype(body.load(P, int64_t(0))) v[kRPT];
@@ -428,7 +439,7 @@ __device__ __forceinline__ void tile_rows(const PartDev& P, int64_t tile, double
 #pragma unroll
   for (int m = 0; m < kRPT; ++m) {
     const int64_t i = row0 + m * kTPB + threadIdx.x;
-    if (i < P.n) body.apply(P, i, v[m], acc);
+    if (i < P.n) body.apply(P, i, v[m], acc[m]);
   }
 }
 
@@ -437,98 +448,20 @@ __device__ __forceinline__ SplitBody<NR, Load, Apply> split_body(Load&& l, Apply
   return SplitBody<NR, Load, Apply>{l, a};
 }
 
-// SpMV tile with the operand staged in shared memory when the tile allows it:
-// the block computes vecf(P, j) once per window element with coalesced loads,
-// then body(P, i, acc, floc) reads floc(c) from shared memory.
-template <int NR, class VecF, class Body>
-__device__ __forceinline__ void tile_rows_staged(const PartDev& P, int64_t tile, double (&acc)[NR],
-                                                 double* stage, VecF&& vecf, Body&& body) {
-  const int64_t lt = tile - P.tile0;
-  const int64_t row0 = lt * kTile;
-  const int32_t* tw = P.tile_win + lt * kWinStride;
-  const int nw = LRB_STAGE ? __ldg(tw) : 0;   // block-uniform
-  Stage S{stage, row0, 0, 0, 0, 0, 0, 0};
-  if (nw > 0) {
-    S.s0 = __ldg(tw + 2);
-    S.l0 = __ldg(tw + 3);
-    if (nw > 1) {
-      S.s1 = __ldg(tw + 4);
-      S.l1 = __ldg(tw + 5);
-    }
-    if (nw > 2) {
-      S.s2 = __ldg(tw + 6);
-      S.l2 = __ldg(tw + 7);
-    }
-    for (int q = threadIdx.x; q < S.l0; q += kTPB) stage[q] = vecf(P, row0 + S.s0 + q);
-    for (int q = threadIdx.x; q < S.l1; q += kTPB) stage[S.l0 + q] = vecf(P, row0 + S.s1 + q);
-    for (int q = threadIdx.x; q < S.l2; q += kTPB)
-      stage[S.l0 + S.l1 + q] = vecf(P, row0 + S.s2 + q);
-    __syncthreads();
-  }
-  auto floc = [&](int64_t c) -> double {
-    if (nw > 0) {
-      const int q = S.pos(c);
-      if (q >= 0) return S.sm[q];
-    }
-    return vecf(P, c);
-  };
-#pragma unroll
-  for (int m = 0; m < kRPT; ++m) {
-    const int64_t i = row0 + m * kTPB + threadIdx.x;
-    if (i < P.n) body(P, i, acc, floc);
-  }
-  if (nw > 0) __syncthreads();   // the next tile overwrites the stage
-}
-
-template <int NR, bool INL, class VecF, class Body>
-__device__ __forceinline__ void team_phase_spmv(const TeamDev& T, double* red, VecF&& vecf,
-                                                Body&& body) {
-  extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed] | stage
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tpb = (T.n_tiles + gridDim.x - 1) / gridDim.x;
-  double* stage = wsm + tpb * kWarps * kMaxRed;
-  int tl = 0;
-  for (int64_t tile = tile_first(T); tile < tile_end(T); tile += tile_step(), ++tl) {
-    const int p = __ldg(T.tile_part + tile);
-    double acc[NR];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-    if constexpr (INL) {
-      tile_rows_staged<NR>(T.lp[p - T.part_begin], tile, acc, stage, vecf, body);
-    } else {
-      const PartDev P = T.parts[p];
-      tile_rows_staged<NR>(P, tile, acc, stage, vecf, body);
-    }
-#pragma unroll
-    for (int j = 0; j < NR; ++j)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < NR; ++j) wsm[(tl * kWarps + warp) * kMaxRed + j] = acc[j];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < tl * NR; idx += kTPB) {
-    const int t = idx / NR, j = idx - t * NR;
-    double s = wsm[(t * kWarps) * kMaxRed + j];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsm[(t * kWarps + w) * kMaxRed + j]);
-    T.partials[tile_of(T, t) * kMaxRed + j] = s;
-  }
-  team_sync<NR>(T, red);
-}
-
+// Tile loop of one phase, then the team barrier with the fused reduction.
 // INL: local part descriptors come from the kernel parameter (T.lp).
 template <int NR, bool INL, class Body>
 __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
-  extern __shared__ double wsm[];   // [tiles of this block][kWarps][kMaxRed]
+  extern __shared__ double wsm[];   // [tiles of this block][kGroups][kMaxRed]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tl = 0;
   for (int64_t tile = tile_first(T); tile < tile_end(T); tile += tile_step(), ++tl) {
     const int p = __ldg(T.tile_part + tile);
-    double acc[NR];
+    double acc[kRPT][NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    for (int m = 0; m < kRPT; ++m)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[m][j] = 0.0;
     if constexpr (INL) {
       tile_rows<NR>(T.lp[p - T.part_begin], tile, acc, body);
     } else {
@@ -536,22 +469,31 @@ __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&&
       tile_rows<NR>(P, tile, acc, body);
     }
 #pragma unroll
-    for (int j = 0; j < NR; ++j)
+    for (int m = 0; m < kRPT; ++m) {
+      group_reduce<NR>(acc[m]);
+      if (lane == 0)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
-    if (lane == 0)
-#pragma unroll
-      for (int j = 0; j < NR; ++j) wsm[(tl * kWarps + warp) * kMaxRed + j] = acc[j];
+        for (int j = 0; j < NR; ++j) wsm[(tl * kGroups + m * kWarps + warp) * kMaxRed + j] = acc[m][j];
+    }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < tl * NR; idx += kTPB) {
     const int t = idx / NR, j = idx - t * NR;
-    double s = wsm[(t * kWarps) * kMaxRed + j];
+    double s = wsm[(t * kGroups) * kMaxRed + j];
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsm[(t * kWarps + w) * kMaxRed + j]);
+    for (int g = 1; g < kGroups; ++g) s = __dadd_rn(s, wsm[(t * kGroups + g) * kMaxRed + j]);
     T.partials[tile_of(T, t) * kMaxRed + j] = s;
   }
-  team_sync<NR>(T, red);
+  team_sync<NR, kRedLanes / kTPB>(T, red);
+}
+
+// SpMV phase: body(P, i, acc, floc) with floc(c) = vecf(P, c) for local columns.
+template <int NR, bool INL, class VecF, class Body>
+__device__ __forceinline__ void team_phase_spmv(const TeamDev& T, double* red, VecF&& vecf,
+                                                Body&& body) {
+  team_phase<NR, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[NR]) {
+    body(P, i, acc, [&](int64_t c) { return vecf(P, c); });
+  });
 }
 
 __device__ __forceinline__ bool team_failed(const TeamDev& T) {

@@ -83,6 +83,29 @@ constexpr int kRPT = LRB_RPT;
 constexpr int kTile = kTPB * kRPT;
 constexpr int kMaxRed = 4;   // reductions fused into one barrier
 
+// Per-tile header of the streaming solvers (stream.cuh), precomputed at team
+// creation and bulk-copied into the shared-memory stage with the tile's data.
+constexpr int kHdrBytes = 256;
+struct alignas(16) StageHdr {
+  int64_t row0;          // first row of the tile (part-local)
+  int64_t e0;            // first SELL entry of the tile
+  int64_t wa[kMaxWin];   // aligned start of each operand window (part-local row)
+  int32_t rows;
+  int32_t part;          // team part index
+  int32_t tile;          // device tile index
+  int32_t tma;           // 1: values + windows staged; 0: direct global loads
+  int32_t nw;            // windows
+  int32_t wtot;          // staged elements per window vector (even)
+  int32_t wl[kMaxWin];   // aligned window lengths (even)
+  int32_t woff[kMaxWin]; // window offsets inside a vector's staged run
+  int32_t vbytes;        // staged value bytes
+  int32_t pad_;
+  int32_t sp[kTile / kSlice + 1];   // slice entry offsets relative to e0
+  int32_t pat[kTile / kSlice];      // slice pattern ids
+  int32_t reserved_[(kHdrBytes - 228) / 4];
+};
+static_assert(sizeof(StageHdr) == kHdrBytes, "stage header must be exactly kHdrBytes");
+
 enum Method { kCG = 0, kPCG = 1, kBiCGStab = 2 };
 
 struct SolveOut {
@@ -124,6 +147,14 @@ struct TeamDev {
   double* hist;             // [hist_cap] recurrence residual per iteration (nullable)
   int32_t hist_cap;
   int32_t max_iter;
+  const void* tile_hdr;     // streaming solvers: StageHdr per device tile
+  long long* prof;          // phase-release timestamps (nullable, diagnostics)
+  long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)
+  int32_t* prof_n;
+  int32_t prof_cap;
+  int32_t pad2_;
+  int32_t stage_bytes;      // streaming solvers: bytes of one shared-memory stage
+  int32_t n_stages;         //   and ring depth (stream.cuh); 0 for the classic kernels
   double tol;
   long long timeout_ns;
   PartDev lp[kInlineParts];  // local parts [part_begin, part_end) when they fit

@@ -1,0 +1,619 @@
+// Streaming (warp-specialized) persistent Krylov solvers for sm_100a.
+//
+// Same algorithms, rounding contract, tile decomposition and reduction order as
+// the classic team kernels in kernels.cuh (so both produce bit-identical
+// iterates), but the HBM traffic is moved by the bulk-copy engine instead of
+// per-thread gathers:
+//
+//   * one CTA per SM: 16 consumer warps (one thread per tile row; warp g is
+//     group g of the canonical tile tree, kernels.cuh) + 1 producer warp;
+//   * the producer walks this CTA's tiles of the current phase and, per tile,
+//     issues cp.async.bulk copies global -> shared into a ring of n_stages
+//     stages, each completing on the stage's "full" mbarrier (expect_tx):
+//       SpMV phases : the tile's SELL values (one contiguous run), its row
+//                     masks, and the <= kMaxWin operand windows of each vector
+//                     the phase reads (tile_win, plan.cpp), + tile vectors;
+//       elementwise : the tile's slice of every vector the phase reads;
+//   * consumers wait on "full", compute from shared memory, store results with
+//     coalesced st.global, and release the stage on its "empty" mbarrier;
+//   * phases end in the same deterministic team barrier/reduction (team_sync).
+//
+// A tile whose pattern is not stageable (no windows: irregular slices, or too
+// large for a stage) is computed by the consumers with direct global loads,
+// exactly like the classic kernel.  Non-local (halo) columns are always read
+// directly from the owning part (peer memory for other devices).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace lrb {
+
+constexpr int kConsumers = kTile;               // one consumer thread per tile row (16 warps)
+constexpr int kStreamThreads = kConsumers + 32;  // + one producer warp
+constexpr int kMaskBytes = kTile * 2;          // uint16 row masks of a tile
+constexpr int kVecTileBytes = kTile * 8;       // one vector's rows of a tile
+constexpr int kStreamMaxStages = 4;
+constexpr int kConsumerBar = 1;                // named barrier of the consumer warps
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Spin on an mbarrier phase.  A ring that never completes is a bug, not a
+// slow peer: after timeout_ns the kernel traps (a clean launch error instead
+// of a hung device).
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, long long timeout_ns) {
+  if (mbar_try_wait(b, parity)) return;
+  const long long t0 = global_ns();
+  for (unsigned k = 1;; ++k) {
+    if (mbar_try_wait(b, parity)) return;
+    if ((k & 1023u) == 0 && global_ns() - t0 > timeout_ns) __trap();
+  }
+}
+// 1D bulk copy global -> shared (TMA engine), completes tx bytes on bar.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
+}
+
+// Ring position shared by producer and consumers (both walk the same tiles).
+struct Ring {
+  int stage = 0;
+  unsigned phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++stage == n) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+struct StreamSmem {
+  char* stages;        // n_stages * stage_bytes
+  uint64_t* full;      // [n_stages]
+  uint64_t* empty;     // [n_stages]
+  double* wpart;       // [2][kGroups][kMaxRed]
+  unsigned long long* cnt;   // [kCnt] wait-cycle counters (diagnostics, T.prof_cta)
+};
+// Diagnostic counters per CTA: [phase kind (0 init, 1 A, 2 B, 3 C)][what]
+// what: 0 consumer warp 0 waiting for data, 1 consumer barrier, 2 producer
+// waiting for a free stage, 3 team barrier (thread 0, arrival -> release).
+constexpr int kCnt = 16;
+
+__device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool inl) {
+  return inl ? T.lp[p - T.part_begin] : T.parts[p];
+}
+
+// What one phase stages: window vectors (SpMV phases) and whole-tile vectors.
+struct Spec {
+  int nwv;                 // window vectors (0: elementwise phase)
+  int ntv;                 // tile vectors
+  const double* wv[2];
+  const double* tv[5];
+};
+
+__device__ __forceinline__ int stage_tail_offset(const StageHdr& H, int nwv) {
+  return nwv ? kHdrBytes + H.vbytes + kMaskBytes + nwv * H.wtot * 8 : kHdrBytes;
+}
+
+// ---------------------------------------------------------------------------
+// Producer: warp 8, lane 0.  Tile headers are precomputed at team creation
+// (T.tile_hdr, one StageHdr per device tile); the producer reads the next
+// tile's addressing fields one tile ahead (their latency hides behind the
+// current tile's copies) and bulk-copies the header itself into the stage.
+// ---------------------------------------------------------------------------
+struct HdrAddr {   // the fields the producer needs, 48 bytes
+  int64_t row0, e0;
+  int64_t wa[kMaxWin];
+  int32_t rows, part;
+};
+__device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a, int32_t (&wl)[kMaxWin],
+                                              int32_t (&woff)[kMaxWin], int32_t& nw, int32_t& wtot,
+                                              int32_t& tma, int32_t& vbytes) {
+  a.row0 = __ldg(&h->row0);
+  a.e0 = __ldg(&h->e0);
+#pragma unroll
+  for (int w = 0; w < kMaxWin; ++w) {
+    a.wa[w] = __ldg(&h->wa[w]);
+    wl[w] = __ldg(&h->wl[w]);
+    woff[w] = __ldg(&h->woff[w]);
+  }
+  a.rows = __ldg(&h->rows);
+  a.part = __ldg(&h->part);
+  nw = __ldg(&h->nw);
+  wtot = __ldg(&h->wtot);
+  tma = __ldg(&h->tma);
+  vbytes = __ldg(&h->vbytes);
+}
+
+template <bool INL, class SpecF>
+__device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
+                                              int kind, SpecF&& spec_of) {
+  const int lane = threadIdx.x & 31;
+  if (lane != 0) {   // keep the ring position in step with lane 0
+    for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) ring.next(T.n_stages);
+    return;
+  }
+  const uint64_t pol_stream = policy_evict_first();   // values / masks: read once per phase
+  const uint64_t pol_vec = policy_evict_normal();     // vectors: re-read by neighbour tiles
+  const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
+  HdrAddr cur{}, nxt{};
+  int32_t cwl[kMaxWin], cwoff[kMaxWin], cnw = 0, cwtot = 0, ctma = 0, cvb = 0;
+  int32_t nwl[kMaxWin], nwoff[kMaxWin], nnw = 0, nwtot = 0, ntma = 0, nvb = 0;
+  if (blockIdx.x < T.n_tiles) load_hdr_addr(hdrs + blockIdx.x, cur, cwl, cwoff, cnw, cwtot, ctma, cvb);
+  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) {
+    const int64_t tn = tile + gridDim.x;
+    if (tn < T.n_tiles) load_hdr_addr(hdrs + tn, nxt, nwl, nwoff, nnw, nwtot, ntma, nvb);
+    const PartDev& P = part_of(T, cur.part, INL);
+    const Spec sp = spec_of(P);
+    const int rows = cur.rows;
+    const int64_t row0 = cur.row0;
+    char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
+    uint64_t* full = S.full + ring.stage;
+    {
+      const long long c0 = T.prof_cta ? clock64() : 0;
+      mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
+      if (T.prof_cta) S.cnt[kind * 4 + 2] += clock64() - c0;
+    }
+    const unsigned vec_bytes = unsigned((rows * 8 + 15) & ~15);
+    if (sp.nwv) {
+      const bool tma = ctma != 0;
+      unsigned bytes = kHdrBytes;
+      if (tma)
+        bytes += unsigned(cvb) + unsigned((rows * 2 + 15) & ~15) + unsigned(sp.nwv * cwtot * 8) +
+                 unsigned(sp.ntv) * vec_bytes;
+      mbar_expect_tx(full, bytes);
+      bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
+      if (tma) {
+        char* d = st + kHdrBytes;
+        bulk_g2s(d, P.val + cur.e0, unsigned(cvb), full, pol_stream);
+        d += cvb;
+        bulk_g2s(d, P.rmask + row0, unsigned((rows * 2 + 15) & ~15), full, pol_stream);
+        d += kMaskBytes;
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+          for (int w = 0; w < kMaxWin; ++w)
+            if (v < sp.nwv && w < cnw)
+              bulk_g2s(d + (size_t(v) * cwtot + cwoff[w]) * 8, sp.wv[v] + cur.wa[w],
+                       unsigned(cwl[w] * 8), full, pol_vec);
+        d += size_t(sp.nwv) * cwtot * 8;
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+          if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
+      }
+    } else {
+      mbar_expect_tx(full, kHdrBytes + unsigned(sp.ntv) * vec_bytes);
+      bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
+      char* d = st + kHdrBytes;
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+        if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
+    }
+    ring.next(T.n_stages);
+    cur = nxt;
+#pragma unroll
+    for (int w = 0; w < kMaxWin; ++w) {
+      cwl[w] = nwl[w];
+      cwoff[w] = nwoff[w];
+    }
+    cnw = nnw;
+    cwtot = nwtot;
+    ctma = ntma;
+    cvb = nvb;
+  }
+}
+
+// Position of local column c in the staged windows (or -1).
+struct WinMap {
+  int64_t wa0, wa1, wa2;
+  int wl0, wl1, wl2, wo1, wo2;
+  __device__ __forceinline__ int pos(int64_t c) const {
+    unsigned d = unsigned(c - wa0);
+    if (d < unsigned(wl0)) return int(d);
+    d = unsigned(c - wa1);
+    if (d < unsigned(wl1)) return wo1 + int(d);
+    d = unsigned(c - wa2);
+    if (d < unsigned(wl2)) return wo2 + int(d);
+    return -1;
+  }
+};
+__device__ __forceinline__ WinMap win_map(const StageHdr& H) {
+  WinMap M;
+  M.wa0 = H.wa[0];
+  M.wa1 = H.wa[1];
+  M.wa2 = H.wa[2];
+  M.wl0 = H.nw > 0 ? H.wl[0] : 0;
+  M.wl1 = H.nw > 1 ? H.wl[1] : 0;
+  M.wl2 = H.nw > 2 ? H.wl[2] : 0;
+  M.wo1 = H.woff[1];
+  M.wo2 = H.woff[2];
+  return M;
+}
+
+// Staged SpMV of the consumer thread's row (lr = tid).  Per warp slice, lane k
+// owns pattern slot k: its column offset and the shared-memory index delta of
+// the window holding that offset's columns (computed once per slice instead
+// of a window search per entry), broadcast with shuffles.  Every local column
+// of a staged tile lies in a window by construction (plan.cpp
+// build_tile_windows).  Entries accumulate in stored order with the reference
+// rounding.  xs(q): staged operand at smem index q; fh(owner part, row): halo
+// column.  Returns A_row . x.
+template <bool HALO, class XS, class FH>
+__device__ __forceinline__ double row_spmv_staged(const PartDev& P, const PartDev* __restrict__ parts,
+                                                  const StageHdr& H, const WinMap& M,
+                                                  const double* __restrict__ sval,
+                                                  const uint16_t* __restrict__ smask, int lr, XS&& xs,
+                                                  FH&& fh) {
+  const int lane = threadIdx.x & 31;
+  const int n = int(P.n);
+  const int lr0 = lr & ~31;                    // warp-uniform
+  const int sl = lr0 >> 5;
+  const int s0 = H.sp[sl];
+  const int w = (H.sp[sl + 1] - s0) >> 5;
+  const int eb = s0 + lane;
+  const int ii = int(H.row0) + lr;
+  const unsigned msk = lr < H.rows ? unsigned(smask[lr]) : 0u;
+  int off_l = 0, e_l = 0;
+  if (lane < w) {
+    off_l = __ldg(P.pat_off + H.pat[sl] * kPatW + lane);
+    const int row_first = int(H.row0) + lr0;
+    int c = row_first + off_l;
+    c = c < 0 ? 0 : (c >= n ? n - 1 : c);
+    e_l = M.pos(c) + off_l - c;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPatW; ++k) {
+    if (k >= w) break;
+    const int e = __shfl_sync(0xffffffffu, e_l, k);
+    const int off = HALO ? __shfl_sync(0xffffffffu, off_l, k) : 0;
+    if ((msk >> k) & 1u) {
+      const double a = sval[eb + k * kSlice];
+      double xv;
+      if (HALO && ii + off >= n) {
+        const int h = ii + off - n;
+        xv = fh(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+      } else {
+        xv = xs(ii + e);
+      }
+      acc = __dadd_rn(acc, __dmul_rn(a, xv));
+    }
+  }
+  return acc;
+}
+
+// Consumer side of one phase: thread tid computes row tid of each tile
+// (body(P, H, st, acc)); warp g's butterfly sum is group g of the canonical
+// tile tree (kernels.cuh), and the group sums are added in group order into
+// T.partials[tile] — bit-identical to the classic kernels.
+template <int NR, bool INL, class Body>
+__device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
+                                              int kind, Body&& body) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tl = 0;
+  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x, ++tl) {
+    const char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
+    const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+    mbar_wait(S.full + ring.stage, ring.phase, T.timeout_ns);
+    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 0] += clock64() - c0;
+    const StageHdr& H = *reinterpret_cast<const StageHdr*>(st);
+    const PartDev& P = part_of(T, H.part, INL);
+    double acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    body(P, H, st, acc);
+    group_reduce<NR>(acc);
+    double* wp = S.wpart + (tl & 1) * kGroups * kMaxRed;
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) wp[warp * kMaxRed + j] = acc[j];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(S.empty + ring.stage);
+    const long long c1 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+    consumer_bar();
+    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 1] += clock64() - c1;
+    if (threadIdx.x < NR) {
+      const int j = threadIdx.x;
+      double s = wp[j];
+#pragma unroll
+      for (int g = 1; g < kGroups; ++g) s = __dadd_rn(s, wp[g * kMaxRed + j]);
+      T.partials[tile * kMaxRed + j] = s;
+    }
+    ring.next(T.n_stages);
+  }
+}
+
+// The consumer thread's row of a tile: lr = tid, i = row0 + lr.
+#define LRB_FOR_ROW(H, i, lr)                                   \
+  if (const int lr = int(threadIdx.x); lr < (H).rows)           \
+    if (const int64_t i = (H).row0 + lr; true)
+
+__device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
+  extern __shared__ __align__(128) char dsm[];
+  StreamSmem S;
+  S.stages = dsm;
+  char* tail = dsm + size_t(T.n_stages) * T.stage_bytes;
+  S.full = reinterpret_cast<uint64_t*>(tail);
+  S.empty = S.full + kStreamMaxStages;
+  S.wpart = reinterpret_cast<double*>(S.empty + kStreamMaxStages);
+  S.cnt = reinterpret_cast<unsigned long long*>(S.wpart + 2 * kGroups * kMaxRed);
+  return S;
+}
+__host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
+  return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * 8 + 2 * kGroups * kMaxRed * 8 +
+         kCnt * 8;
+}
+
+__device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& S) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < T.n_stages; ++s) {
+      mbar_init(S.full + s, 1);
+      mbar_init(S.empty + s, kGroups);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < kCnt) S.cnt[threadIdx.x] = 0;
+  __syncthreads();
+}
+
+// Phase wrapper: producer warp streams, consumers compute, then the team
+// barrier with the fused reduction (all threads).
+template <int NR, bool INL, class SpecF, class Body>
+__device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
+                                             double* red, int kind, SpecF&& spec_of, Body&& body) {
+  if (threadIdx.x >= kConsumers) {
+    fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
+    produce_phase<INL>(T, S, ring, kind, spec_of);
+  } else {
+    consume_phase<NR, INL>(T, S, ring, kind, body);
+  }
+  fence_proxy_async_global();
+  const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+  team_sync<NR, kRedLanes / kConsumers>(T, red);
+  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 3] += clock64() - c0;
+}
+
+// Diagnostics: this CTA's counters to T.prof_cta[blockIdx.x * kCnt ...].
+__device__ __forceinline__ void stream_flush_counters(const TeamDev& T, const StreamSmem& S) {
+  __syncthreads();
+  if (T.prof_cta && threadIdx.x < kCnt) T.prof_cta[blockIdx.x * kCnt + threadIdx.x] = (long long)S.cnt[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// CG / Jacobi-PCG, streaming.  Phases and arithmetic are those of
+// team_cg_kernel (kernels.cuh): A = {p_new, q = A p_new, p.q},
+// B = {x, r update, r.r (r.z)}, C = {|b - A x|^2}.
+// ---------------------------------------------------------------------------
+template <bool JAC, bool INL>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    team_cg_stream_kernel(const __grid_constant__ TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  const StreamSmem S = stream_smem(T);
+  stream_init(T, S);
+  Ring ring;
+  double red[2];
+  // ---- phase 0: x = 0, r = b, (z = dinv*b), b.b (, b.z)
+  stream_phase<2, INL>(
+      T, S, ring, red, 0,
+      [&](const PartDev& P) {
+        return Spec{0, JAC ? 2 : 1, {nullptr, nullptr}, {P.b, JAC ? P.dinv : nullptr}};
+      },
+      [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[2]) {
+        const double* vb = reinterpret_cast<const double*>(st + kHdrBytes);
+        const double* vd = vb + kTile;
+        LRB_FOR_ROW(H, i, lr) {
+          const double b = vb[lr];
+          P.x[i] = 0.0;
+          P.r[i] = b;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+          if (JAC) {
+            const double z = __dmul_rn(vd[lr], b);
+            P.s[i] = z;
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(b, z));
+          }
+        }
+      });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  double rho = JAC ? red[1] : bb;
+  double beta = 0.0, res = 1.0;
+  int pa = 0;
+  bool first = true, converged = false;
+  int it = 0;
+  for (it = 1; it <= T.max_iter; ++it) {
+    // ---- phase A: p_new = z + beta p_old (staged windows), q = A p_new, p.q
+    auto pnew_g = [&](const PartDev& Q, int64_t j) -> double {
+      const double z = JAC ? Q.s[j] : Q.r[j];
+      if (first) return z;
+      const double po = pa ? Q.p1[j] : Q.p0[j];
+      return __dadd_rn(z, __dmul_rn(beta, po));
+    };
+    stream_phase<1, INL>(
+        T, S, ring, red, 1,
+        [&](const PartDev& P) {
+          const double* z = JAC ? P.s : P.r;
+          const double* po = pa ? P.p1 : P.p0;
+          return first ? Spec{1, 0, {z, nullptr}, {}} : Spec{2, 0, {z, po}, {}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[1]) {
+          double* pout = pa ? P.p0 : P.p1;
+          if (H.tma) {
+            const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
+            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
+            const double* zw = reinterpret_cast<const double*>(st + kHdrBytes + H.vbytes + kMaskBytes);
+            const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
+            auto pn_s = [&](int q) -> double {
+              return first ? zw[q] : __dadd_rn(zw[q], __dmul_rn(beta, pw[q]));
+            };
+            const WinMap M = win_map(H);
+            const int lr = int(threadIdx.x);
+            const double qi = P.n_halo ? row_spmv_staged<true>(P, parts, H, M, sval, smask, lr, pn_s, pnew_g)
+                                       : row_spmv_staged<false>(P, parts, H, M, sval, smask, lr, pn_s, pnew_g);
+            if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const double pi = pn_s(M.pos(i));
+              pout[i] = pi;
+              P.q[i] = qi;
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
+            }
+          } else {
+            LRB_FOR_ROW(H, i, lr) {
+              const double pi = pnew_g(P, i);
+              const double qi = row_spmv(P, parts, i, pnew_g);
+              pout[i] = pi;
+              P.q[i] = qi;
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
+            }
+          }
+        });
+    if (team_failed(T)) break;
+    const double pq = red[0];
+    if (pq <= 0.0) {
+      if (lead) team_fail(T, LRB_ENOTPD);
+      break;
+    }
+    const double step = rho / pq;
+    pa ^= 1;
+    // ---- phase B: x += step p, r -= step q, r.r (, r.z)
+    stream_phase<2, INL>(
+        T, S, ring, red, 2,
+        [&](const PartDev& P) {
+          return Spec{0, JAC ? 5 : 4, {nullptr, nullptr},
+                      {pa ? P.p1 : P.p0, P.x, P.r, P.q, JAC ? P.dinv : nullptr}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[2]) {
+          const double* vp = reinterpret_cast<const double*>(st + kHdrBytes);
+          const double* vx = vp + kTile;
+          const double* vr = vx + kTile;
+          const double* vq = vr + kTile;
+          const double* vd = vq + kTile;
+          LRB_FOR_ROW(H, i, lr) {
+            const double x = __dadd_rn(vx[lr], __dmul_rn(step, vp[lr]));
+            const double r = __dsub_rn(vr[lr], __dmul_rn(step, vq[lr]));
+            P.x[i] = x;
+            P.r[i] = r;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+            if (JAC) {
+              const double z = __dmul_rn(vd[lr], r);
+              P.s[i] = z;
+              acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
+            }
+          }
+        });
+    if (team_failed(T)) break;
+    const double rr_new = red[0];
+    const double rho_new = JAC ? red[1] : rr_new;
+    const double rec = sqrt(rr_new) / bnorm;
+    if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
+    if (rec <= T.tol || it % 10 == 0) {
+      // ---- phase C: true residual |b - A x|
+      auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
+      stream_phase<1, INL>(
+          T, S, ring, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
+          [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[1]) {
+            if (H.tma) {
+              const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
+              const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
+              const double* xw = reinterpret_cast<const double*>(st + kHdrBytes + H.vbytes + kMaskBytes);
+              const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
+              const WinMap M = win_map(H);
+              const int lr = int(threadIdx.x);
+              auto xs = [&](int q) { return xw[q]; };
+              const double ax = P.n_halo ? row_spmv_staged<true>(P, parts, H, M, sval, smask, lr, xs, xg)
+                                         : row_spmv_staged<false>(P, parts, H, M, sval, smask, lr, xs, xg);
+              if (lr < H.rows) {
+                const double d = __dsub_rn(vb[lr], ax);
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+              }
+            } else {
+              LRB_FOR_ROW(H, i, lr) {
+                const double ax = row_spmv(P, parts, i, xg);
+                const double d = __dsub_rn(P.b[i], ax);
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+              }
+            }
+          });
+      if (team_failed(T)) break;
+      res = sqrt(red[0]) / bnorm;
+      if (res <= T.tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      res = rec;
+    }
+    beta = rho_new / rho;
+    rho = rho_new;
+    first = false;
+  }
+  stream_flush_counters(T, S);
+  if (lead) {
+    out->iterations = it > T.max_iter ? T.max_iter : it;
+    out->converged = converged ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+}  // namespace lrb

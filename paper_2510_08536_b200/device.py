@@ -266,6 +266,37 @@ class Team:
         N.check(N.lrb_team_read_vector(self.h, part, self.VECS[name], n, N.ptr(out)))
         return out
 
+    def kernel_info(self, method):
+        """Solve-kernel geometry on device rank 0 (lrb_team_kernel_info)."""
+        out = np.zeros(6, np.int64)
+        N.check(N.lrb_team_kernel_info(self.h, N.METHODS[method], N.ptr(out)))
+        keys = ("streaming", "grid", "block", "stages", "stage_bytes", "smem")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def profile(self, cap):
+        """Record phase-release timestamps in later solves (cap entries; 0: off)."""
+        N.check(N.lrb_team_profile(self.h, int(cap)))
+        self._prof_cap = int(cap)
+
+    def phase_times_ns(self):
+        """Timestamps (ns) of the last solve's barrier releases on device rank 0."""
+        cap = getattr(self, "_prof_cap", 0)
+        out = np.zeros(max(cap, 1), np.int64)
+        n = N.lrb_team_profile_read(self.h, N.ptr(out), cap)
+        if n < 0:
+            N.check(n)
+        return out[:n]
+
+    def wait_counters(self, method):
+        """Per-CTA SM-cycle counters of the last streaming solve, shape
+        (grid, 4 phase kinds, 4): data wait, consumer barrier, stage wait, team barrier."""
+        grid = self.kernel_info(method)["grid"]
+        out = np.zeros(grid * 16, np.int64)
+        n = N.lrb_team_profile_counters(self.h, N.METHODS[method], N.ptr(out), len(out))
+        if n < 0:
+            N.check(n)
+        return out[:n].reshape(-1, 4, 4)
+
     def debug(self, n_dev):
         out = np.zeros(1 + n_dev, np.int64)
         N.check(N.lrb_team_debug(self.h, N.ptr(out)))

@@ -278,7 +278,9 @@ def test_bicgstab_matches_oracle(alpha):
     assert rep.converged and ro.converged
     assert abs(rep.iterations - ro.iterations) <= 1
     n = min(len(ro.history), len(rep.history))
-    np.testing.assert_allclose(rep.history[:n], ro.history[:n], rtol=1e-8)
+    # history is |r|/|b|; the in-part dot order differs from the oracle's, so
+    # the tail carries cancellation noise of a few ulps of |b| (atol 1e-13)
+    np.testing.assert_allclose(rep.history[:n], ro.history[:n], rtol=1e-8, atol=1e-13)
     np.testing.assert_allclose(x, np.concatenate(xo), rtol=1e-8, atol=1e-12)
 
 

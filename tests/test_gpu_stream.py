@@ -1,0 +1,137 @@
+"""The streaming (bulk-copy / mbarrier ring) solvers against the classic
+per-thread-gather solvers: same tiles, same rounding, same reduction tree, so
+every iterate must be bit-identical — on stencil parts (every tile staged),
+multi-part devices, split device ranks (peer-flag protocol) and irregular
+random systems (tiles computed by the consumers' direct-load fallback)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2510_08536_b200 as lrb
+from helpers_b200 import cavity_case, golden_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _teams(parts, dev_ranks=None):
+    from paper_2510_08536_b200.device import Team
+    old = os.environ.get("LRB_SOLVER")
+    try:
+        os.environ["LRB_SOLVER"] = "classic"
+        classic = Team(parts, dev_ranks=dev_ranks)
+        os.environ.pop("LRB_SOLVER")
+        stream = Team(parts, dev_ranks=dev_ranks)
+    finally:
+        if old is None:
+            os.environ.pop("LRB_SOLVER", None)
+        else:
+            os.environ["LRB_SOLVER"] = old
+    return classic, stream
+
+
+def _compare(parts, methods, tol, max_iter, dev_ranks=None, rhs_seed=None, expect_stream=True):
+    classic, stream = _teams(parts, dev_ranks)
+    out = {}
+    for method in methods:
+        info = stream.kernel_info(method)
+        assert info["streaming"] == int(expect_stream), info
+        if expect_stream:
+            assert info["block"] == 544 and info["stages"] >= 2
+        assert classic.kernel_info(method)["streaming"] == 0
+        if rhs_seed is None:
+            bs = [np.ones(p.n) for p in parts]
+        else:
+            rng = np.random.default_rng(rhs_seed)
+            bs = [rng.standard_normal(p.n) for p in parts]
+        xa, ra, ha = classic.solve(method, bs, tol, max_iter, hist_cap=max_iter)
+        xb, rb, hb = stream.solve(method, bs, tol, max_iter, hist_cap=max_iter)
+        assert (ra.iterations, ra.converged, ra.status) == (rb.iterations, rb.converged, rb.status)
+        assert ra.residual == rb.residual and ra.bnorm == rb.bnorm
+        assert np.array_equal(ha, hb)
+        for a, b in zip(xa, xb):
+            assert np.array_equal(a, b)
+        out[method] = rb
+    return out
+
+
+def _owner_parts(asm, pm):
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        parts = s.comm.allgather(s.part)
+        return parts if s.comm.group_rank == 0 else None
+
+    return lrb.run_world(len(asm), program)
+
+
+@pytest.mark.parametrize("dims,n_cpu,alpha", [((16, 16, 16), 2, 2), ((32, 32, 32), 4, 4),
+                                              ((48, 40, 36), 3, 3), ((24, 24, 24), 8, 2)])
+def test_stream_bit_identical_cavity(dims, n_cpu, alpha):
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 3), "direct")
+        parts = s.comm.allgather(s.part) if s.is_owner else None
+        if s.is_owner and s.comm.group_rank == 0:
+            holder["r"] = _compare(parts, ("cg", "pcg"), 1e-9, 400)
+            holder["r2"] = _compare(parts, ("pcg",), 1e-30, 23, rhs_seed=7)   # max_iter exit
+        return None
+
+    lrb.run_world(n_cpu, program)
+    assert holder["r"]["cg"].converged and holder["r"]["pcg"].converged
+    assert not holder["r2"]["pcg"].converged and holder["r2"]["pcg"].iterations == 23
+
+
+def test_stream_bit_identical_split_devices():
+    _, asm, pm = cavity_case((20, 20, 20), 4, 1)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        parts = s.comm.allgather(s.part)
+        if s.comm.group_rank == 0:
+            holder["a"] = _compare(parts, ("cg", "pcg"), 1e-9, 400, dev_ranks=[0, 0, 1, 1])
+            holder["b"] = _compare(parts, ("pcg",), 1e-9, 400, dev_ranks=[0, 1, 2, 3])
+        return None
+
+    lrb.run_world(4, program)
+    assert holder["a"]["cg"].converged and holder["b"]["pcg"].converged
+
+
+@pytest.mark.parametrize("name", ["rand0", "rand7", "rand23"])
+def test_stream_bit_identical_irregular(name):
+    """Random systems: irregular slices fall back to direct loads per tile."""
+    pm, per_rank = golden_inputs(name)
+    parts = _owner_parts(per_rank, pm)[0]
+    # the random values are not SPD in general: compare the first iterations
+    classic, stream = _teams(parts)
+    bs = [np.ones(p.n) for p in parts]
+    for method in ("cg", "pcg"):
+        try:
+            xa, ra, ha = classic.solve(method, bs, 1e-30, 6, hist_cap=6)
+            ea = None
+        except ValueError as e:
+            ea = str(e)
+        try:
+            xb, rb, hb = stream.solve(method, bs, 1e-30, 6, hist_cap=6)
+            eb = None
+        except ValueError as e:
+            eb = str(e)
+        assert ea == eb
+        if ea is None:
+            assert ra.iterations == rb.iterations and np.array_equal(ha, hb)
+            for a, b in zip(xa, xb):
+                assert np.array_equal(a, b)
+
+
+def test_stream_solver_is_default_and_reports_geometry():
+    _, asm, pm = cavity_case((32, 32, 32), 4, 4)
+    parts = _owner_parts(asm, pm)[0]
+    from paper_2510_08536_b200.device import Team
+    info = Team(parts).kernel_info("pcg")
+    assert info["streaming"] == 1 and info["block"] == 544
+    assert info["grid"] >= 1 and info["stage_bytes"] % 128 == 0
+    assert info["smem"] >= info["stages"] * info["stage_bytes"]
