@@ -194,8 +194,9 @@ int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out);
 int lrb_team_profile(lrb_team* team, int32_t cap);
 int lrb_team_profile_read(lrb_team* team, int64_t* out, int32_t cap);
 /* Streaming solvers with profiling on: per-CTA SM-cycle counters of the last
- * solve of `method`, 16 per CTA = [phase kind: init, A, B, C][consumer data
- * wait, consumer barrier, producer stage wait, team barrier]; returns the
+ * solve of `method`, 32 per CTA = [phase kind: init, A, B, C][consumer data
+ * wait, end-of-phase barrier, producer stage wait, team barrier, row bodies,
+ * group reduce, tile sums, producer issue] (stream.cuh kCnt); returns the
  * number of values copied (0: not streaming / profiling off). */
 int lrb_team_profile_counters(lrb_team* team, int32_t method, int64_t* out, int32_t cap);
 

@@ -634,6 +634,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_peer_flags = take(sizeof(void*) * n_dev);
   const size_t o_peer_red = take(sizeof(void*) * n_dev);
   const size_t o_out = take(sizeof(SolveOut));
+  const size_t o_ctr = take(sizeof(unsigned) * 2);
   // streaming solvers: stage size from the largest stageable tile, and the
   // per-tile stage headers
   const bool want_stream = solver_choice() != 1;
@@ -666,6 +667,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
   H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
   H.out = D.out_dev;
+  H.tile_ctr = reinterpret_cast<unsigned*>(w + o_ctr);
   {
     const char* env = getenv("LRB_BARRIER_TIMEOUT_S");
     const double s = env ? atof(env) : 20.0;
@@ -848,6 +850,10 @@ static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, in
     }
   }
   best = (best + 127) & ~int64_t(127);
+  int64_t n = std::min<int64_t>(kStreamMaxStages, budget / best);
+  // grow the stage to pack 3 elementwise tiles when that keeps the ring depth
+  const int64_t packed = (3 * (kHdrBytes + 5 * int64_t(kVecTileBytes)) + 127) & ~int64_t(127);
+  if (packed > best && std::min<int64_t>(kStreamMaxStages, budget / packed) >= n) best = packed;
   *n_stages = int(std::min<int64_t>(kStreamMaxStages, budget / best));
   return int(best);
 }
@@ -1394,6 +1400,7 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
       }
     LRB_CUDA(cudaMemsetAsync(D.out_dev, 0, sizeof(SolveOut), D.stream));
     if (D.prof_dev) LRB_CUDA(cudaMemsetAsync(D.prof_dev, 0, sizeof(long long), D.stream));
+    LRB_CUDA(cudaMemsetAsync(D.host.tile_ctr, 0, sizeof(unsigned) * 2, D.stream));
     TeamDev& H = D.host;
     H.tol = tol;
     H.max_iter = max_iter;

@@ -300,7 +300,7 @@ __device__ void team_fail(const TeamDev& T, int code) {
 // (NVLink peer stores + release/acquire flags), sums all parts in ascending
 // GPU rank and releases everybody.  Returns the team-reduced values in red[].
 template <int NR, int LPT>
-__device__ void team_sync(const TeamDev& T, double* red) {
+__device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = nullptr) {
   __shared__ unsigned s_last, s_gen;
   __shared__ double gs[kRedGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
@@ -317,6 +317,7 @@ __device__ void team_sync(const TeamDev& T, double* red) {
   __syncthreads();
   if (s_last) {
     __threadfence();
+    if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
     // Part values are double-buffered by epoch parity: a fast peer may already
     // publish epoch e+1 into our buffer while we still read epoch e (it only
     // needs our flag for e, which we raise before summing).  It cannot reach
@@ -363,6 +364,7 @@ __device__ void team_sync(const TeamDev& T, double* red) {
         T.red[j] = s;
       }
       if (T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
+      if (reset_ctr) *reset_ctr = 0;   // every CTA is done grabbing tiles of this phase
       *T.bar_count = 0;
       __threadfence();
       atomicAdd(T.bar_gen, 1u);

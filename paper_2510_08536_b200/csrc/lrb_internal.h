@@ -148,6 +148,7 @@ struct TeamDev {
   int32_t hist_cap;
   int32_t max_iter;
   const void* tile_hdr;     // streaming solvers: StageHdr per device tile
+  unsigned int* tile_ctr;   // streaming solvers: [2] dynamic tile counters (phase parity)
   long long* prof;          // phase-release timestamps (nullable, diagnostics)
   long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)
   int32_t* prof_n;

@@ -33,6 +33,8 @@ constexpr int kStreamThreads = kConsumers + 32;  // + one producer warp
 constexpr int kMaskBytes = kTile * 2;          // uint16 row masks of a tile
 constexpr int kVecTileBytes = kTile * 8;       // one vector's rows of a tile
 constexpr int kStreamMaxStages = 4;
+constexpr int kMaxPack = 4;                     // tiles per stage in elementwise phases
+constexpr int kSlotRing = 2 * kStreamMaxStages; // group-sum slots (see consume_phase)
 constexpr int kConsumerBar = 1;                // named barrier of the consumer warps
 
 
@@ -121,12 +123,22 @@ struct StreamSmem {
   uint64_t* full;      // [n_stages]
   uint64_t* empty;     // [n_stages]
   double* wpart;       // [2][kGroups][kMaxRed]
+  int32_t* stile;      // [n_stages] first tile of each stage (-1: end of phase)
+  int32_t* scnt;       // [n_stages] tiles packed in the stage (elementwise phases: up to kMaxPack)
+  int32_t* ssub;       // [n_stages] byte stride between the packed tiles
+  double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
+  int32_t* wtile;      // [kSlotRing] first tile of the stage in the slot
+  int32_t* wcnt;       // [kSlotRing] tiles of the stage in the slot
+  int2* slot;          // [kGroups warps][kPatW] pattern slot table (offset, smem delta)
   unsigned long long* cnt;   // [kCnt] wait-cycle counters (diagnostics, T.prof_cta)
 };
 // Diagnostic counters per CTA: [phase kind (0 init, 1 A, 2 B, 3 C)][what]
-// what: 0 consumer warp 0 waiting for data, 1 consumer barrier, 2 producer
-// waiting for a free stage, 3 team barrier (thread 0, arrival -> release).
-constexpr int kCnt = 16;
+// what: 0 consumer warp 0 waiting for data, 1 end-of-phase consumer barrier,
+// 2 producer waiting for a free stage, 3 team barrier (thread 0, arrival ->
+// release), 4 warp 0 row bodies, 5 warp 0 group reduce + park, 6 warp 0 tile
+// sums, 7 producer issuing (stage free -> copies issued).
+constexpr int kCntPer = 8;
+constexpr int kCnt = 4 * kCntPer;
 
 __device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool inl) {
   return inl ? T.lp[p - T.part_begin] : T.parts[p];
@@ -174,35 +186,51 @@ __device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a, int
   vbytes = __ldg(&h->vbytes);
 }
 
+// Tiles are handed out dynamically: the producer grabs the next tile of the
+// phase from the device's phase counter (atomicAdd, issued one tile ahead so
+// its latency hides behind the current tile's copies), so CTAs finish a
+// phase together whatever their bandwidth share.  Partials are per tile, so
+// results do not depend on which CTA computed a tile.  After the last tile the
+// producer publishes a sentinel (stile = -1) through the ring.
 template <bool INL, class SpecF>
 __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                              int kind, SpecF&& spec_of) {
-  const int lane = threadIdx.x & 31;
-  if (lane != 0) {   // keep the ring position in step with lane 0
-    for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) ring.next(T.n_stages);
-    return;
-  }
+                                              int kind, unsigned* ctr, SpecF&& spec_of) {
+  if ((threadIdx.x & 31) != 0) return;
   const uint64_t pol_stream = policy_evict_first();   // values / masks: read once per phase
   const uint64_t pol_vec = policy_evict_normal();     // vectors: re-read by neighbour tiles
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
+  const int64_t n_tiles = T.n_tiles;
   HdrAddr cur{}, nxt{};
   int32_t cwl[kMaxWin], cwoff[kMaxWin], cnw = 0, cwtot = 0, ctma = 0, cvb = 0;
   int32_t nwl[kMaxWin], nwoff[kMaxWin], nnw = 0, nwtot = 0, ntma = 0, nvb = 0;
-  if (blockIdx.x < T.n_tiles) load_hdr_addr(hdrs + blockIdx.x, cur, cwl, cwoff, cnw, cwtot, ctma, cvb);
-  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x) {
-    const int64_t tn = tile + gridDim.x;
-    if (tn < T.n_tiles) load_hdr_addr(hdrs + tn, nxt, nwl, nwoff, nnw, nwtot, ntma, nvb);
-    const PartDev& P = part_of(T, cur.part, INL);
-    const Spec sp = spec_of(P);
-    const int rows = cur.rows;
-    const int64_t row0 = cur.row0;
+  // lookahead: tile indices two ahead, headers one ahead
+  int64_t tile = atomicAdd(ctr, 1u);
+  int64_t tn = tile < n_tiles ? int64_t(atomicAdd(ctr, 1u)) : n_tiles;
+  if (tile < n_tiles) load_hdr_addr(hdrs + tile, cur, cwl, cwoff, cnw, cwtot, ctma, cvb);
+  while (true) {
+    const int64_t tnn = tn < n_tiles ? int64_t(atomicAdd(ctr, 1u)) : n_tiles;
+    if (tn < n_tiles) load_hdr_addr(hdrs + tn, nxt, nwl, nwoff, nnw, nwtot, ntma, nvb);
     char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
     uint64_t* full = S.full + ring.stage;
     {
       const long long c0 = T.prof_cta ? clock64() : 0;
       mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
-      if (T.prof_cta) S.cnt[kind * 4 + 2] += clock64() - c0;
+      if (T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
+    if (tile >= n_tiles) {   // sentinel: the consumers leave the phase
+      S.stile[ring.stage] = -1;
+      mbar_arrive(full);
+      ring.next(T.n_stages);
+      break;
+    }
+    const long long ci = T.prof_cta ? clock64() : 0;
+    S.stile[ring.stage] = int32_t(tile);
+    S.scnt[ring.stage] = 1;
+    S.ssub[ring.stage] = 0;
+    const PartDev& P = part_of(T, cur.part, INL);
+    const Spec sp = spec_of(P);
+    const int rows = cur.rows;
+    const int64_t row0 = cur.row0;
     const unsigned vec_bytes = unsigned((rows * 8 + 15) & ~15);
     if (sp.nwv) {
       const bool tma = ctma != 0;
@@ -238,7 +266,10 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
       for (int v = 0; v < 5; ++v)
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
     }
+    if (T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
     ring.next(T.n_stages);
+    tile = tn;
+    tn = tnn;
     cur = nxt;
 #pragma unroll
     for (int w = 0; w < kMaxWin; ++w) {
@@ -249,6 +280,96 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
     cwtot = nwtot;
     ctma = ntma;
     cvb = nvb;
+  }
+}
+
+// Elementwise phases: a tile needs only kHdrBytes + ntv * kVecTileBytes, so
+// the producer grabs K consecutive tiles per atomic and packs them into one
+// stage (K = stage_bytes / tile bytes, at most kMaxPack): K times the bytes in
+// flight of one tile per stage, with the same ring.
+template <bool INL, class SpecF>
+__device__ __forceinline__ void produce_elementwise(const TeamDev& T, const StreamSmem& S, Ring& ring,
+                                                    int kind, unsigned* ctr, SpecF&& spec_of) {
+  if ((threadIdx.x & 31) != 0) return;
+  const uint64_t pol_vec = policy_evict_normal();
+  const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
+  const int64_t n_tiles = T.n_tiles;
+  const bool one_part = T.part_end - T.part_begin == 1;
+  const int ntv = spec_of(part_of(T, T.part_begin, INL)).ntv;
+  const int sub = kHdrBytes + ntv * kVecTileBytes;
+  int K = T.stage_bytes / sub;
+  K = K < 1 ? 1 : (K > kMaxPack ? kMaxPack : K);
+  int64_t c0 = atomicAdd(ctr, unsigned(K));
+  int64_t c1 = c0 < n_tiles ? int64_t(atomicAdd(ctr, unsigned(K))) : n_tiles;
+  while (true) {
+    const int64_t c2 = c1 < n_tiles ? int64_t(atomicAdd(ctr, unsigned(K))) : n_tiles;
+    char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
+    uint64_t* full = S.full + ring.stage;
+    {
+      const long long t0 = T.prof_cta ? clock64() : 0;
+      mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
+      if (T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - t0;
+    }
+    if (c0 >= n_tiles) {
+      S.stile[ring.stage] = -1;
+      mbar_arrive(full);
+      ring.next(T.n_stages);
+      break;
+    }
+    const long long ci = T.prof_cta ? clock64() : 0;
+    const int cnt = int(n_tiles - c0 < K ? n_tiles - c0 : K);
+    S.stile[ring.stage] = int32_t(c0);
+    S.scnt[ring.stage] = cnt;
+    S.ssub[ring.stage] = sub;
+    int part[kMaxPack], rows[kMaxPack];
+    int64_t row0[kMaxPack];
+    unsigned bytes = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxPack; ++j) {
+      if (j < cnt) {
+        const int64_t tile = c0 + j;
+        part[j] = one_part ? T.part_begin : __ldg(T.tile_part + tile);
+        const PartDev& P = part_of(T, part[j], INL);
+        row0[j] = (tile - P.tile0) * kTile;
+        rows[j] = int(P.n - row0[j] < kTile ? P.n - row0[j] : int64_t(kTile));
+        bytes += kHdrBytes;
+      }
+    }
+    if (part[0] == part[cnt - 1])
+      bytes += unsigned(ntv) * unsigned(((row0[cnt - 1] + rows[cnt - 1] - row0[0]) * 8 + 15) & ~int64_t(15));
+    else
+      for (int j = 0; j < cnt; ++j) bytes += unsigned(ntv) * unsigned((rows[j] * 8 + 15) & ~15);
+    mbar_expect_tx(full, bytes);
+    // stage layout: [cnt headers][vector 0: cnt tiles][vector 1: cnt tiles]...
+    // consecutive tiles of one part are contiguous rows: one copy per vector
+    bulk_g2s(st, hdrs + c0, unsigned(cnt) * kHdrBytes, full, pol_vec);
+    char* vbase = st + size_t(cnt) * kHdrBytes;
+    const size_t vstride = size_t(cnt) * kVecTileBytes;
+    if (part[0] == part[cnt - 1]) {
+      const PartDev& P = part_of(T, part[0], INL);
+      const Spec sp = spec_of(P);
+      const unsigned vb = unsigned(((row0[cnt - 1] + rows[cnt - 1] - row0[0]) * 8 + 15) & ~int64_t(15));
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+        if (v < sp.ntv) bulk_g2s(vbase + v * vstride, sp.tv[v] + row0[0], vb, full, pol_vec);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMaxPack; ++j) {
+        if (j < cnt) {
+          const PartDev& P = part_of(T, part[j], INL);
+          const Spec sp = spec_of(P);
+          const unsigned vb = unsigned((rows[j] * 8 + 15) & ~15);
+#pragma unroll
+          for (int v = 0; v < 5; ++v)
+            if (v < sp.ntv)
+              bulk_g2s(vbase + v * vstride + size_t(j) * kVecTileBytes, sp.tv[v] + row0[j], vb, full, pol_vec);
+        }
+      }
+    }
+    if (T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
+    ring.next(T.n_stages);
+    c0 = c1;
+    c1 = c2;
   }
 }
 
@@ -287,90 +408,196 @@ __device__ __forceinline__ WinMap win_map(const StageHdr& H) {
 // build_tile_windows).  Entries accumulate in stored order with the reference
 // rounding.  xs(q): staged operand at smem index q; fh(owner part, row): halo
 // column.  Returns A_row . x.
-template <bool HALO, class XS, class FH>
-__device__ __forceinline__ double row_spmv_staged(const PartDev& P, const PartDev* __restrict__ parts,
-                                                  const StageHdr& H, const WinMap& M,
-                                                  const double* __restrict__ sval,
-                                                  const uint16_t* __restrict__ smask, int lr, XS&& xs,
-                                                  FH&& fh) {
-  const int lane = threadIdx.x & 31;
-  const int n = int(P.n);
-  const int lr0 = lr & ~31;                    // warp-uniform
-  const int sl = lr0 >> 5;
-  const int s0 = H.sp[sl];
-  const int w = (H.sp[sl + 1] - s0) >> 5;
-  const int eb = s0 + lane;
-  const int ii = int(H.row0) + lr;
-  const unsigned msk = lr < H.rows ? unsigned(smask[lr]) : 0u;
-  int off_l = 0, e_l = 0;
-  if (lane < w) {
-    off_l = __ldg(P.pat_off + H.pat[sl] * kPatW + lane);
-    const int row_first = int(H.row0) + lr0;
-    int c = row_first + off_l;
-    c = c < 0 ? 0 : (c >= n ? n - 1 : c);
-    e_l = M.pos(c) + off_l - c;
+// Operand of a staged window position: NV = 1: w0[q]; NV = 2: the on-the-fly
+// p_new = w0[q] + beta * w1[q] (z and p_old windows, reference rounding).
+template <int NV>
+__device__ __forceinline__ double staged_operand(const double* __restrict__ w0,
+                                                 const double* __restrict__ w1, double beta, int q) {
+  if constexpr (NV == 1) {
+    return w0[q];
+  } else {
+    return __dadd_rn(w0[q], __dmul_rn(beta, w1[q]));
+  }
+}
+
+// Fixed-width row product: WM pattern slots, all operand loads issued
+// before the accumulation chain (slots k >= w and holes are masked to 0).
+template <int NV, int WM>
+__device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
+                                            const int2* __restrict__ slot,
+                                            const double* __restrict__ sval,
+                                            const double* __restrict__ w0,
+                                            const double* __restrict__ w1, double beta) {
+  double a[WM], x[WM];
+#pragma unroll
+  for (int k = 0; k < WM; ++k) {
+    const bool on = k < w && ((msk >> k) & 1u);
+    const int2 se = slot[k];
+    a[k] = on ? sval[eb + k * kSlice] : 0.0;
+    x[k] = on ? staged_operand<NV>(w0, w1, beta, ii + se.y) : 0.0;
   }
   double acc = 0.0;
 #pragma unroll
-  for (int k = 0; k < kPatW; ++k) {
-    if (k >= w) break;
-    const int e = __shfl_sync(0xffffffffu, e_l, k);
-    const int off = HALO ? __shfl_sync(0xffffffffu, off_l, k) : 0;
-    if ((msk >> k) & 1u) {
+  for (int k = 0; k < WM; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k], x[k]));
+  return acc;
+}
+
+template <int NV, bool HALO, class FH>
+__device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ pat_off,
+                                                  const int32_t* __restrict__ hpart,
+                                                  const int32_t* __restrict__ hidx,
+                                                  const PartDev* __restrict__ parts, const StageHdr& H,
+                                                  const WinMap& M, const double* __restrict__ sval,
+                                                  const uint16_t* __restrict__ smask,
+                                                  const double* __restrict__ w0,
+                                                  const double* __restrict__ w1, double beta, int lr,
+                                                  int2* __restrict__ slot, FH&& fh) {
+  const int lane = threadIdx.x & 31;
+  const int rows = H.rows;
+  const int lr0 = lr & ~31;                    // warp-uniform
+  const int sl = lr0 >> 5;
+  const int s0 = H.sp[sl];
+  const int w = lr0 < rows ? (H.sp[sl + 1] - s0) >> 5 : 0;
+  const int eb = s0 + lane;
+  const int ii = int(H.row0) + lr;
+  const unsigned msk = lr < rows ? unsigned(smask[lr]) : 0u;
+  __syncwarp();   // the warp's previous readers of its slot table are done
+  if (lane < w) {
+    const int off = __ldg(pat_off + H.pat[sl] * kPatW + lane);
+    const int row_first = int(H.row0) + lr0;
+    int c = row_first + off;
+    c = c < 0 ? 0 : (c >= n ? n - 1 : c);
+    slot[lane] = make_int2(off, M.pos(c) + off - c);
+  }
+  __syncwarp();
+  if constexpr (!HALO) {
+    if (w == 7) return row_fixed<NV, 7>(w, ii, eb, msk, slot, sval, w0, w1, beta);
+    if (w <= 8) return row_fixed<NV, 8>(w, ii, eb, msk, slot, sval, w0, w1, beta);
+    return row_fixed<NV, kPatW>(w, ii, eb, msk, slot, sval, w0, w1, beta);
+  } else {
+    // holes (mask bit clear) have value 0.0 in the SELL layout and get operand
+    // 0.0 here, so acc + 0 * 0 leaves acc unchanged (acc is never -0.0)
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+      const int2 se = slot[k];
+      const bool on = (msk >> k) & 1u;
       const double a = sval[eb + k * kSlice];
+      const int c = ii + se.x;
       double xv;
-      if (HALO && ii + off >= n) {
-        const int h = ii + off - n;
-        xv = fh(parts[__ldg(P.hpart + h)], int64_t(__ldg(P.hidx + h)));
+      if (on && c >= n) {
+        xv = fh(parts[__ldg(hpart + (c - n))], int64_t(__ldg(hidx + (c - n))));
       } else {
-        xv = xs(ii + e);
+        xv = staged_operand<NV>(w0, w1, beta, on ? ii + se.y : 0);
+        xv = on ? xv : 0.0;
       }
       acc = __dadd_rn(acc, __dmul_rn(a, xv));
     }
+    return acc;
   }
-  return acc;
+}
+
+// Vectors of one packed elementwise tile: vector v at base + v * stride.
+struct VecView {
+  const char* base;
+  size_t stride;
+  __device__ __forceinline__ const double* operator[](int v) const {
+    return reinterpret_cast<const double*>(base + v * stride);
+  }
+};
+
+// Tile sum of the stage in slot ss: group g's sum of sub-tile j was parked at
+// wsum[ss % kSlotRing][j][g] by warp g; warp (ss*kMaxPack + j) % kGroups adds
+// the 16 group sums in group order (the canonical tile tree, kernels.cuh).
+template <int NR>
+__device__ __forceinline__ void sum_stage_slot(const TeamDev& T, const StreamSmem& S, int ss) {
+  const int sl = ss % kSlotRing;
+  const int cnt = S.wcnt[sl];
+  const int64_t t0 = S.wtile[sl];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = 0; j < cnt; ++j) {
+    if (warp == ((ss * kMaxPack + j) & (kGroups - 1)) && lane < NR) {
+      const double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups) * 2;
+      double sum = w[lane];
+#pragma unroll
+      for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * 2 + lane]);
+      T.partials[(t0 + j) * kMaxRed + lane] = sum;
+    }
+  }
 }
 
 // Consumer side of one phase: thread tid computes row tid of each tile
 // (body(P, H, st, acc)); warp g's butterfly sum is group g of the canonical
-// tile tree (kernels.cuh), and the group sums are added in group order into
-// T.partials[tile] — bit-identical to the classic kernels.
+// tile tree and is parked in the stage's group-sum slot.  No per-tile block
+// barrier: a warp that starts stage ss knows (through the ring: the producer
+// refilled that stage only after every warp released stage ss - n_stages)
+// that all group sums of stage ss - n_stages are written, and sums them then;
+// the last n_stages stages are summed after one barrier at the end.  Slots
+// are reused after kSlotRing = 2 * max stages, beyond the fastest warp's lead.
 template <int NR, bool INL, class Body>
 __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
                                               int kind, Body&& body) {
+  static_assert(NR <= 2, "group-sum slots hold two reductions");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int tl = 0;
-  for (int64_t tile = blockIdx.x; tile < T.n_tiles; tile += gridDim.x, ++tl) {
-    const char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
+  const int ns = T.n_stages;
+  int ss = 0;
+  for (;; ++ss) {
+    const char* st0 = S.stages + size_t(ring.stage) * T.stage_bytes;
     const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
     mbar_wait(S.full + ring.stage, ring.phase, T.timeout_ns);
-    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 0] += clock64() - c0;
-    const StageHdr& H = *reinterpret_cast<const StageHdr*>(st);
-    const PartDev& P = part_of(T, H.part, INL);
-    double acc[NR];
+    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
+    {
+      const long long c2 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      if (ss >= ns) sum_stage_slot<NR>(T, S, ss - ns);
+      if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 6] += clock64() - c2;
+    }
+    const int64_t tile0 = S.stile[ring.stage];
+    if (tile0 < 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(S.empty + ring.stage);
+      ring.next(ns);
+      break;
+    }
+    const int cnt = S.scnt[ring.stage];
+    const int sub = S.ssub[ring.stage];
+    const int sl = ss % kSlotRing;
+    if (threadIdx.x == 0) {
+      S.wtile[sl] = int32_t(tile0);
+      S.wcnt[sl] = cnt;
+    }
+    for (int j = 0; j < cnt; ++j) {
+      // SpMV stages hold one tile at st0; packed elementwise stages hold cnt
+      // headers, then each vector's cnt tiles (produce_elementwise)
+      const char* st = sub ? st0 + size_t(j) * kHdrBytes : st0;
+      const VecView V{sub ? st0 + size_t(cnt) * kHdrBytes + size_t(j) * kVecTileBytes : nullptr,
+                      size_t(cnt) * kVecTileBytes};
+      const StageHdr& H = *reinterpret_cast<const StageHdr*>(st);
+      const PartDev& P = part_of(T, H.part, INL);
+      double acc[NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-    body(P, H, st, acc);
-    group_reduce<NR>(acc);
-    double* wp = S.wpart + (tl & 1) * kGroups * kMaxRed;
-    if (lane == 0) {
+      for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+      const long long c3 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      body(P, H, st, V, acc);
+      const long long c4 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      group_reduce<NR>(acc);
+      if (lane == 0) {
+        double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups + warp) * 2;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) wp[warp * kMaxRed + j] = acc[j];
+        for (int q = 0; q < NR; ++q) w[q] = acc[q];
+      }
+      if (T.prof_cta && threadIdx.x == 0) {
+        const long long c5 = clock64();
+        S.cnt[kind * kCntPer + 4] += c4 - c3;
+        S.cnt[kind * kCntPer + 5] += c5 - c4;
+      }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(S.empty + ring.stage);
-    const long long c1 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-    consumer_bar();
-    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 1] += clock64() - c1;
-    if (threadIdx.x < NR) {
-      const int j = threadIdx.x;
-      double s = wp[j];
-#pragma unroll
-      for (int g = 1; g < kGroups; ++g) s = __dadd_rn(s, wp[g * kMaxRed + j]);
-      T.partials[tile * kMaxRed + j] = s;
-    }
-    ring.next(T.n_stages);
+    if (lane == 0) mbar_arrive(S.empty + ring.stage);   // group sums written before the release
+    ring.next(ns);
   }
+  const long long c1 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+  consumer_bar();
+  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 1] += clock64() - c1;
+  for (int s2 = (ss - ns + 1 > 0 ? ss - ns + 1 : 0); s2 < ss; ++s2) sum_stage_slot<NR>(T, S, s2);
 }
 
 // The consumer thread's row of a tile: lr = tid, i = row0 + lr.
@@ -387,11 +614,19 @@ __device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
   S.empty = S.full + kStreamMaxStages;
   S.wpart = reinterpret_cast<double*>(S.empty + kStreamMaxStages);
   S.cnt = reinterpret_cast<unsigned long long*>(S.wpart + 2 * kGroups * kMaxRed);
+  S.stile = reinterpret_cast<int32_t*>(S.cnt + kCnt);
+  S.scnt = S.stile + kStreamMaxStages;
+  S.ssub = S.scnt + kStreamMaxStages;
+  S.wtile = S.ssub + kStreamMaxStages;
+  S.wcnt = S.wtile + kSlotRing;
+  S.slot = reinterpret_cast<int2*>(S.wcnt + kSlotRing);                   // 8-byte aligned
+  S.wsum = reinterpret_cast<double*>(S.slot + kGroups * kPatW);
   return S;
 }
 __host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
   return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * 8 + 2 * kGroups * kMaxRed * 8 +
-         kCnt * 8;
+         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 + kGroups * kPatW * 8 +
+         size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8;
 }
 
 __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& S) {
@@ -408,19 +643,25 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
 
 // Phase wrapper: producer warp streams, consumers compute, then the team
 // barrier with the fused reduction (all threads).
-template <int NR, bool INL, class SpecF, class Body>
+template <int NR, bool INL, bool ELEM, class SpecF, class Body>
 __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                             double* red, int kind, SpecF&& spec_of, Body&& body) {
+                                             double* red, int kind, int& seq, SpecF&& spec_of,
+                                             Body&& body) {
+  unsigned* ctr = T.tile_ctr + (seq & 1);   // phase seq grabs tiles here; reset at its barrier
   if (threadIdx.x >= kConsumers) {
     fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
-    produce_phase<INL>(T, S, ring, kind, spec_of);
+    if constexpr (ELEM)
+      produce_elementwise<INL>(T, S, ring, kind, ctr, spec_of);
+    else
+      produce_phase<INL>(T, S, ring, kind, ctr, spec_of);
   } else {
     consume_phase<NR, INL>(T, S, ring, kind, body);
   }
   fence_proxy_async_global();
   const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-  team_sync<NR, kRedLanes / kConsumers>(T, red);
-  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * 4 + 3] += clock64() - c0;
+  team_sync<NR, kRedLanes / kConsumers>(T, red, ctr);
+  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
+  ++seq;
 }
 
 // Diagnostics: this CTA's counters to T.prof_cta[blockIdx.x * kCnt ...].
@@ -441,16 +682,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   const StreamSmem S = stream_smem(T);
   stream_init(T, S);
   Ring ring;
+  int seq = 0;   // phase sequence number (tile counter parity)
   double red[2];
   // ---- phase 0: x = 0, r = b, (z = dinv*b), b.b (, b.z)
-  stream_phase<2, INL>(
-      T, S, ring, red, 0,
+  stream_phase<2, INL, true>(
+      T, S, ring, red, 0, seq,
       [&](const PartDev& P) {
         return Spec{0, JAC ? 2 : 1, {nullptr, nullptr}, {P.b, JAC ? P.dinv : nullptr}};
       },
-      [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[2]) {
-        const double* vb = reinterpret_cast<const double*>(st + kHdrBytes);
-        const double* vd = vb + kTile;
+      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, double (&acc)[2]) {
+        const double* vb = V[0];
+        const double* vd = V[1];
         LRB_FOR_ROW(H, i, lr) {
           const double b = vb[lr];
           P.x[i] = 0.0;
@@ -489,30 +731,40 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       const double po = pa ? Q.p1[j] : Q.p0[j];
       return __dadd_rn(z, __dmul_rn(beta, po));
     };
-    stream_phase<1, INL>(
-        T, S, ring, red, 1,
+    stream_phase<1, INL, false>(
+        T, S, ring, red, 1, seq,
         [&](const PartDev& P) {
           const double* z = JAC ? P.s : P.r;
           const double* po = pa ? P.p1 : P.p0;
           return first ? Spec{1, 0, {z, nullptr}, {}} : Spec{2, 0, {z, po}, {}};
         },
-        [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[1]) {
+        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           if (H.tma) {
             const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
             const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
             const double* zw = reinterpret_cast<const double*>(st + kHdrBytes + H.vbytes + kMaskBytes);
             const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
-            auto pn_s = [&](int q) -> double {
-              return first ? zw[q] : __dadd_rn(zw[q], __dmul_rn(beta, pw[q]));
-            };
             const WinMap M = win_map(H);
             const int lr = int(threadIdx.x);
-            const double qi = P.n_halo ? row_spmv_staged<true>(P, parts, H, M, sval, smask, lr, pn_s, pnew_g)
-                                       : row_spmv_staged<false>(P, parts, H, M, sval, smask, lr, pn_s, pnew_g);
+            const int n = int(P.n);
+            const int32_t* pat_off = P.pat_off;
+            double qi;
+            if (first) {
+              qi = P.n_halo ? row_spmv_staged<1, true>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
+                                                      zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g)
+                            : row_spmv_staged<1, false>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval,
+                                                       smask, zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g);
+            } else {
+              qi = P.n_halo ? row_spmv_staged<2, true>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
+                                                      zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g)
+                            : row_spmv_staged<2, false>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval,
+                                                       smask, zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g);
+            }
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const double pi = pn_s(M.pos(i));
+              const int qd = M.pos(i);
+              const double pi = first ? zw[qd] : staged_operand<2>(zw, pw, beta, qd);
               pout[i] = pi;
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
@@ -536,18 +788,18 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     const double step = rho / pq;
     pa ^= 1;
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
-    stream_phase<2, INL>(
-        T, S, ring, red, 2,
+    stream_phase<2, INL, true>(
+        T, S, ring, red, 2, seq,
         [&](const PartDev& P) {
           return Spec{0, JAC ? 5 : 4, {nullptr, nullptr},
                       {pa ? P.p1 : P.p0, P.x, P.r, P.q, JAC ? P.dinv : nullptr}};
         },
-        [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[2]) {
-          const double* vp = reinterpret_cast<const double*>(st + kHdrBytes);
-          const double* vx = vp + kTile;
-          const double* vr = vx + kTile;
-          const double* vq = vr + kTile;
-          const double* vd = vq + kTile;
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, double (&acc)[2]) {
+          const double* vp = V[0];
+          const double* vx = V[1];
+          const double* vr = V[2];
+          const double* vq = V[3];
+          const double* vd = V[4];
           LRB_FOR_ROW(H, i, lr) {
             const double x = __dadd_rn(vx[lr], __dmul_rn(step, vp[lr]));
             const double r = __dsub_rn(vr[lr], __dmul_rn(step, vq[lr]));
@@ -569,9 +821,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     if (rec <= T.tol || it % 10 == 0) {
       // ---- phase C: true residual |b - A x|
       auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
-      stream_phase<1, INL>(
-          T, S, ring, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
-          [&](const PartDev& P, const StageHdr& H, const char* st, double (&acc)[1]) {
+      stream_phase<1, INL, false>(
+          T, S, ring, red, 3, seq, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
+          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
             if (H.tma) {
               const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
               const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
@@ -579,9 +831,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
               const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
               const WinMap M = win_map(H);
               const int lr = int(threadIdx.x);
-              auto xs = [&](int q) { return xw[q]; };
-              const double ax = P.n_halo ? row_spmv_staged<true>(P, parts, H, M, sval, smask, lr, xs, xg)
-                                         : row_spmv_staged<false>(P, parts, H, M, sval, smask, lr, xs, xg);
+              const int n = int(P.n);
+              const double ax =
+                  P.n_halo ? row_spmv_staged<1, true>(n, P.pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
+                                                     xw, xw, 0.0, lr, S.slot + (threadIdx.x >> 5) * kPatW, xg)
+                           : row_spmv_staged<1, false>(n, P.pat_off, P.hpart, P.hidx, parts, H, M, sval,
+                                                      smask, xw, xw, 0.0, lr, S.slot + (threadIdx.x >> 5) * kPatW, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(vb[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));

@@ -289,13 +289,13 @@ class Team:
 
     def wait_counters(self, method):
         """Per-CTA SM-cycle counters of the last streaming solve, shape
-        (grid, 4 phase kinds, 4): data wait, consumer barrier, stage wait, team barrier."""
+        (grid, 4 phase kinds, 8) — see stream.cuh kCnt."""
         grid = self.kernel_info(method)["grid"]
-        out = np.zeros(grid * 16, np.int64)
+        out = np.zeros(grid * 32, np.int64)
         n = N.lrb_team_profile_counters(self.h, N.METHODS[method], N.ptr(out), len(out))
         if n < 0:
             N.check(n)
-        return out[:n].reshape(-1, 4, 4)
+        return out[:n].reshape(-1, 4, 8)
 
     def debug(self, n_dev):
         out = np.zeros(1 + n_dev, np.int64)

@@ -74,11 +74,12 @@ def main():
         total = []
         for _ in range(args.repeat):
             _, rep, hist = team.solve(args.method, bs, TOL, MAX_ITER, want_x=False, hist_cap=MAX_ITER)
-            ts = team.phase_times_ns()
+            ts = team.phase_times_ns().reshape(-1, 2)   # (last arrival, release) per phase
             kinds = phase_kinds(hist, rep.iterations, TOL)
-            d = np.diff(ts) / 1e3   # us, phase k = release k-1 -> release k
-            for k, dt in zip(kinds[1:], d):
-                per.setdefault(k, []).append(dt)
+            for q in range(1, len(ts)):
+                k = kinds[q]
+                per.setdefault(k, []).append((ts[q, 1] - ts[q - 1, 1]) / 1e3)
+                per.setdefault(k + "_sync", []).append((ts[q, 1] - ts[q, 0]) / 1e3)
             total.append(rep.device_ms)
         out = {"family": family, "iterations": rep.iterations, "device_ms": round(float(np.mean(total)), 4),
                "info": team.kernel_info(args.method)}
@@ -86,14 +87,16 @@ def main():
         if cnt.size:
             # mean over CTAs, in us at the sampled SM clock, per phase kind
             mhz = float(os.environ.get("LRB_SM_MHZ", "1965"))
-            names = ("data_wait", "cons_bar", "stage_wait", "team_bar")
+            names = ("data_wait", "end_bar", "stage_wait", "team_bar", "body", "reduce", "tile_sums",
+                     "issue")
             out["waits_us"] = {kind: {nm: round(float(cnt[:, ki, wi].mean()) / mhz, 1)
                                       for wi, nm in enumerate(names)}
                                for ki, kind in enumerate(("init", "A", "B", "C"))}
         for k, v in sorted(per.items()):
             us = float(np.mean(v))
-            out[k] = {"count": len(v) // args.repeat, "us": round(us, 2),
-                      "gbs": round(bytes_of[k] / (us * 1e-6) / 1e9, 1)}
+            out[k] = {"count": len(v) // args.repeat, "us": round(us, 2)}
+            if k in bytes_of:
+                out[k]["gbs"] = round(bytes_of[k] / (us * 1e-6) / 1e9, 1)
         print(json.dumps(out), flush=True)
         del team
 
