@@ -57,5 +57,18 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
     return lib
 
 
+PROF_LIB = os.path.join(HERE, "libldurepart_b200_prof.so")
+
+
+def build_profiling(force: bool = False) -> str:
+    """Diagnostics variant with the streaming solvers' wait/issue counters
+    compiled in (-DLRB_PROF=1); select it with LRB_LIB=<path> (tools/)."""
+    if not force and os.path.exists(PROF_LIB) and os.path.getmtime(PROF_LIB) >= os.path.getmtime(LIB) \
+            and not _stale():
+        return PROF_LIB
+    return build(force=True, out=PROF_LIB, extra=["-DLRB_PROF=1"])
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_profiling(force="--force" in sys.argv))

@@ -95,7 +95,7 @@ struct lrb_part {
   PartDev d{};                      // device pointers (host copy)
   std::vector<int64_t> seg_off, seg_rows, slice_ptr;
   std::vector<int32_t> tile_win;           // host copies (stage headers of the streaming solvers)
-  std::vector<int32_t> slice_pat_host;
+  std::vector<int32_t> slice_pat_host, pat_off_host;
   std::vector<int32_t> loc_sell, nl_sell;  // SELL slot of each CSR entry (value mirror)
   int64_t nnz_l = 0, nnz_n = 0;
   cudaStream_t main = nullptr;
@@ -229,6 +229,7 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   part->slice_ptr = P.slice_ptr;
   part->tile_win = P.tile_win;
   part->slice_pat_host = P.slice_pat;
+  part->pat_off_host = P.pat_off;
   part->nnz_l = int64_t(P.loc_col.size());
   part->nnz_n = int64_t(P.nl_col.size());
   part->stage = host_stage;
@@ -596,7 +597,7 @@ static const void* stream_kernel(int method, bool inl);
 static int stream_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t smem);
 static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, int* n_stages);
 static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, int stage_bytes,
-                                std::vector<StageHdr>& out);
+                                std::vector<StageHdr>& out, std::vector<StageTab>& tabs);
 static int solver_choice();
 static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share,
                     int64_t stage_doubles, size_t* smem);
@@ -642,6 +643,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const int stage_bytes = want_stream ? stream_stage_bytes(D, by_index, &n_stages) : 0;
   const bool use_stream = want_stream && n_stages >= 2;
   const size_t o_hdr = use_stream ? take(sizeof(StageHdr) * n_tiles) : 0;
+  const size_t o_tab = use_stream ? take(sizeof(StageTab) * n_tiles) : 0;
   LRB_CUDA(cudaMalloc(&D.ws, bytes));
   LRB_CUDA(cudaMemset(D.ws, 0, bytes));
   D.ws_bytes = bytes;
@@ -687,11 +689,15 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.stage_bytes = stage_bytes;
   H.n_stages = n_stages;
   H.tile_hdr = nullptr;
+  H.tile_tab = nullptr;
   if (use_stream) {
     std::vector<StageHdr> hdr;
-    build_stage_headers(D, by_index, stage_bytes, hdr);
+    std::vector<StageTab> tab;
+    build_stage_headers(D, by_index, stage_bytes, hdr, tab);
     H.tile_hdr = w + o_hdr;
+    H.tile_tab = w + o_tab;
     LRB_CUDA(cudaMemcpy(w + o_hdr, hdr.data(), sizeof(StageHdr) * hdr.size(), cudaMemcpyHostToDevice));
+    LRB_CUDA(cudaMemcpy(w + o_tab, tab.data(), sizeof(StageTab) * tab.size(), cudaMemcpyHostToDevice));
   }
   for (int m = 0; m < 3; ++m) {
     const void* sfn = use_stream ? stream_kernel(m, D.inl) : nullptr;
@@ -828,7 +834,7 @@ static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int6
   }
   h.wtot = int32_t(wtot);
   if (h.nw <= 0) return 0;
-  const int64_t base = kHdrBytes + h.vbytes + kMaskBytes;
+  const int64_t base = kHdrBytes + kTabBytes + h.vbytes + kMaskBytes;
   return std::max(base + 2 * wtot * 8, base + wtot * 8 + kVecTileBytes);
 }
 
@@ -858,19 +864,53 @@ static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, in
   return int(best);
 }
 
-// One StageHdr per device tile; tiles without windows, or larger than a
-// stage, are marked for the consumers' direct-load path (tma = 0).
+// One StageHdr + StageTab per device tile; tiles without windows, larger
+// than a stage, or with more than kHdrPats distinct slice patterns are marked
+// for the consumers' direct-load path (tma = 0).
 static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, int stage_bytes,
-                                std::vector<StageHdr>& out) {
+                                std::vector<StageHdr>& out, std::vector<StageTab>& tabs) {
   out.assign(size_t(std::max<int64_t>(D.n_tiles, 1)), StageHdr{});
+  tabs.assign(out.size(), StageTab{});
   for (int p : D.parts) {
     const lrb_part* P = by_index[p];
+    const int64_t n = P->d.n;
     for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
       StageHdr& h = out[P->d.tile0 + lt];
+      StageTab& tb = tabs[P->d.tile0 + lt];
       const int64_t need = tile_geometry(P, lt, p, P->d.tile0 + lt, h);
       h.tma = (need > 0 && need <= stage_bytes) ? 1 : 0;
       const int64_t s0 = h.row0 / kSlice, nsl = (h.rows + kSlice - 1) / kSlice;
-      for (int64_t s = 0; s < nsl; ++s) h.pat[s] = P->slice_pat_host[s0 + s];
+      std::vector<int32_t> local;   // distinct pattern ids, first-seen order
+      for (int64_t s = 0; s < nsl; ++s) {
+        const int32_t pid = P->slice_pat_host[s0 + s];
+        h.pat[s] = pid;
+        auto it = std::find(local.begin(), local.end(), pid);
+        if (it == local.end()) {
+          local.push_back(pid);
+          it = local.end() - 1;
+        }
+        h.spat[s] = int8_t(std::min<int64_t>(it - local.begin(), kHdrPats - 1));
+      }
+      if (int(local.size()) > kHdrPats) h.tma = 0;
+      h.npat = int32_t(std::min<size_t>(local.size(), kHdrPats));
+      if (!h.tma) continue;
+      for (int j = 0; j < h.npat; ++j) {
+        h.sdiag[j] = -1;
+        if (local[j] < 0) {
+          h.tma = 0;
+          break;
+        }
+        for (int k = 0; k < kPatW; ++k) {
+          const int32_t off = P->pat_off_host[size_t(local[j]) * kPatW + k];
+          // the window holding this offset's local columns (one per tile)
+          const int64_t c = std::min<int64_t>(std::max<int64_t>(h.row0 + off, 0), n - 1);
+          int32_t e = 0;
+          for (int w = 0; w < h.nw; ++w)
+            if (c >= h.wa[w] && c < h.wa[w] + h.wl[w]) e = int32_t(h.woff[w] - h.wa[w] + off);
+          tb.slot[j][k] = int2_t_{off, e};
+          if (off == 0 && h.sdiag[j] < 0) h.sdiag[j] = int8_t(k);
+        }
+      }
     }
   }
 }

@@ -86,6 +86,7 @@ constexpr int kMaxRed = 4;   // reductions fused into one barrier
 // Per-tile header of the streaming solvers (stream.cuh), precomputed at team
 // creation and bulk-copied into the shared-memory stage with the tile's data.
 constexpr int kHdrBytes = 256;
+constexpr int kHdrPats = 4;    // distinct slice patterns a staged tile may hold
 struct alignas(16) StageHdr {
   int64_t row0;          // first row of the tile (part-local)
   int64_t e0;            // first SELL entry of the tile
@@ -99,13 +100,27 @@ struct alignas(16) StageHdr {
   int32_t wl[kMaxWin];   // aligned window lengths (even)
   int32_t woff[kMaxWin]; // window offsets inside a vector's staged run
   int32_t vbytes;        // staged value bytes
-  int32_t pad_;
+  int32_t npat;          // distinct patterns of the tile (slot tables in StageTab)
   int32_t sp[kTile / kSlice + 1];   // slice entry offsets relative to e0
-  int32_t pat[kTile / kSlice];      // slice pattern ids
-  int32_t reserved_[(kHdrBytes - 228) / 4];
+  int32_t pat[kTile / kSlice];      // slice pattern ids (dictionary)
+  int8_t spat[kTile / kSlice];      // slice -> slot table of the tile's StageTab
+  int8_t sdiag[kHdrPats];           // slot of the diagonal (offset 0) per table
+  int32_t reserved_[(kHdrBytes - 248) / 4];
 };
 static_assert(sizeof(StageHdr) == kHdrBytes, "stage header must be exactly kHdrBytes");
 
+struct int2_t_ {
+  int32_t x, y;
+};
+
+// Slot tables of a staged tile: for each distinct pattern and slot k, the
+// column offset (col - row) and the shared-memory delta e such that a row i's
+// operand for that slot sits at staged index i + e (window arithmetic done
+// once on the host instead of per warp and row on the device).
+constexpr int kTabBytes = kHdrPats * 16 * 8;
+struct alignas(16) StageTab {
+  int2_t_ slot[kHdrPats][16];
+};
 enum Method { kCG = 0, kPCG = 1, kBiCGStab = 2 };
 
 struct SolveOut {
@@ -148,6 +163,7 @@ struct TeamDev {
   int32_t hist_cap;
   int32_t max_iter;
   const void* tile_hdr;     // streaming solvers: StageHdr per device tile
+  const void* tile_tab;     // streaming solvers: StageTab per device tile
   unsigned int* tile_ctr;   // streaming solvers: [2] dynamic tile counters (phase parity)
   long long* prof;          // phase-release timestamps (nullable, diagnostics)
   long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)

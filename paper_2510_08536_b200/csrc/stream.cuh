@@ -129,7 +129,6 @@ struct StreamSmem {
   double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
   int32_t* wtile;      // [kSlotRing] first tile of the stage in the slot
   int32_t* wcnt;       // [kSlotRing] tiles of the stage in the slot
-  int2* slot;          // [kGroups warps][kPatW] pattern slot table (offset, smem delta)
   unsigned long long* cnt;   // [kCnt] wait-cycle counters (diagnostics, T.prof_cta)
 };
 // Diagnostic counters per CTA: [phase kind (0 init, 1 A, 2 B, 3 C)][what]
@@ -137,6 +136,10 @@ struct StreamSmem {
 // 2 producer waiting for a free stage, 3 team barrier (thread 0, arrival ->
 // release), 4 warp 0 row bodies, 5 warp 0 group reduce + park, 6 warp 0 tile
 // sums, 7 producer issuing (stage free -> copies issued).
+#ifndef LRB_PROF
+#define LRB_PROF 0   // build with -DLRB_PROF=1 for the wait/issue counters
+#endif
+constexpr bool kProf = LRB_PROF != 0;
 constexpr int kCntPer = 8;
 constexpr int kCnt = 4 * kCntPer;
 
@@ -153,7 +156,7 @@ struct Spec {
 };
 
 __device__ __forceinline__ int stage_tail_offset(const StageHdr& H, int nwv) {
-  return nwv ? kHdrBytes + H.vbytes + kMaskBytes + nwv * H.wtot * 8 : kHdrBytes;
+  return nwv ? kHdrBytes + kTabBytes + H.vbytes + kMaskBytes + nwv * H.wtot * 8 : kHdrBytes;
 }
 
 // ---------------------------------------------------------------------------
@@ -213,9 +216,9 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
     char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
     uint64_t* full = S.full + ring.stage;
     {
-      const long long c0 = T.prof_cta ? clock64() : 0;
+      const long long c0 = (kProf && T.prof_cta) ? clock64() : 0;
       mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
-      if (T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - c0;
+      if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
     if (tile >= n_tiles) {   // sentinel: the consumers leave the phase
       S.stile[ring.stage] = -1;
@@ -223,7 +226,7 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
       ring.next(T.n_stages);
       break;
     }
-    const long long ci = T.prof_cta ? clock64() : 0;
+    const long long ci = (kProf && T.prof_cta) ? clock64() : 0;
     S.stile[ring.stage] = int32_t(tile);
     S.scnt[ring.stage] = 1;
     S.ssub[ring.stage] = 0;
@@ -236,12 +239,14 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
       const bool tma = ctma != 0;
       unsigned bytes = kHdrBytes;
       if (tma)
-        bytes += unsigned(cvb) + unsigned((rows * 2 + 15) & ~15) + unsigned(sp.nwv * cwtot * 8) +
-                 unsigned(sp.ntv) * vec_bytes;
+        bytes += kTabBytes + unsigned(cvb) + unsigned((rows * 2 + 15) & ~15) +
+                 unsigned(sp.nwv * cwtot * 8) + unsigned(sp.ntv) * vec_bytes;
       mbar_expect_tx(full, bytes);
       bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
       if (tma) {
-        char* d = st + kHdrBytes;
+        bulk_g2s(st + kHdrBytes, reinterpret_cast<const StageTab*>(T.tile_tab) + tile, kTabBytes, full,
+                 pol_vec);
+        char* d = st + kHdrBytes + kTabBytes;
         bulk_g2s(d, P.val + cur.e0, unsigned(cvb), full, pol_stream);
         d += cvb;
         bulk_g2s(d, P.rmask + row0, unsigned((rows * 2 + 15) & ~15), full, pol_stream);
@@ -266,7 +271,7 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
       for (int v = 0; v < 5; ++v)
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
     }
-    if (T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
+    if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
     ring.next(T.n_stages);
     tile = tn;
     tn = tnn;
@@ -306,9 +311,9 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
     char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
     uint64_t* full = S.full + ring.stage;
     {
-      const long long t0 = T.prof_cta ? clock64() : 0;
+      const long long t0 = (kProf && T.prof_cta) ? clock64() : 0;
       mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
-      if (T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - t0;
+      if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - t0;
     }
     if (c0 >= n_tiles) {
       S.stile[ring.stage] = -1;
@@ -316,7 +321,7 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
       ring.next(T.n_stages);
       break;
     }
-    const long long ci = T.prof_cta ? clock64() : 0;
+    const long long ci = (kProf && T.prof_cta) ? clock64() : 0;
     const int cnt = int(n_tiles - c0 < K ? n_tiles - c0 : K);
     S.stile[ring.stage] = int32_t(c0);
     S.scnt[ring.stage] = cnt;
@@ -366,7 +371,7 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
         }
       }
     }
-    if (T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
+    if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
     ring.next(T.n_stages);
     c0 = c1;
     c1 = c2;
@@ -442,16 +447,21 @@ __device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
   return acc;
 }
 
+// Slot table of the warp's slice in the staged StageTab.
+__device__ __forceinline__ const int2* slice_slots(const char* st, const StageHdr& H, int sl) {
+  return reinterpret_cast<const int2*>(st + kHdrBytes) + H.spat[sl] * 16;
+}
+
 template <int NV, bool HALO, class FH>
-__device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ pat_off,
-                                                  const int32_t* __restrict__ hpart,
+__device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ hpart,
                                                   const int32_t* __restrict__ hidx,
                                                   const PartDev* __restrict__ parts, const StageHdr& H,
-                                                  const WinMap& M, const double* __restrict__ sval,
+                                                  const int2* __restrict__ slot,
+                                                  const double* __restrict__ sval,
                                                   const uint16_t* __restrict__ smask,
                                                   const double* __restrict__ w0,
                                                   const double* __restrict__ w1, double beta, int lr,
-                                                  int2* __restrict__ slot, FH&& fh) {
+                                                  FH&& fh) {
   const int lane = threadIdx.x & 31;
   const int rows = H.rows;
   const int lr0 = lr & ~31;                    // warp-uniform
@@ -461,15 +471,6 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
   const int eb = s0 + lane;
   const int ii = int(H.row0) + lr;
   const unsigned msk = lr < rows ? unsigned(smask[lr]) : 0u;
-  __syncwarp();   // the warp's previous readers of its slot table are done
-  if (lane < w) {
-    const int off = __ldg(pat_off + H.pat[sl] * kPatW + lane);
-    const int row_first = int(H.row0) + lr0;
-    int c = row_first + off;
-    c = c < 0 ? 0 : (c >= n ? n - 1 : c);
-    slot[lane] = make_int2(off, M.pos(c) + off - c);
-  }
-  __syncwarp();
   if constexpr (!HALO) {
     if (w == 7) return row_fixed<NV, 7>(w, ii, eb, msk, slot, sval, w0, w1, beta);
     if (w <= 8) return row_fixed<NV, 8>(w, ii, eb, msk, slot, sval, w0, w1, beta);
@@ -525,6 +526,68 @@ __device__ __forceinline__ void sum_stage_slot(const TeamDev& T, const StreamSme
   }
 }
 
+// L2 prefetch of a future tile (the bulk copies of whoever processes it then
+// hit L2): its SELL values and row masks (SpMV phases) and its own rows of
+// every vector the phase reads.  Issued by the consumers, spread one line
+// per thread, PD = kPrefetchRounds * grid tiles ahead of the tile being
+// computed (dynamic scheduling hands tiles out in increasing order, so every
+// tile is prefetched once, about that many tiles before it is copied).
+// Off by default: measured on B200 at C3 it slows the solve 11.1 -> 15.5 ms
+// (the consumers stall on the prefetch addresses and the extra L2 requests
+// compete with the bulk copies).  -DLRB_PREFETCH_ROUNDS=2 to experiment.
+#ifndef LRB_PREFETCH_ROUNDS
+#define LRB_PREFETCH_ROUNDS 0
+#endif
+constexpr int kPrefetchRounds = LRB_PREFETCH_ROUNDS;
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+struct PrefetchTarget {
+  int64_t row0, e0;
+  int32_t rows, part, vbytes, ok;
+};
+
+__device__ __forceinline__ PrefetchTarget prefetch_target(const TeamDev& T, int64_t tile) {
+  PrefetchTarget f{0, 0, 0, 0, 0, 0};
+  if (kPrefetchRounds > 0 && tile < T.n_tiles) {
+    const StageHdr* h = reinterpret_cast<const StageHdr*>(T.tile_hdr) + tile;
+    f.row0 = __ldg(&h->row0);
+    f.e0 = __ldg(&h->e0);
+    f.rows = __ldg(&h->rows);
+    f.part = __ldg(&h->part);
+    f.vbytes = __ldg(&h->vbytes);
+    f.ok = 1;
+  }
+  return f;
+}
+
+template <bool INL, class SpecF>
+__device__ __forceinline__ void prefetch_tile(const TeamDev& T, const PrefetchTarget& f, SpecF&& spec_of) {
+  if (!f.ok) return;
+  const PartDev& Q = part_of(T, f.part, INL);
+  const Spec sp = spec_of(Q);
+  const int t = threadIdx.x;
+  const int vl = (f.rows * 8 + 127) >> 7;   // 128-byte lines of one vector's rows
+  int line = t;
+  if (sp.nwv) {
+    const char* vb = reinterpret_cast<const char*>(Q.val + f.e0);
+    for (int off = t * 128; off < f.vbytes; off += kConsumers * 128) prefetch_l2(vb + off);
+    line -= (f.vbytes + 127) >> 7;
+    const int ml = (f.rows * 2 + 127) >> 7;
+    if (line >= 0 && line < ml) prefetch_l2(reinterpret_cast<const char*>(Q.rmask + f.row0) + line * 128);
+    line -= ml;
+  }
+  if (line < 0) line += kConsumers;   // threads past the values take the vectors
+  const int nv = sp.nwv + sp.ntv;
+  if (line >= 0 && line < nv * vl) {
+    const int v = line / vl;
+    const double* vec = v < sp.nwv ? sp.wv[v] : sp.tv[v - sp.nwv];
+    prefetch_l2(reinterpret_cast<const char*>(vec + f.row0) + (line - v * vl) * 128);
+  }
+}
+
 // Consumer side of one phase: thread tid computes row tid of each tile
 // (body(P, H, st, acc)); warp g's butterfly sum is group g of the canonical
 // tile tree and is parked in the stage's group-sum slot.  No per-tile block
@@ -533,22 +596,22 @@ __device__ __forceinline__ void sum_stage_slot(const TeamDev& T, const StreamSme
 // that all group sums of stage ss - n_stages are written, and sums them then;
 // the last n_stages stages are summed after one barrier at the end.  Slots
 // are reused after kSlotRing = 2 * max stages, beyond the fastest warp's lead.
-template <int NR, bool INL, class Body>
+template <int NR, bool INL, class SpecF, class Body>
 __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                              int kind, Body&& body) {
+                                              int kind, SpecF&& spec_of, Body&& body) {
   static_assert(NR <= 2, "group-sum slots hold two reductions");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ns = T.n_stages;
   int ss = 0;
   for (;; ++ss) {
     const char* st0 = S.stages + size_t(ring.stage) * T.stage_bytes;
-    const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+    const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
     mbar_wait(S.full + ring.stage, ring.phase, T.timeout_ns);
-    if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
+    if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
     {
-      const long long c2 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      const long long c2 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       if (ss >= ns) sum_stage_slot<NR>(T, S, ss - ns);
-      if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 6] += clock64() - c2;
+      if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 6] += clock64() - c2;
     }
     const int64_t tile0 = S.stile[ring.stage];
     if (tile0 < 0) {
@@ -564,7 +627,9 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       S.wtile[sl] = int32_t(tile0);
       S.wcnt[sl] = cnt;
     }
+    const int64_t pd = int64_t(kPrefetchRounds) * gridDim.x;
     for (int j = 0; j < cnt; ++j) {
+      const PrefetchTarget pf = prefetch_target(T, tile0 + j + pd);
       // SpMV stages hold one tile at st0; packed elementwise stages hold cnt
       // headers, then each vector's cnt tiles (produce_elementwise)
       const char* st = sub ? st0 + size_t(j) * kHdrBytes : st0;
@@ -575,16 +640,17 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       double acc[NR];
 #pragma unroll
       for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-      const long long c3 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      const long long c3 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       body(P, H, st, V, acc);
-      const long long c4 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      prefetch_tile<INL>(T, pf, spec_of);
+      const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       group_reduce<NR>(acc);
       if (lane == 0) {
         double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups + warp) * 2;
 #pragma unroll
         for (int q = 0; q < NR; ++q) w[q] = acc[q];
       }
-      if (T.prof_cta && threadIdx.x == 0) {
+      if (kProf && T.prof_cta && threadIdx.x == 0) {
         const long long c5 = clock64();
         S.cnt[kind * kCntPer + 4] += c4 - c3;
         S.cnt[kind * kCntPer + 5] += c5 - c4;
@@ -594,9 +660,9 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
     if (lane == 0) mbar_arrive(S.empty + ring.stage);   // group sums written before the release
     ring.next(ns);
   }
-  const long long c1 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+  const long long c1 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
   consumer_bar();
-  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 1] += clock64() - c1;
+  if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 1] += clock64() - c1;
   for (int s2 = (ss - ns + 1 > 0 ? ss - ns + 1 : 0); s2 < ss; ++s2) sum_stage_slot<NR>(T, S, s2);
 }
 
@@ -619,13 +685,12 @@ __device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
   S.ssub = S.scnt + kStreamMaxStages;
   S.wtile = S.ssub + kStreamMaxStages;
   S.wcnt = S.wtile + kSlotRing;
-  S.slot = reinterpret_cast<int2*>(S.wcnt + kSlotRing);                   // 8-byte aligned
-  S.wsum = reinterpret_cast<double*>(S.slot + kGroups * kPatW);
+  S.wsum = reinterpret_cast<double*>(S.wcnt + kSlotRing);   // 8-byte aligned
   return S;
 }
 __host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
   return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * 8 + 2 * kGroups * kMaxRed * 8 +
-         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 + kGroups * kPatW * 8 +
+         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 +
          size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8;
 }
 
@@ -655,19 +720,19 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
     else
       produce_phase<INL>(T, S, ring, kind, ctr, spec_of);
   } else {
-    consume_phase<NR, INL>(T, S, ring, kind, body);
+    consume_phase<NR, INL>(T, S, ring, kind, spec_of, body);
   }
   fence_proxy_async_global();
-  const long long c0 = (T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+  const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
   team_sync<NR, kRedLanes / kConsumers>(T, red, ctr);
-  if (T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
+  if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
   ++seq;
 }
 
 // Diagnostics: this CTA's counters to T.prof_cta[blockIdx.x * kCnt ...].
 __device__ __forceinline__ void stream_flush_counters(const TeamDev& T, const StreamSmem& S) {
   __syncthreads();
-  if (T.prof_cta && threadIdx.x < kCnt) T.prof_cta[blockIdx.x * kCnt + threadIdx.x] = (long long)S.cnt[threadIdx.x];
+  if (kProf && T.prof_cta && threadIdx.x < kCnt) T.prof_cta[blockIdx.x * kCnt + threadIdx.x] = (long long)S.cnt[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -741,29 +806,30 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           if (H.tma) {
-            const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
-            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
-            const double* zw = reinterpret_cast<const double*>(st + kHdrBytes + H.vbytes + kMaskBytes);
+            const double* sval = reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes);
+            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes + H.vbytes);
+            const double* zw =
+                reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes + H.vbytes + kMaskBytes);
             const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
-            const WinMap M = win_map(H);
             const int lr = int(threadIdx.x);
+            const int sl = lr >> 5;
+            const int2* slot = slice_slots(st, H, sl);
             const int n = int(P.n);
-            const int32_t* pat_off = P.pat_off;
             double qi;
             if (first) {
-              qi = P.n_halo ? row_spmv_staged<1, true>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
-                                                      zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g)
-                            : row_spmv_staged<1, false>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval,
-                                                       smask, zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g);
+              qi = P.n_halo ? row_spmv_staged<1, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw, pw,
+                                                      beta, lr, pnew_g)
+                            : row_spmv_staged<1, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw,
+                                                       pw, beta, lr, pnew_g);
             } else {
-              qi = P.n_halo ? row_spmv_staged<2, true>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
-                                                      zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g)
-                            : row_spmv_staged<2, false>(n, pat_off, P.hpart, P.hidx, parts, H, M, sval,
-                                                       smask, zw, pw, beta, lr, S.slot + (threadIdx.x >> 5) * kPatW, pnew_g);
+              qi = P.n_halo ? row_spmv_staged<2, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw, pw,
+                                                      beta, lr, pnew_g)
+                            : row_spmv_staged<2, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw,
+                                                       pw, beta, lr, pnew_g);
             }
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const int qd = M.pos(i);
+              const int qd = int(i) + slot[H.sdiag[H.spat[sl]]].y;   // the diagonal's operand
               const double pi = first ? zw[qd] : staged_operand<2>(zw, pw, beta, qd);
               pout[i] = pi;
               P.q[i] = qi;
@@ -825,18 +891,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           T, S, ring, red, 3, seq, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
           [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
             if (H.tma) {
-              const double* sval = reinterpret_cast<const double*>(st + kHdrBytes);
-              const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + H.vbytes);
-              const double* xw = reinterpret_cast<const double*>(st + kHdrBytes + H.vbytes + kMaskBytes);
+              const double* sval = reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes);
+              const uint16_t* smask =
+                  reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes + H.vbytes);
+              const double* xw =
+                  reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes + H.vbytes + kMaskBytes);
               const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
-              const WinMap M = win_map(H);
               const int lr = int(threadIdx.x);
+              const int2* slot = slice_slots(st, H, lr >> 5);
               const int n = int(P.n);
               const double ax =
-                  P.n_halo ? row_spmv_staged<1, true>(n, P.pat_off, P.hpart, P.hidx, parts, H, M, sval, smask,
-                                                     xw, xw, 0.0, lr, S.slot + (threadIdx.x >> 5) * kPatW, xg)
-                           : row_spmv_staged<1, false>(n, P.pat_off, P.hpart, P.hidx, parts, H, M, sval,
-                                                      smask, xw, xw, 0.0, lr, S.slot + (threadIdx.x >> 5) * kPatW, xg);
+                  P.n_halo ? row_spmv_staged<1, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, xw, xw,
+                                                     0.0, lr, xg)
+                           : row_spmv_staged<1, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, xw,
+                                                      xw, 0.0, lr, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(vb[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));

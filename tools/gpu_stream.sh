@@ -18,6 +18,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:team
 tail -3 gpurun_out/prof_stream.log
 fi
 if [ "${PHASE:-0}" = 1 ]; then
-timeout 600 python tools/phase_profile.py > gpurun_out/phase.json 2> gpurun_out/phase.err; echo phase=$?
+LRB_LIB=$PWD/paper_2510_08536_b200/libldurepart_b200_prof.so timeout 600 python tools/phase_profile.py > gpurun_out/phase.json 2> gpurun_out/phase.err; echo phase=$?
 cat gpurun_out/phase.json; tail -3 gpurun_out/phase.err
 fi
