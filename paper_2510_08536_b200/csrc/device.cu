@@ -96,6 +96,7 @@ struct lrb_part {
   std::vector<int64_t> seg_off, seg_rows, slice_ptr;
   std::vector<int32_t> tile_win;           // host copies (stage headers of the streaming solvers)
   std::vector<int32_t> slice_pat_host, pat_off_host;
+  std::vector<uint16_t> rmask_host;
   std::vector<int32_t> loc_sell, nl_sell;  // SELL slot of each CSR entry (value mirror)
   int64_t nnz_l = 0, nnz_n = 0;
   cudaStream_t main = nullptr;
@@ -230,6 +231,7 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   part->tile_win = P.tile_win;
   part->slice_pat_host = P.slice_pat;
   part->pat_off_host = P.pat_off;
+  part->rmask_host = P.rmask;
   part->nnz_l = int64_t(P.loc_col.size());
   part->nnz_n = int64_t(P.nl_col.size());
   part->stage = host_stage;
@@ -643,7 +645,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const int stage_bytes = want_stream ? stream_stage_bytes(D, by_index, &n_stages) : 0;
   const bool use_stream = want_stream && n_stages >= 2;
   const size_t o_hdr = use_stream ? take(sizeof(StageHdr) * n_tiles) : 0;
-  const size_t o_tab = use_stream ? take(sizeof(StageTab) * n_tiles) : 0;
+  const size_t o_rec = use_stream ? take(sizeof(TileRec) * n_tiles) : 0;
   LRB_CUDA(cudaMalloc(&D.ws, bytes));
   LRB_CUDA(cudaMemset(D.ws, 0, bytes));
   D.ws_bytes = bytes;
@@ -689,15 +691,30 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.stage_bytes = stage_bytes;
   H.n_stages = n_stages;
   H.tile_hdr = nullptr;
-  H.tile_tab = nullptr;
+  H.tile_rec = nullptr;
   if (use_stream) {
     std::vector<StageHdr> hdr;
     std::vector<StageTab> tab;
     build_stage_headers(D, by_index, stage_bytes, hdr, tab);
+    std::vector<TileRec> rec(hdr.size());
+    for (size_t t = 0; t < hdr.size(); ++t) {
+      rec[t].h = hdr[t];
+      rec[t].t = tab[t];
+      std::memset(rec[t].mask, 0, sizeof(rec[t].mask));
+    }
+    for (int p : D.parts) {
+      const lrb_part* P = by_index[p];
+      for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
+        TileRec& r = rec[P->d.tile0 + lt];
+        const int64_t row0 = lt * kTile, rows = std::min<int64_t>(kTile, P->d.n - row0);
+        if (int64_t(P->rmask_host.size()) >= row0 + rows)
+          std::memcpy(r.mask, P->rmask_host.data() + row0, sizeof(uint16_t) * rows);
+      }
+    }
     H.tile_hdr = w + o_hdr;
-    H.tile_tab = w + o_tab;
+    H.tile_rec = w + o_rec;
     LRB_CUDA(cudaMemcpy(w + o_hdr, hdr.data(), sizeof(StageHdr) * hdr.size(), cudaMemcpyHostToDevice));
-    LRB_CUDA(cudaMemcpy(w + o_tab, tab.data(), sizeof(StageTab) * tab.size(), cudaMemcpyHostToDevice));
+    LRB_CUDA(cudaMemcpy(w + o_rec, rec.data(), sizeof(TileRec) * rec.size(), cudaMemcpyHostToDevice));
   }
   for (int m = 0; m < 3; ++m) {
     const void* sfn = use_stream ? stream_kernel(m, D.inl) : nullptr;
@@ -834,7 +851,7 @@ static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int6
   }
   h.wtot = int32_t(wtot);
   if (h.nw <= 0) return 0;
-  const int64_t base = kHdrBytes + kTabBytes + h.vbytes + kMaskBytes;
+  const int64_t base = kRecBytes + h.vbytes;
   return std::max(base + 2 * wtot * 8, base + wtot * 8 + kVecTileBytes);
 }
 

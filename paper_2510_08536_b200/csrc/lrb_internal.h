@@ -121,6 +121,18 @@ constexpr int kTabBytes = kHdrPats * 16 * 8;
 struct alignas(16) StageTab {
   int2_t_ slot[kHdrPats][16];
 };
+
+// What a staged SpMV tile carries besides values and windows, as ONE
+// contiguous record so the producer moves it with one bulk copy: the header,
+// the slot tables and the tile's row masks (a copy of rmask).
+constexpr int kRecMaskBytes = kTile * 2;
+constexpr int kRecBytes = kHdrBytes + kTabBytes + kRecMaskBytes;
+struct alignas(16) TileRec {
+  StageHdr h;
+  StageTab t;
+  uint16_t mask[kTile];
+};
+static_assert(sizeof(TileRec) == kRecBytes, "tile record layout");
 enum Method { kCG = 0, kPCG = 1, kBiCGStab = 2 };
 
 struct SolveOut {
@@ -163,7 +175,7 @@ struct TeamDev {
   int32_t hist_cap;
   int32_t max_iter;
   const void* tile_hdr;     // streaming solvers: StageHdr per device tile
-  const void* tile_tab;     // streaming solvers: StageTab per device tile
+  const void* tile_rec;     // streaming solvers: TileRec per device tile (header | tables | masks)
   unsigned int* tile_ctr;   // streaming solvers: [2] dynamic tile counters (phase parity)
   long long* prof;          // phase-release timestamps (nullable, diagnostics)
   long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)

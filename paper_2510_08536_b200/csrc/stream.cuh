@@ -156,7 +156,7 @@ struct Spec {
 };
 
 __device__ __forceinline__ int stage_tail_offset(const StageHdr& H, int nwv) {
-  return nwv ? kHdrBytes + kTabBytes + H.vbytes + kMaskBytes + nwv * H.wtot * 8 : kHdrBytes;
+  return nwv ? kRecBytes + H.vbytes + nwv * H.wtot * 8 : kHdrBytes;
 }
 
 // ---------------------------------------------------------------------------
@@ -237,20 +237,17 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
     const unsigned vec_bytes = unsigned((rows * 8 + 15) & ~15);
     if (sp.nwv) {
       const bool tma = ctma != 0;
-      unsigned bytes = kHdrBytes;
-      if (tma)
-        bytes += kTabBytes + unsigned(cvb) + unsigned((rows * 2 + 15) & ~15) +
-                 unsigned(sp.nwv * cwtot * 8) + unsigned(sp.ntv) * vec_bytes;
+      // record (header | slot tables | masks) in one copy, then the values
+      const unsigned bytes = tma ? kRecBytes + unsigned(cvb) + unsigned(sp.nwv * cwtot * 8) +
+                                       unsigned(sp.ntv) * vec_bytes
+                                 : kHdrBytes;
       mbar_expect_tx(full, bytes);
-      bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
+      const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
+      bulk_g2s(st, recs + tile, tma ? kRecBytes : kHdrBytes, full, pol_vec);
       if (tma) {
-        bulk_g2s(st + kHdrBytes, reinterpret_cast<const StageTab*>(T.tile_tab) + tile, kTabBytes, full,
-                 pol_vec);
-        char* d = st + kHdrBytes + kTabBytes;
+        char* d = st + kRecBytes;
         bulk_g2s(d, P.val + cur.e0, unsigned(cvb), full, pol_stream);
         d += cvb;
-        bulk_g2s(d, P.rmask + row0, unsigned((rows * 2 + 15) & ~15), full, pol_stream);
-        d += kMaskBytes;
 #pragma unroll
         for (int v = 0; v < 2; ++v)
 #pragma unroll
@@ -806,10 +803,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           if (H.tma) {
-            const double* sval = reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes);
-            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes + H.vbytes);
-            const double* zw =
-                reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes + H.vbytes + kMaskBytes);
+            const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
+            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
+            const double* zw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
             const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
             const int lr = int(threadIdx.x);
             const int sl = lr >> 5;
@@ -891,11 +887,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           T, S, ring, red, 3, seq, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
           [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
             if (H.tma) {
-              const double* sval = reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes);
-              const uint16_t* smask =
-                  reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes + H.vbytes);
-              const double* xw =
-                  reinterpret_cast<const double*>(st + kHdrBytes + kTabBytes + H.vbytes + kMaskBytes);
+              const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
+              const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
+              const double* xw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
               const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
               const int lr = int(threadIdx.x);
               const int2* slot = slice_slots(st, H, lr >> 5);
