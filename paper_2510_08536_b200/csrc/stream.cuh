@@ -29,11 +29,15 @@
 namespace lrb {
 
 constexpr int kConsumers = kTile;               // one consumer thread per tile row (16 warps)
-constexpr int kStreamThreads = kConsumers + 32;  // + one producer warp
+constexpr int kStreamThreads = kConsumers + 64;  // + two producer warps (see produce_phase)
 constexpr int kMaskBytes = kTile * 2;          // uint16 row masks of a tile
 constexpr int kVecTileBytes = kTile * 8;       // one vector's rows of a tile
 constexpr int kStreamMaxStages = 4;
 constexpr int kMaxPack = 4;                     // tiles per stage in elementwise phases
+#ifndef LRB_SPMV_ISSUERS
+#define LRB_SPMV_ISSUERS 2
+#endif
+constexpr int kSpmvIssuers = LRB_SPMV_ISSUERS;  // producer warps alternating SpMV stages
 constexpr int kSlotRing = 2 * kStreamMaxStages; // group-sum slots (see consume_phase)
 constexpr int kConsumerBar = 1;                // named barrier of the consumer warps
 
@@ -129,6 +133,7 @@ struct StreamSmem {
   double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
   int32_t* wtile;      // [kSlotRing] first tile of the stage in the slot
   int32_t* wcnt;       // [kSlotRing] tiles of the stage in the slot
+  int32_t* ring;       // [2] ring position after the phase (stage, phase)
   unsigned long long* cnt;   // [kCnt] wait-cycle counters (diagnostics, T.prof_cta)
 };
 // Diagnostic counters per CTA: [phase kind (0 init, 1 A, 2 B, 3 C)][what]
@@ -197,8 +202,16 @@ __device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a, int
 // producer publishes a sentinel (stile = -1) through the ring.
 template <bool INL, class SpecF>
 __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                              int kind, unsigned* ctr, SpecF&& spec_of) {
+                                              int kind, unsigned*, SpecF&& spec_of) {
   if ((threadIdx.x & 31) != 0) return;
+  // kSpmvIssuers producer warps take alternate stages of the ring (stage
+  // sequence k -> warp k % kSpmvIssuers), each issuing all copies of its
+  // tiles: the per-copy issue cost no longer adds up on one thread.  Tiles
+  // are static (tile of stage k = cta + k * grid) so every issuer knows
+  // where the sentinel stage K* (first k with tile(k) >= n_tiles) falls.
+  // The ring position is re-synchronised from the consumers after the phase.
+  const int pw = (int(threadIdx.x) - kConsumers) >> 5;
+  if (pw >= kSpmvIssuers) return;
   const uint64_t pol_stream = policy_evict_first();   // values / masks: read once per phase
   const uint64_t pol_vec = policy_evict_normal();     // vectors: re-read by neighbour tiles
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
@@ -206,12 +219,13 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
   HdrAddr cur{}, nxt{};
   int32_t cwl[kMaxWin], cwoff[kMaxWin], cnw = 0, cwtot = 0, ctma = 0, cvb = 0;
   int32_t nwl[kMaxWin], nwoff[kMaxWin], nnw = 0, nwtot = 0, ntma = 0, nvb = 0;
-  // lookahead: tile indices two ahead, headers one ahead
-  int64_t tile = atomicAdd(ctr, 1u);
-  int64_t tn = tile < n_tiles ? int64_t(atomicAdd(ctr, 1u)) : n_tiles;
+  const int64_t step = int64_t(gridDim.x) * kSpmvIssuers;
+  int64_t tile = int64_t(blockIdx.x) + int64_t(pw) * gridDim.x;
+  for (int q = 0; q < pw; ++q) ring.next(T.n_stages);   // this issuer's first stage
   if (tile < n_tiles) load_hdr_addr(hdrs + tile, cur, cwl, cwoff, cnw, cwtot, ctma, cvb);
   while (true) {
-    const int64_t tnn = tn < n_tiles ? int64_t(atomicAdd(ctr, 1u)) : n_tiles;
+    if (tile >= n_tiles && tile - gridDim.x >= n_tiles) break;   // K* is another issuer's
+    const int64_t tn = tile + step;
     if (tn < n_tiles) load_hdr_addr(hdrs + tn, nxt, nwl, nwoff, nnw, nwtot, ntma, nvb);
     char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
     uint64_t* full = S.full + ring.stage;
@@ -220,10 +234,9 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
       mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
       if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
-    if (tile >= n_tiles) {   // sentinel: the consumers leave the phase
+    if (tile >= n_tiles) {   // sentinel stage K*: the consumers leave the phase
       S.stile[ring.stage] = -1;
       mbar_arrive(full);
-      ring.next(T.n_stages);
       break;
     }
     const long long ci = (kProf && T.prof_cta) ? clock64() : 0;
@@ -269,10 +282,19 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
     }
     if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
-    ring.next(T.n_stages);
+    for (int q = 0; q < kSpmvIssuers; ++q) ring.next(T.n_stages);
+    const bool last = tile + gridDim.x >= n_tiles;   // stage k+1 (sentinel or not) belongs to the next issuer
     tile = tn;
-    tn = tnn;
     cur = nxt;
+    if (last && kSpmvIssuers > 1) {
+      // stages after this one: the sentinel falls at the first k with
+      // tile(k) >= n_tiles; if that is not ours, stop here
+      if (tile >= n_tiles && (tile - step + gridDim.x) >= n_tiles) {
+        // our next tile is past the end and the sentinel stage belongs to the
+        // issuer right after us: nothing more to issue
+        break;
+      }
+    }
 #pragma unroll
     for (int w = 0; w < kMaxWin; ++w) {
       cwl[w] = nwl[w];
@@ -292,7 +314,7 @@ __device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem
 template <bool INL, class SpecF>
 __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const StreamSmem& S, Ring& ring,
                                                     int kind, unsigned* ctr, SpecF&& spec_of) {
-  if ((threadIdx.x & 31) != 0) return;
+  if ((threadIdx.x & 31) != 0 || threadIdx.x >= kConsumers + 32) return;   // producer warp 0
   const uint64_t pol_vec = policy_evict_normal();
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
   const int64_t n_tiles = T.n_tiles;
@@ -682,12 +704,13 @@ __device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
   S.ssub = S.scnt + kStreamMaxStages;
   S.wtile = S.ssub + kStreamMaxStages;
   S.wcnt = S.wtile + kSlotRing;
-  S.wsum = reinterpret_cast<double*>(S.wcnt + kSlotRing);   // 8-byte aligned
+  S.ring = S.wcnt + kSlotRing;
+  S.wsum = reinterpret_cast<double*>(S.ring + 2);   // 8-byte aligned
   return S;
 }
 __host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
   return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * 8 + 2 * kGroups * kMaxRed * 8 +
-         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 +
+         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 + 8 +
          size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8;
 }
 
@@ -719,10 +742,16 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
   } else {
     consume_phase<NR, INL>(T, S, ring, kind, spec_of, body);
   }
+  if (threadIdx.x == 0) {   // the consumers' ring position is the truth for every thread
+    S.ring[0] = ring.stage;
+    S.ring[1] = int(ring.phase);
+  }
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
   team_sync<NR, kRedLanes / kConsumers>(T, red, ctr);
   if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
+  ring.stage = S.ring[0];
+  ring.phase = unsigned(S.ring[1]);
   ++seq;
 }
 
