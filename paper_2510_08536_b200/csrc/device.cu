@@ -643,7 +643,8 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const bool want_stream = solver_choice() != 1;
   int n_stages = 0;
   const int stage_bytes = want_stream ? stream_stage_bytes(D, by_index, &n_stages) : 0;
-  const bool use_stream = want_stream && n_stages >= 2;
+  // the ring needs a stage per issuer and per consumer team in flight
+  const bool use_stream = want_stream && n_stages >= std::max(kTeams, kIssuers);
   const size_t o_hdr = use_stream ? take(sizeof(StageHdr) * n_tiles) : 0;
   const size_t o_rec = use_stream ? take(sizeof(TileRec) * n_tiles) : 0;
   LRB_CUDA(cudaMalloc(&D.ws, bytes));

@@ -1,46 +1,63 @@
 // Streaming (warp-specialized) persistent Krylov solvers for sm_100a.
 //
-// Same algorithms, rounding contract, tile decomposition and reduction order as
-// the classic team kernels in kernels.cuh (so both produce bit-identical
-// iterates), but the HBM traffic is moved by the bulk-copy engine instead of
-// per-thread gathers:
+// Same algorithms, rounding contract, tile decomposition and reduction order
+// as the classic team kernels in kernels.cuh (both produce bit-identical
+// iterates), but the HBM traffic is moved by the bulk-copy (TMA) engine into
+// a shared-memory ring instead of by per-thread gathers.
 //
-//   * one CTA per SM: 16 consumer warps (one thread per tile row; warp g is
-//     group g of the canonical tile tree, kernels.cuh) + 1 producer warp;
-//   * the producer walks this CTA's tiles of the current phase and, per tile,
-//     issues cp.async.bulk copies global -> shared into a ring of n_stages
-//     stages, each completing on the stage's "full" mbarrier (expect_tx):
-//       SpMV phases : the tile's SELL values (one contiguous run), its row
-//                     masks, and the <= kMaxWin operand windows of each vector
-//                     the phase reads (tile_win, plan.cpp), + tile vectors;
-//       elementwise : the tile's slice of every vector the phase reads;
-//   * consumers wait on "full", compute from shared memory, store results with
-//     coalesced st.global, and release the stage on its "empty" mbarrier;
-//   * phases end in the same deterministic team barrier/reduction (team_sync).
+// CTA = one per SM:
+//   * kIssuers producer warps; stage k of a phase is issued by warp
+//     k % kIssuers (lane 0), which waits for the slot's "empty" mbarrier and
+//     issues every bulk copy of the stage against its "full" mbarrier
+//     (expect_tx).  cp.async.bulk serializes per issuing thread at ~0.1-0.35
+//     us per copy (tools/tma_probe.cu), so alternate stages go to different
+//     warps (measured at C3: one issuer 11.2 ms/step, two 9.2 ms);
+//   * two consumer teams of 8 warps; team k % 2 consumes stage k.  Team
+//     thread t computes rows t and t + kTPB of the tile — the classic
+//     kernels' row mapping, so warp w of a team produces groups w and w + 8
+//     of the canonical tile tree (kernels.cuh);
+//   * phases end in the deterministic team barrier/reduction (team_sync).
 //
-// A tile whose pattern is not stageable (no windows: irregular slices, or too
-// large for a stage) is computed by the consumers with direct global loads,
-// exactly like the classic kernel.  Non-local (halo) columns are always read
-// directly from the owning part (peer memory for other devices).
+// Stage contents:
+//   SpMV phases (A: q = A p_new, C: |b - A x|): one tile = the tile record
+//     (header | slot tables | row masks, one copy), its SELL values (one
+//     copy), the <= kMaxWin operand windows of each vector the phase reads
+//     (tile_win, plan.cpp) and whole-tile vectors;
+//   elementwise phases (init, B): K consecutive tiles (the packing factor
+//     K = stage_bytes / tile bytes): their headers, then each vector's K
+//     tiles (one copy per vector).
+// Tiles are assigned statically (stage k of CTA c holds tile c + k * grid,
+// elementwise: chunk c + k * grid), so producers and consumers both know a
+// phase's stage count and no sentinel stages are needed.
+//
+// A tile whose pattern is not stageable (irregular slices, or too large for a
+// stage) is computed by the consumers with direct global loads, exactly like
+// the classic kernel.  Non-local (halo) columns are always read directly from
+// the owning part (peer memory for other devices).
 #pragma once
 
 #include "kernels.cuh"
 
 namespace lrb {
 
-constexpr int kConsumers = kTile;               // one consumer thread per tile row (16 warps)
-constexpr int kStreamThreads = kConsumers + 64;  // + two producer warps (see produce_phase)
-constexpr int kMaskBytes = kTile * 2;          // uint16 row masks of a tile
-constexpr int kVecTileBytes = kTile * 8;       // one vector's rows of a tile
-constexpr int kStreamMaxStages = 4;
-constexpr int kMaxPack = 4;                     // tiles per stage in elementwise phases
-#ifndef LRB_SPMV_ISSUERS
-#define LRB_SPMV_ISSUERS 2
+constexpr int kConsumers = kTile;                 // 16 consumer warps in two teams
+constexpr int kTeams = 2;
+constexpr int kTeamThreads = kConsumers / kTeams;
+constexpr int kTeamWarps = kTeamThreads / 32;
+static_assert(kTeamThreads == kTPB && kTile == kTPB * kRPT && kRPT == 2,
+              "a team thread computes rows t and t + kTPB, like the classic kernels");
+// issuer p fills exactly the stages team p consumes (G % kTeams == p)
+#ifndef LRB_ISSUERS
+#define LRB_ISSUERS 2
 #endif
-constexpr int kSpmvIssuers = LRB_SPMV_ISSUERS;  // producer warps alternating SpMV stages
-constexpr int kSlotRing = 2 * kStreamMaxStages; // group-sum slots (see consume_phase)
-constexpr int kConsumerBar = 1;                // named barrier of the consumer warps
-
+constexpr int kIssuers = LRB_ISSUERS;             // producer warps (alternate stages)
+static_assert(kIssuers == 1 || kIssuers == kTeams, "one issuer, or one per consumer team");
+constexpr int kStreamThreads = kConsumers + 32 * kIssuers;
+constexpr int kVecTileBytes = kTile * 8;          // one vector's rows of a tile
+constexpr int kStreamMaxStages = 4;
+constexpr int kMaxPack = 4;                       // tiles per stage in elementwise phases
+constexpr int kSlotRing = 2 * kStreamMaxStages;   // group-sum slots (see consume_phase)
+constexpr int kConsumerBar = 1;                   // named barrier of the consumer warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -90,18 +107,10 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
-}
-__device__ __forceinline__ void fence_proxy_async_shared() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -110,43 +119,41 @@ __device__ __forceinline__ void consumer_bar() {
   asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
 }
 
-// Ring position shared by producer and consumers (both walk the same tiles).
-struct Ring {
-  int stage = 0;
-  unsigned phase = 0;
-  __device__ __forceinline__ void next(int n) {
-    if (++stage == n) {
-      stage = 0;
-      phase ^= 1u;
-    }
-  }
-};
-
-struct StreamSmem {
-  char* stages;        // n_stages * stage_bytes
-  uint64_t* full;      // [n_stages]
-  uint64_t* empty;     // [n_stages]
-  double* wpart;       // [2][kGroups][kMaxRed]
-  int32_t* stile;      // [n_stages] first tile of each stage (-1: end of phase)
-  int32_t* scnt;       // [n_stages] tiles packed in the stage (elementwise phases: up to kMaxPack)
-  int32_t* ssub;       // [n_stages] byte stride between the packed tiles
-  double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
-  int32_t* wtile;      // [kSlotRing] first tile of the stage in the slot
-  int32_t* wcnt;       // [kSlotRing] tiles of the stage in the slot
-  int32_t* ring;       // [2] ring position after the phase (stage, phase)
-  unsigned long long* cnt;   // [kCnt] wait-cycle counters (diagnostics, T.prof_cta)
-};
-// Diagnostic counters per CTA: [phase kind (0 init, 1 A, 2 B, 3 C)][what]
-// what: 0 consumer warp 0 waiting for data, 1 end-of-phase consumer barrier,
-// 2 producer waiting for a free stage, 3 team barrier (thread 0, arrival ->
-// release), 4 warp 0 row bodies, 5 warp 0 group reduce + park, 6 warp 0 tile
-// sums, 7 producer issuing (stage free -> copies issued).
+// Diagnostic counters per CTA (build with -DLRB_PROF=1; lrb_team_profile_counters):
+// [phase kind (0 init, 1 A, 2 B, 3 C)][what]: 0 consumer thread 0 waiting for
+// data, 1 end-of-phase consumer barrier, 2 issuer 0 waiting for a free stage,
+// 3 team barrier (thread 0, arrival -> release), 4 thread 0 row bodies,
+// 5 thread 0 group reduce + park, 6 thread 0 tile sums, 7 issuer 0 issuing.
 #ifndef LRB_PROF
-#define LRB_PROF 0   // build with -DLRB_PROF=1 for the wait/issue counters
+#define LRB_PROF 0
 #endif
 constexpr bool kProf = LRB_PROF != 0;
 constexpr int kCntPer = 8;
 constexpr int kCnt = 4 * kCntPer;
+
+struct StreamSmem {
+  char* stages;        // n_stages * stage_bytes
+  uint64_t* full;      // [kStreamMaxStages][kTeams]
+  uint64_t* empty;     // [kStreamMaxStages][kTeams]
+  double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
+  unsigned long long* cnt;   // [kCnt]
+};
+
+__device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
+  extern __shared__ __align__(128) char dsm[];
+  StreamSmem S;
+  S.stages = dsm;
+  char* tail = dsm + size_t(T.n_stages) * T.stage_bytes;
+  S.full = reinterpret_cast<uint64_t*>(tail);
+  S.empty = S.full + kStreamMaxStages * kTeams;
+  S.wsum = reinterpret_cast<double*>(S.empty + kStreamMaxStages * kTeams);
+  S.cnt = reinterpret_cast<unsigned long long*>(S.wsum + size_t(kSlotRing) * kMaxPack * kGroups * 2);
+  return S;
+}
+__host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
+  return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * kTeams * 8 +
+         size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8 + kCnt * 8;
+}
 
 __device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool inl) {
   return inl ? T.lp[p - T.part_begin] : T.parts[p];
@@ -164,224 +171,197 @@ __device__ __forceinline__ int stage_tail_offset(const StageHdr& H, int nwv) {
   return nwv ? kRecBytes + H.vbytes + nwv * H.wtot * 8 : kHdrBytes;
 }
 
+// Static stage sequence of a phase for this CTA: stage k holds unit
+// cta + k * grid (a tile in SpMV phases, a chunk of K tiles in elementwise
+// phases); the CTA's stage count.
+__device__ __forceinline__ int stage_count(int64_t units) {
+  return int64_t(blockIdx.x) < units ? int((units - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+}
+// Packing factor of an elementwise phase with ntv vectors.
+__device__ __forceinline__ int pack_factor(const TeamDev& T, int ntv) {
+  const int k = T.stage_bytes / (kHdrBytes + ntv * kVecTileBytes);
+  return k < 1 ? 1 : (k > kMaxPack ? kMaxPack : k);
+}
+// Ring position of the CTA's global stage number G (G = gseq + phase-local
+// stage; identical in every thread).  Stage G lives in slot G % n_stages and
+// belongs to consumer team (and issuer) G % kTeams.  Every (slot, team) pair
+// has its own full/empty mbarriers: a pair recurs every L = lcm(n_stages,
+// kTeams) stages, always for the same team, so each barrier is waited on in
+// phase order by one team (consumers) or after its previous phase was seen
+// (issuers) — a parity wait can never be satisfied by a stale phase, which a
+// slot shared by two teams would allow.
+struct RingPos {
+  int slot;
+  int team;
+  int bar;           // slot * kTeams + team
+  unsigned parity;   // parity of this use of the pair's barriers
+};
+__device__ __forceinline__ RingPos ring_pos(int G, int n_stages) {
+  const int L = (n_stages % kTeams) ? n_stages * kTeams : n_stages;
+  const int slot = G % n_stages, team = G % kTeams;
+  return RingPos{slot, team, slot * kTeams + team, unsigned((G / L) & 1)};
+}
+// First phase-local stage k of this CTA with (gseq + k) % m == r.
+__device__ __forceinline__ int first_stage(int gseq, int r, int m) {
+  return ((r - gseq) % m + m) % m;
+}
+// Issuer side: before filling stage G, wait until the previous stage in the
+// same slot (G - n_stages, possibly of an earlier phase) was released.
+__device__ __forceinline__ void wait_slot_free(const StreamSmem& S, int G, int n_stages, long long timeout_ns) {
+  const int Gp = G - n_stages;
+  if (Gp < 0) return;
+  const RingPos pp = ring_pos(Gp, n_stages);
+  mbar_wait(S.empty + pp.bar, pp.parity, timeout_ns);
+}
+
 // ---------------------------------------------------------------------------
-// Producer: warp 8, lane 0.  Tile headers are precomputed at team creation
-// (T.tile_hdr, one StageHdr per device tile); the producer reads the next
-// tile's addressing fields one tile ahead (their latency hides behind the
-// current tile's copies) and bulk-copies the header itself into the stage.
+// Producers
 // ---------------------------------------------------------------------------
-struct HdrAddr {   // the fields the producer needs, 48 bytes
+struct HdrAddr {   // the header fields a producer needs
   int64_t row0, e0;
   int64_t wa[kMaxWin];
-  int32_t rows, part;
+  int32_t wl[kMaxWin], woff[kMaxWin];
+  int32_t rows, part, nw, wtot, tma, vbytes;
 };
-__device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a, int32_t (&wl)[kMaxWin],
-                                              int32_t (&woff)[kMaxWin], int32_t& nw, int32_t& wtot,
-                                              int32_t& tma, int32_t& vbytes) {
+__device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a) {
   a.row0 = __ldg(&h->row0);
   a.e0 = __ldg(&h->e0);
 #pragma unroll
   for (int w = 0; w < kMaxWin; ++w) {
     a.wa[w] = __ldg(&h->wa[w]);
-    wl[w] = __ldg(&h->wl[w]);
-    woff[w] = __ldg(&h->woff[w]);
+    a.wl[w] = __ldg(&h->wl[w]);
+    a.woff[w] = __ldg(&h->woff[w]);
   }
   a.rows = __ldg(&h->rows);
   a.part = __ldg(&h->part);
-  nw = __ldg(&h->nw);
-  wtot = __ldg(&h->wtot);
-  tma = __ldg(&h->tma);
-  vbytes = __ldg(&h->vbytes);
+  a.nw = __ldg(&h->nw);
+  a.wtot = __ldg(&h->wtot);
+  a.tma = __ldg(&h->tma);
+  a.vbytes = __ldg(&h->vbytes);
 }
 
-// Tiles are handed out dynamically: the producer grabs the next tile of the
-// phase from the device's phase counter (atomicAdd, issued one tile ahead so
-// its latency hides behind the current tile's copies), so CTAs finish a
-// phase together whatever their bandwidth share.  Partials are per tile, so
-// results do not depend on which CTA computed a tile.  After the last tile the
-// producer publishes a sentinel (stile = -1) through the ring.
+// SpMV phases: issuer pw issues stages k = pw, pw + kIssuers, ... (tile
+// cta + k * grid), reading each tile's header one of its stages ahead.
 template <bool INL, class SpecF>
-__device__ __forceinline__ void produce_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                              int kind, unsigned*, SpecF&& spec_of) {
-  if ((threadIdx.x & 31) != 0) return;
-  // kSpmvIssuers producer warps take alternate stages of the ring (stage
-  // sequence k -> warp k % kSpmvIssuers), each issuing all copies of its
-  // tiles: the per-copy issue cost no longer adds up on one thread.  Tiles
-  // are static (tile of stage k = cta + k * grid) so every issuer knows
-  // where the sentinel stage K* (first k with tile(k) >= n_tiles) falls.
-  // The ring position is re-synchronised from the consumers after the phase.
+__device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem& S, int gseq, int kind,
+                                             SpecF&& spec_of) {
   const int pw = (int(threadIdx.x) - kConsumers) >> 5;
-  if (pw >= kSpmvIssuers) return;
-  const uint64_t pol_stream = policy_evict_first();   // values / masks: read once per phase
+  if ((threadIdx.x & 31) != 0) return;
+  const uint64_t pol_stream = policy_evict_first();   // values: read once per phase
   const uint64_t pol_vec = policy_evict_normal();     // vectors: re-read by neighbour tiles
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
-  const int64_t n_tiles = T.n_tiles;
+  const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
+  const int64_t G = gridDim.x;
+  const int count = stage_count(T.n_tiles);
   HdrAddr cur{}, nxt{};
-  int32_t cwl[kMaxWin], cwoff[kMaxWin], cnw = 0, cwtot = 0, ctma = 0, cvb = 0;
-  int32_t nwl[kMaxWin], nwoff[kMaxWin], nnw = 0, nwtot = 0, ntma = 0, nvb = 0;
-  const int64_t step = int64_t(gridDim.x) * kSpmvIssuers;
-  int64_t tile = int64_t(blockIdx.x) + int64_t(pw) * gridDim.x;
-  for (int q = 0; q < pw; ++q) ring.next(T.n_stages);   // this issuer's first stage
-  if (tile < n_tiles) load_hdr_addr(hdrs + tile, cur, cwl, cwoff, cnw, cwtot, ctma, cvb);
-  while (true) {
-    if (tile >= n_tiles && tile - gridDim.x >= n_tiles) break;   // K* is another issuer's
-    const int64_t tn = tile + step;
-    if (tn < n_tiles) load_hdr_addr(hdrs + tn, nxt, nwl, nwoff, nnw, nwtot, ntma, nvb);
-    char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
-    uint64_t* full = S.full + ring.stage;
+  const int k0 = first_stage(gseq, pw, kIssuers);
+  if (k0 < count) load_hdr_addr(hdrs + blockIdx.x + k0 * G, cur);
+  for (int k = k0; k < count; k += kIssuers) {
+    const int64_t tile = blockIdx.x + k * G;
+    if (k + kIssuers < count) load_hdr_addr(hdrs + tile + kIssuers * G, nxt);
+    const RingPos rp = ring_pos(gseq + k, T.n_stages);
+    char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
+    uint64_t* full = S.full + rp.bar;
     {
-      const long long c0 = (kProf && T.prof_cta) ? clock64() : 0;
-      mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
-      if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - c0;
+      const long long c0 = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
+      wait_slot_free(S, gseq + k, T.n_stages, T.timeout_ns);
+      if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
-    if (tile >= n_tiles) {   // sentinel stage K*: the consumers leave the phase
-      S.stile[ring.stage] = -1;
-      mbar_arrive(full);
-      break;
-    }
-    const long long ci = (kProf && T.prof_cta) ? clock64() : 0;
-    S.stile[ring.stage] = int32_t(tile);
-    S.scnt[ring.stage] = 1;
-    S.ssub[ring.stage] = 0;
+    const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
     const PartDev& P = part_of(T, cur.part, INL);
     const Spec sp = spec_of(P);
-    const int rows = cur.rows;
-    const int64_t row0 = cur.row0;
-    const unsigned vec_bytes = unsigned((rows * 8 + 15) & ~15);
-    if (sp.nwv) {
-      const bool tma = ctma != 0;
-      // record (header | slot tables | masks) in one copy, then the values
-      const unsigned bytes = tma ? kRecBytes + unsigned(cvb) + unsigned(sp.nwv * cwtot * 8) +
-                                       unsigned(sp.ntv) * vec_bytes
-                                 : kHdrBytes;
-      mbar_expect_tx(full, bytes);
-      const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
-      bulk_g2s(st, recs + tile, tma ? kRecBytes : kHdrBytes, full, pol_vec);
-      if (tma) {
-        char* d = st + kRecBytes;
-        bulk_g2s(d, P.val + cur.e0, unsigned(cvb), full, pol_stream);
-        d += cvb;
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-#pragma unroll
-          for (int w = 0; w < kMaxWin; ++w)
-            if (v < sp.nwv && w < cnw)
-              bulk_g2s(d + (size_t(v) * cwtot + cwoff[w]) * 8, sp.wv[v] + cur.wa[w],
-                       unsigned(cwl[w] * 8), full, pol_vec);
-        d += size_t(sp.nwv) * cwtot * 8;
-#pragma unroll
-        for (int v = 0; v < 5; ++v)
-          if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
-      }
-    } else {
-      mbar_expect_tx(full, kHdrBytes + unsigned(sp.ntv) * vec_bytes);
+    const unsigned vec_bytes = unsigned((cur.rows * 8 + 15) & ~15);
+    if (!cur.tma) {
+      mbar_expect_tx(full, kHdrBytes);
       bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
-      char* d = st + kHdrBytes;
+    } else {
+      // record (header | slot tables | masks), values, windows, tile vectors
+      mbar_expect_tx(full, kRecBytes + unsigned(cur.vbytes) + unsigned(sp.nwv * cur.wtot * 8) +
+                               unsigned(sp.ntv) * vec_bytes);
+      bulk_g2s(st, recs + tile, kRecBytes, full, pol_vec);
+      char* d = st + kRecBytes;
+      bulk_g2s(d, P.val + cur.e0, unsigned(cur.vbytes), full, pol_stream);
+      d += cur.vbytes;
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int w = 0; w < kMaxWin; ++w)
+          if (v < sp.nwv && w < cur.nw)
+            bulk_g2s(d + (size_t(v) * cur.wtot + cur.woff[w]) * 8, sp.wv[v] + cur.wa[w],
+                     unsigned(cur.wl[w] * 8), full, pol_vec);
+      d += size_t(sp.nwv) * cur.wtot * 8;
 #pragma unroll
       for (int v = 0; v < 5; ++v)
-        if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + row0, vec_bytes, full, pol_vec);
+        if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + cur.row0, vec_bytes, full, pol_vec);
     }
-    if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
-    for (int q = 0; q < kSpmvIssuers; ++q) ring.next(T.n_stages);
-    const bool last = tile + gridDim.x >= n_tiles;   // stage k+1 (sentinel or not) belongs to the next issuer
-    tile = tn;
+    if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 7] += clock64() - ci;
     cur = nxt;
-    if (last && kSpmvIssuers > 1) {
-      // stages after this one: the sentinel falls at the first k with
-      // tile(k) >= n_tiles; if that is not ours, stop here
-      if (tile >= n_tiles && (tile - step + gridDim.x) >= n_tiles) {
-        // our next tile is past the end and the sentinel stage belongs to the
-        // issuer right after us: nothing more to issue
-        break;
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < kMaxWin; ++w) {
-      cwl[w] = nwl[w];
-      cwoff[w] = nwoff[w];
-    }
-    cnw = nnw;
-    cwtot = nwtot;
-    ctma = ntma;
-    cvb = nvb;
   }
 }
 
-// Elementwise phases: a tile needs only kHdrBytes + ntv * kVecTileBytes, so
-// the producer grabs K consecutive tiles per atomic and packs them into one
-// stage (K = stage_bytes / tile bytes, at most kMaxPack): K times the bytes in
-// flight of one tile per stage, with the same ring.
+// Elementwise phases: stage k holds chunk q = cta + k * grid = tiles
+// [q * K, q * K + K) ∩ [0, n_tiles): the headers, then each vector's tiles
+// (one copy per vector when the tiles belong to one part).
 template <bool INL, class SpecF>
-__device__ __forceinline__ void produce_elementwise(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                                    int kind, unsigned* ctr, SpecF&& spec_of) {
-  if ((threadIdx.x & 31) != 0 || threadIdx.x >= kConsumers + 32) return;   // producer warp 0
+__device__ __forceinline__ void produce_elementwise(const TeamDev& T, const StreamSmem& S, int gseq,
+                                                    int kind, SpecF&& spec_of) {
+  const int pw = (int(threadIdx.x) - kConsumers) >> 5;
+  if ((threadIdx.x & 31) != 0) return;
   const uint64_t pol_vec = policy_evict_normal();
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
   const int64_t n_tiles = T.n_tiles;
   const bool one_part = T.part_end - T.part_begin == 1;
   const int ntv = spec_of(part_of(T, T.part_begin, INL)).ntv;
-  const int sub = kHdrBytes + ntv * kVecTileBytes;
-  int K = T.stage_bytes / sub;
-  K = K < 1 ? 1 : (K > kMaxPack ? kMaxPack : K);
-  int64_t c0 = atomicAdd(ctr, unsigned(K));
-  int64_t c1 = c0 < n_tiles ? int64_t(atomicAdd(ctr, unsigned(K))) : n_tiles;
-  while (true) {
-    const int64_t c2 = c1 < n_tiles ? int64_t(atomicAdd(ctr, unsigned(K))) : n_tiles;
-    char* st = S.stages + size_t(ring.stage) * T.stage_bytes;
-    uint64_t* full = S.full + ring.stage;
+  const int K = pack_factor(T, ntv);
+  const int count = stage_count((n_tiles + K - 1) / K);
+  for (int k = first_stage(gseq, pw, kIssuers); k < count; k += kIssuers) {
+    const int64_t c0 = (int64_t(blockIdx.x) + int64_t(k) * gridDim.x) * K;
+    const RingPos rp = ring_pos(gseq + k, T.n_stages);
+    char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
+    uint64_t* full = S.full + rp.bar;
     {
-      const long long t0 = (kProf && T.prof_cta) ? clock64() : 0;
-      mbar_wait(S.empty + ring.stage, ring.phase ^ 1u, T.timeout_ns);
-      if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 2] += clock64() - t0;
+      const long long t0 = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
+      wait_slot_free(S, gseq + k, T.n_stages, T.timeout_ns);
+      if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - t0;
     }
-    if (c0 >= n_tiles) {
-      S.stile[ring.stage] = -1;
-      mbar_arrive(full);
-      ring.next(T.n_stages);
-      break;
-    }
-    const long long ci = (kProf && T.prof_cta) ? clock64() : 0;
+    const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
     const int cnt = int(n_tiles - c0 < K ? n_tiles - c0 : K);
-    S.stile[ring.stage] = int32_t(c0);
-    S.scnt[ring.stage] = cnt;
-    S.ssub[ring.stage] = sub;
     int part[kMaxPack], rows[kMaxPack];
     int64_t row0[kMaxPack];
-    unsigned bytes = 0;
+    unsigned bytes = unsigned(cnt) * kHdrBytes;
 #pragma unroll
     for (int j = 0; j < kMaxPack; ++j) {
+      part[j] = T.part_begin;
+      rows[j] = 0;
+      row0[j] = 0;
       if (j < cnt) {
         const int64_t tile = c0 + j;
         part[j] = one_part ? T.part_begin : __ldg(T.tile_part + tile);
         const PartDev& P = part_of(T, part[j], INL);
         row0[j] = (tile - P.tile0) * kTile;
         rows[j] = int(P.n - row0[j] < kTile ? P.n - row0[j] : int64_t(kTile));
-        bytes += kHdrBytes;
       }
     }
-    if (part[0] == part[cnt - 1])
-      bytes += unsigned(ntv) * unsigned(((row0[cnt - 1] + rows[cnt - 1] - row0[0]) * 8 + 15) & ~int64_t(15));
+    const bool merged = part[0] == part[cnt - 1];
+    const unsigned span = unsigned(((row0[cnt - 1] + rows[cnt - 1] - row0[0]) * 8 + 15) & ~int64_t(15));
+    if (merged)
+      bytes += unsigned(ntv) * span;
     else
       for (int j = 0; j < cnt; ++j) bytes += unsigned(ntv) * unsigned((rows[j] * 8 + 15) & ~15);
     mbar_expect_tx(full, bytes);
-    // stage layout: [cnt headers][vector 0: cnt tiles][vector 1: cnt tiles]...
-    // consecutive tiles of one part are contiguous rows: one copy per vector
     bulk_g2s(st, hdrs + c0, unsigned(cnt) * kHdrBytes, full, pol_vec);
     char* vbase = st + size_t(cnt) * kHdrBytes;
     const size_t vstride = size_t(cnt) * kVecTileBytes;
-    if (part[0] == part[cnt - 1]) {
-      const PartDev& P = part_of(T, part[0], INL);
-      const Spec sp = spec_of(P);
-      const unsigned vb = unsigned(((row0[cnt - 1] + rows[cnt - 1] - row0[0]) * 8 + 15) & ~int64_t(15));
+    if (merged) {
+      const Spec sp = spec_of(part_of(T, part[0], INL));
 #pragma unroll
       for (int v = 0; v < 5; ++v)
-        if (v < sp.ntv) bulk_g2s(vbase + v * vstride, sp.tv[v] + row0[0], vb, full, pol_vec);
+        if (v < sp.ntv) bulk_g2s(vbase + v * vstride, sp.tv[v] + row0[0], span, full, pol_vec);
     } else {
 #pragma unroll
       for (int j = 0; j < kMaxPack; ++j) {
         if (j < cnt) {
-          const PartDev& P = part_of(T, part[j], INL);
-          const Spec sp = spec_of(P);
+          const Spec sp = spec_of(part_of(T, part[j], INL));
           const unsigned vb = unsigned((rows[j] * 8 + 15) & ~15);
 #pragma unroll
           for (int v = 0; v < 5; ++v)
@@ -390,48 +370,13 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
         }
       }
     }
-    if (kProf && T.prof_cta) S.cnt[kind * kCntPer + 7] += clock64() - ci;
-    ring.next(T.n_stages);
-    c0 = c1;
-    c1 = c2;
+    if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 7] += clock64() - ci;
   }
 }
 
-// Position of local column c in the staged windows (or -1).
-struct WinMap {
-  int64_t wa0, wa1, wa2;
-  int wl0, wl1, wl2, wo1, wo2;
-  __device__ __forceinline__ int pos(int64_t c) const {
-    unsigned d = unsigned(c - wa0);
-    if (d < unsigned(wl0)) return int(d);
-    d = unsigned(c - wa1);
-    if (d < unsigned(wl1)) return wo1 + int(d);
-    d = unsigned(c - wa2);
-    if (d < unsigned(wl2)) return wo2 + int(d);
-    return -1;
-  }
-};
-__device__ __forceinline__ WinMap win_map(const StageHdr& H) {
-  WinMap M;
-  M.wa0 = H.wa[0];
-  M.wa1 = H.wa[1];
-  M.wa2 = H.wa[2];
-  M.wl0 = H.nw > 0 ? H.wl[0] : 0;
-  M.wl1 = H.nw > 1 ? H.wl[1] : 0;
-  M.wl2 = H.nw > 2 ? H.wl[2] : 0;
-  M.wo1 = H.woff[1];
-  M.wo2 = H.woff[2];
-  return M;
-}
-
-// Staged SpMV of the consumer thread's row (lr = tid).  Per warp slice, lane k
-// owns pattern slot k: its column offset and the shared-memory index delta of
-// the window holding that offset's columns (computed once per slice instead
-// of a window search per entry), broadcast with shuffles.  Every local column
-// of a staged tile lies in a window by construction (plan.cpp
-// build_tile_windows).  Entries accumulate in stored order with the reference
-// rounding.  xs(q): staged operand at smem index q; fh(owner part, row): halo
-// column.  Returns A_row . x.
+// ---------------------------------------------------------------------------
+// Consumers: staged row products
+// ---------------------------------------------------------------------------
 // Operand of a staged window position: NV = 1: w0[q]; NV = 2: the on-the-fly
 // p_new = w0[q] + beta * w1[q] (z and p_old windows, reference rounding).
 template <int NV>
@@ -445,7 +390,9 @@ __device__ __forceinline__ double staged_operand(const double* __restrict__ w0,
 }
 
 // Fixed-width row product: WM pattern slots, all operand loads issued
-// before the accumulation chain (slots k >= w and holes are masked to 0).
+// before the accumulation chain (slots k >= w and holes are masked to 0:
+// holes hold 0.0 in the SELL layout, so acc + 0 * 0 leaves acc unchanged —
+// acc is never -0.0).
 template <int NV, int WM>
 __device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
                                             const int2* __restrict__ slot,
@@ -466,11 +413,13 @@ __device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
   return acc;
 }
 
-// Slot table of the warp's slice in the staged StageTab.
+// Slot table of a slice in the staged StageTab: for slot k, (column offset,
+// delta e such that row i's operand sits at staged index i + e).
 __device__ __forceinline__ const int2* slice_slots(const char* st, const StageHdr& H, int sl) {
   return reinterpret_cast<const int2*>(st + kHdrBytes) + H.spat[sl] * 16;
 }
 
+// Staged SpMV of tile row lr (its 32-row slice is warp-uniform).
 template <int NV, bool HALO, class FH>
 __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ hpart,
                                                   const int32_t* __restrict__ hidx,
@@ -483,7 +432,7 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
                                                   FH&& fh) {
   const int lane = threadIdx.x & 31;
   const int rows = H.rows;
-  const int lr0 = lr & ~31;                    // warp-uniform
+  const int lr0 = lr & ~31;
   const int sl = lr0 >> 5;
   const int s0 = H.sp[sl];
   const int w = lr0 < rows ? (H.sp[sl + 1] - s0) >> 5 : 0;
@@ -495,8 +444,6 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
     if (w <= 8) return row_fixed<NV, 8>(w, ii, eb, msk, slot, sval, w0, w1, beta);
     return row_fixed<NV, kPatW>(w, ii, eb, msk, slot, sval, w0, w1, beta);
   } else {
-    // holes (mask bit clear) have value 0.0 in the SELL layout and get operand
-    // 0.0 here, so acc + 0 * 0 leaves acc unchanged (acc is never -0.0)
     double acc = 0.0;
     for (int k = 0; k < w; ++k) {
       const int2 se = slot[k];
@@ -525,149 +472,95 @@ struct VecView {
   }
 };
 
-// Tile sum of the stage in slot ss: group g's sum of sub-tile j was parked at
-// wsum[ss % kSlotRing][j][g] by warp g; warp (ss*kMaxPack + j) % kGroups adds
-// the 16 group sums in group order (the canonical tile tree, kernels.cuh).
+// ---------------------------------------------------------------------------
+// Consumers: phase loop and deferred tile sums
+// ---------------------------------------------------------------------------
+// Tile sums of stage k (slot k % kSlotRing): group g's sum of its tile j was
+// parked at wsum[slot][j][g]; the designated warp adds the 16 group sums in
+// group order (the canonical tile tree) into T.partials[tile].
 template <int NR>
-__device__ __forceinline__ void sum_stage_slot(const TeamDev& T, const StreamSmem& S, int ss) {
-  const int sl = ss % kSlotRing;
-  const int cnt = S.wcnt[sl];
-  const int64_t t0 = S.wtile[sl];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S, int k, int64_t tile0,
+                                          int cnt, int warp_sel, int n_sel, int my_warp) {
+  const int lane = threadIdx.x & 31;
+  const int sl = k % kSlotRing;
   for (int j = 0; j < cnt; ++j) {
-    if (warp == ((ss * kMaxPack + j) & (kGroups - 1)) && lane < NR) {
+    if (my_warp == (warp_sel + j) % n_sel && lane < NR) {
       const double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups) * 2;
       double sum = w[lane];
 #pragma unroll
       for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * 2 + lane]);
-      T.partials[(t0 + j) * kMaxRed + lane] = sum;
+      T.partials[(tile0 + j) * kMaxRed + lane] = sum;
     }
   }
 }
 
-// L2 prefetch of a future tile (the bulk copies of whoever processes it then
-// hit L2): its SELL values and row masks (SpMV phases) and its own rows of
-// every vector the phase reads.  Issued by the consumers, spread one line
-// per thread, PD = kPrefetchRounds * grid tiles ahead of the tile being
-// computed (dynamic scheduling hands tiles out in increasing order, so every
-// tile is prefetched once, about that many tiles before it is copied).
-// Off by default: measured on B200 at C3 it slows the solve 11.1 -> 15.5 ms
-// (the consumers stall on the prefetch addresses and the extra L2 requests
-// compete with the bulk copies).  -DLRB_PREFETCH_ROUNDS=2 to experiment.
-#ifndef LRB_PREFETCH_ROUNDS
-#define LRB_PREFETCH_ROUNDS 0
-#endif
-constexpr int kPrefetchRounds = LRB_PREFETCH_ROUNDS;
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-struct PrefetchTarget {
-  int64_t row0, e0;
-  int32_t rows, part, vbytes, ok;
-};
-
-__device__ __forceinline__ PrefetchTarget prefetch_target(const TeamDev& T, int64_t tile) {
-  PrefetchTarget f{0, 0, 0, 0, 0, 0};
-  if (kPrefetchRounds > 0 && tile < T.n_tiles) {
-    const StageHdr* h = reinterpret_cast<const StageHdr*>(T.tile_hdr) + tile;
-    f.row0 = __ldg(&h->row0);
-    f.e0 = __ldg(&h->e0);
-    f.rows = __ldg(&h->rows);
-    f.part = __ldg(&h->part);
-    f.vbytes = __ldg(&h->vbytes);
-    f.ok = 1;
-  }
-  return f;
-}
-
-template <bool INL, class SpecF>
-__device__ __forceinline__ void prefetch_tile(const TeamDev& T, const PrefetchTarget& f, SpecF&& spec_of) {
-  if (!f.ok) return;
-  const PartDev& Q = part_of(T, f.part, INL);
-  const Spec sp = spec_of(Q);
-  const int t = threadIdx.x;
-  const int vl = (f.rows * 8 + 127) >> 7;   // 128-byte lines of one vector's rows
-  int line = t;
-  if (sp.nwv) {
-    const char* vb = reinterpret_cast<const char*>(Q.val + f.e0);
-    for (int off = t * 128; off < f.vbytes; off += kConsumers * 128) prefetch_l2(vb + off);
-    line -= (f.vbytes + 127) >> 7;
-    const int ml = (f.rows * 2 + 127) >> 7;
-    if (line >= 0 && line < ml) prefetch_l2(reinterpret_cast<const char*>(Q.rmask + f.row0) + line * 128);
-    line -= ml;
-  }
-  if (line < 0) line += kConsumers;   // threads past the values take the vectors
-  const int nv = sp.nwv + sp.ntv;
-  if (line >= 0 && line < nv * vl) {
-    const int v = line / vl;
-    const double* vec = v < sp.nwv ? sp.wv[v] : sp.tv[v - sp.nwv];
-    prefetch_l2(reinterpret_cast<const char*>(vec + f.row0) + (line - v * vl) * 128);
-  }
-}
-
-// Consumer side of one phase: thread tid computes row tid of each tile
-// (body(P, H, st, acc)); warp g's butterfly sum is group g of the canonical
-// tile tree and is parked in the stage's group-sum slot.  No per-tile block
-// barrier: a warp that starts stage ss knows (through the ring: the producer
-// refilled that stage only after every warp released stage ss - n_stages)
-// that all group sums of stage ss - n_stages are written, and sums them then;
-// the last n_stages stages are summed after one barrier at the end.  Slots
-// are reused after kSlotRing = 2 * max stages, beyond the fastest warp's lead.
-template <int NR, bool INL, class SpecF, class Body>
-__device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                              int kind, SpecF&& spec_of, Body&& body) {
+// Team tm consumes stages k = tm, tm + 2, ...; per tile each thread computes
+// rows t and t + kTPB (body(P, H, st, V, lr, acc)), butterfly-reduces each into
+// its group (warp w of the team: groups w and w + 8) and parks the group sums
+// in the stage's slot.  No per-tile barrier: a warp that starts stage k knows
+// (through the ring: the producer refilled that slot only after stage
+// k - n_stages was released) that every group sum of stage k - n_stages is
+// written, and a warp of its team sums that stage; the last n_stages stages
+// are summed after one barrier at the end of the phase.  Slots are reused
+// after kSlotRing = 2 * max stages stages, beyond the fastest warp's lead.
+template <int NR, bool INL, bool ELEM, class Body>
+__device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, int gseq, int kind,
+                                              int ntv, Body&& body) {
   static_assert(NR <= 2, "group-sum slots hold two reductions");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = warp / kTeamWarps;             // team
+  const int wt = warp - tm * kTeamWarps;        // warp within the team
+  const int tt = int(threadIdx.x) - tm * kTeamThreads;
   const int ns = T.n_stages;
-  int ss = 0;
-  for (;; ++ss) {
-    const char* st0 = S.stages + size_t(ring.stage) * T.stage_bytes;
-    const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-    mbar_wait(S.full + ring.stage, ring.phase, T.timeout_ns);
-    if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
+  const int64_t G = gridDim.x;
+  const int K = ELEM ? pack_factor(T, ntv) : 1;
+  const int64_t n_tiles = T.n_tiles;
+  const int count = stage_count(ELEM ? (n_tiles + K - 1) / K : n_tiles);
+  auto first_tile = [&](int k) -> int64_t { return (int64_t(blockIdx.x) + int64_t(k) * G) * K; };
+  auto tiles_in = [&](int k) -> int {
+    const int64_t t0 = first_tile(k);
+    return int(n_tiles - t0 < K ? n_tiles - t0 : K);
+  };
+  for (int k = first_stage(gseq, tm, kTeams); k < count; k += kTeams) {
+    const RingPos rp = ring_pos(gseq + k, ns);
+    const char* st0 = S.stages + size_t(rp.slot) * T.stage_bytes;
     {
+      const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      mbar_wait(S.full + rp.bar, rp.parity, T.timeout_ns);
+      if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
+    }
+    if (k >= ns) {
       const long long c2 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      if (ss >= ns) sum_stage_slot<NR>(T, S, ss - ns);
+      const int kd = k - ns;
+      sum_stage<NR>(T, S, kd, first_tile(kd), tiles_in(kd), (kd * kMaxPack) % kTeamWarps, kTeamWarps, wt);
       if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 6] += clock64() - c2;
     }
-    const int64_t tile0 = S.stile[ring.stage];
-    if (tile0 < 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(S.empty + ring.stage);
-      ring.next(ns);
-      break;
-    }
-    const int cnt = S.scnt[ring.stage];
-    const int sub = S.ssub[ring.stage];
-    const int sl = ss % kSlotRing;
-    if (threadIdx.x == 0) {
-      S.wtile[sl] = int32_t(tile0);
-      S.wcnt[sl] = cnt;
-    }
-    const int64_t pd = int64_t(kPrefetchRounds) * gridDim.x;
+    const int cnt = tiles_in(k);
+    const int sl = k % kSlotRing;
     for (int j = 0; j < cnt; ++j) {
-      const PrefetchTarget pf = prefetch_target(T, tile0 + j + pd);
       // SpMV stages hold one tile at st0; packed elementwise stages hold cnt
       // headers, then each vector's cnt tiles (produce_elementwise)
-      const char* st = sub ? st0 + size_t(j) * kHdrBytes : st0;
-      const VecView V{sub ? st0 + size_t(cnt) * kHdrBytes + size_t(j) * kVecTileBytes : nullptr,
+      const char* st = ELEM ? st0 + size_t(j) * kHdrBytes : st0;
+      const VecView V{ELEM ? st0 + size_t(cnt) * kHdrBytes + size_t(j) * kVecTileBytes : nullptr,
                       size_t(cnt) * kVecTileBytes};
       const StageHdr& H = *reinterpret_cast<const StageHdr*>(st);
       const PartDev& P = part_of(T, H.part, INL);
-      double acc[NR];
-#pragma unroll
-      for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+      double acc[kRPT][NR];
       const long long c3 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      body(P, H, st, V, acc);
-      prefetch_tile<INL>(T, pf, spec_of);
-      const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      group_reduce<NR>(acc);
-      if (lane == 0) {
-        double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups + warp) * 2;
 #pragma unroll
-        for (int q = 0; q < NR; ++q) w[q] = acc[q];
+      for (int m = 0; m < kRPT; ++m) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) acc[m][q] = 0.0;
+        body(P, H, st, V, tt + m * kTPB, acc[m]);
+      }
+      const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+      double* ws = S.wsum + size_t(sl * kMaxPack + j) * kGroups * 2;
+#pragma unroll
+      for (int m = 0; m < kRPT; ++m) {
+        group_reduce<NR>(acc[m]);
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < NR; ++q) ws[(m * kTeamWarps + wt) * 2 + q] = acc[m][q];
       }
       if (kProf && T.prof_cta && threadIdx.x == 0) {
         const long long c5 = clock64();
@@ -676,49 +569,20 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(S.empty + ring.stage);   // group sums written before the release
-    ring.next(ns);
+    if (lane == 0) mbar_arrive(S.empty + rp.bar);   // group sums written before the release
   }
   const long long c1 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
   consumer_bar();
   if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 1] += clock64() - c1;
-  for (int s2 = (ss - ns + 1 > 0 ? ss - ns + 1 : 0); s2 < ss; ++s2) sum_stage_slot<NR>(T, S, s2);
-}
-
-// The consumer thread's row of a tile: lr = tid, i = row0 + lr.
-#define LRB_FOR_ROW(H, i, lr)                                   \
-  if (const int lr = int(threadIdx.x); lr < (H).rows)           \
-    if (const int64_t i = (H).row0 + lr; true)
-
-__device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
-  extern __shared__ __align__(128) char dsm[];
-  StreamSmem S;
-  S.stages = dsm;
-  char* tail = dsm + size_t(T.n_stages) * T.stage_bytes;
-  S.full = reinterpret_cast<uint64_t*>(tail);
-  S.empty = S.full + kStreamMaxStages;
-  S.wpart = reinterpret_cast<double*>(S.empty + kStreamMaxStages);
-  S.cnt = reinterpret_cast<unsigned long long*>(S.wpart + 2 * kGroups * kMaxRed);
-  S.stile = reinterpret_cast<int32_t*>(S.cnt + kCnt);
-  S.scnt = S.stile + kStreamMaxStages;
-  S.ssub = S.scnt + kStreamMaxStages;
-  S.wtile = S.ssub + kStreamMaxStages;
-  S.wcnt = S.wtile + kSlotRing;
-  S.ring = S.wcnt + kSlotRing;
-  S.wsum = reinterpret_cast<double*>(S.ring + 2);   // 8-byte aligned
-  return S;
-}
-__host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
-  return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * 8 + 2 * kGroups * kMaxRed * 8 +
-         kCnt * 8 + 3 * kStreamMaxStages * 4 + 2 * kSlotRing * 4 + 8 +
-         size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8;
+  for (int kd = (count - ns > 0 ? count - ns : 0); kd < count; ++kd)
+    sum_stage<NR>(T, S, kd, first_tile(kd), tiles_in(kd), (kd * kMaxPack) % kGroups, kGroups, warp);
 }
 
 __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& S) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < T.n_stages; ++s) {
-      mbar_init(S.full + s, 1);
-      mbar_init(S.empty + s, kGroups);
+    for (int b = 0; b < T.n_stages * kTeams; ++b) {
+      mbar_init(S.full + b, 1);
+      mbar_init(S.empty + b, kTeamWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -726,39 +590,35 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
   __syncthreads();
 }
 
-// Phase wrapper: producer warp streams, consumers compute, then the team
-// barrier with the fused reduction (all threads).
+// Phase wrapper: issuers stream, consumer teams compute, then the team
+// barrier with the fused reduction (all threads); gseq advances by the
+// phase's stage count (identical in every thread).
 template <int NR, bool INL, bool ELEM, class SpecF, class Body>
-__device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, Ring& ring,
-                                             double* red, int kind, int& seq, SpecF&& spec_of,
-                                             Body&& body) {
-  unsigned* ctr = T.tile_ctr + (seq & 1);   // phase seq grabs tiles here; reset at its barrier
+__device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, int& gseq, double* red,
+                                             int kind, SpecF&& spec_of, Body&& body) {
+  const int ntv = ELEM ? spec_of(part_of(T, T.part_begin, INL)).ntv : 0;
   if (threadIdx.x >= kConsumers) {
     fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
     if constexpr (ELEM)
-      produce_elementwise<INL>(T, S, ring, kind, ctr, spec_of);
+      produce_elementwise<INL>(T, S, gseq, kind, spec_of);
     else
-      produce_phase<INL>(T, S, ring, kind, ctr, spec_of);
+      produce_spmv<INL>(T, S, gseq, kind, spec_of);
   } else {
-    consume_phase<NR, INL>(T, S, ring, kind, spec_of, body);
-  }
-  if (threadIdx.x == 0) {   // the consumers' ring position is the truth for every thread
-    S.ring[0] = ring.stage;
-    S.ring[1] = int(ring.phase);
+    consume_phase<NR, INL, ELEM>(T, S, gseq, kind, ntv, body);
   }
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-  team_sync<NR, kRedLanes / kConsumers>(T, red, ctr);
+  team_sync<NR, kRedLanes / kConsumers>(T, red);
   if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
-  ring.stage = S.ring[0];
-  ring.phase = unsigned(S.ring[1]);
-  ++seq;
+  const int K = ELEM ? pack_factor(T, ntv) : 1;
+  gseq += stage_count(ELEM ? (T.n_tiles + K - 1) / K : T.n_tiles);
 }
 
 // Diagnostics: this CTA's counters to T.prof_cta[blockIdx.x * kCnt ...].
 __device__ __forceinline__ void stream_flush_counters(const TeamDev& T, const StreamSmem& S) {
   __syncthreads();
-  if (kProf && T.prof_cta && threadIdx.x < kCnt) T.prof_cta[blockIdx.x * kCnt + threadIdx.x] = (long long)S.cnt[threadIdx.x];
+  if (kProf && T.prof_cta && threadIdx.x < kCnt)
+    T.prof_cta[blockIdx.x * kCnt + threadIdx.x] = (long long)S.cnt[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -772,28 +632,25 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   const PartDev* __restrict__ parts = T.parts;
   const StreamSmem S = stream_smem(T);
   stream_init(T, S);
-  Ring ring;
-  int seq = 0;   // phase sequence number (tile counter parity)
+  int gseq = 0;
   double red[2];
   // ---- phase 0: x = 0, r = b, (z = dinv*b), b.b (, b.z)
   stream_phase<2, INL, true>(
-      T, S, ring, red, 0, seq,
+      T, S, gseq, red, 0,
       [&](const PartDev& P) {
         return Spec{0, JAC ? 2 : 1, {nullptr, nullptr}, {P.b, JAC ? P.dinv : nullptr}};
       },
-      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, double (&acc)[2]) {
-        const double* vb = V[0];
-        const double* vd = V[1];
-        LRB_FOR_ROW(H, i, lr) {
-          const double b = vb[lr];
-          P.x[i] = 0.0;
-          P.r[i] = b;
-          acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
-          if (JAC) {
-            const double z = __dmul_rn(vd[lr], b);
-            P.s[i] = z;
-            acc[1] = __dadd_rn(acc[1], __dmul_rn(b, z));
-          }
+      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
+        if (lr >= H.rows) return;
+        const int64_t i = H.row0 + lr;
+        const double b = V[0][lr];
+        P.x[i] = 0.0;
+        P.r[i] = b;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+        if (JAC) {
+          const double z = __dmul_rn(V[1][lr], b);
+          P.s[i] = z;
+          acc[1] = __dadd_rn(acc[1], __dmul_rn(b, z));
         }
       });
   const double bb = red[0];
@@ -823,20 +680,19 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       return __dadd_rn(z, __dmul_rn(beta, po));
     };
     stream_phase<1, INL, false>(
-        T, S, ring, red, 1, seq,
+        T, S, gseq, red, 1,
         [&](const PartDev& P) {
           const double* z = JAC ? P.s : P.r;
           const double* po = pa ? P.p1 : P.p0;
           return first ? Spec{1, 0, {z, nullptr}, {}} : Spec{2, 0, {z, po}, {}};
         },
-        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
+        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           if (H.tma) {
             const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
             const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
             const double* zw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
             const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
-            const int lr = int(threadIdx.x);
             const int sl = lr >> 5;
             const int2* slot = slice_slots(st, H, sl);
             const int n = int(P.n);
@@ -860,14 +716,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
             }
-          } else {
-            LRB_FOR_ROW(H, i, lr) {
-              const double pi = pnew_g(P, i);
-              const double qi = row_spmv(P, parts, i, pnew_g);
-              pout[i] = pi;
-              P.q[i] = qi;
-              acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
-            }
+          } else if (lr < H.rows) {
+            const int64_t i = H.row0 + lr;
+            const double pi = pnew_g(P, i);
+            const double qi = row_spmv(P, parts, i, pnew_g);
+            pout[i] = pi;
+            P.q[i] = qi;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
           }
         });
     if (team_failed(T)) break;
@@ -880,28 +735,23 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     pa ^= 1;
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
     stream_phase<2, INL, true>(
-        T, S, ring, red, 2, seq,
+        T, S, gseq, red, 2,
         [&](const PartDev& P) {
           return Spec{0, JAC ? 5 : 4, {nullptr, nullptr},
                       {pa ? P.p1 : P.p0, P.x, P.r, P.q, JAC ? P.dinv : nullptr}};
         },
-        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, double (&acc)[2]) {
-          const double* vp = V[0];
-          const double* vx = V[1];
-          const double* vr = V[2];
-          const double* vq = V[3];
-          const double* vd = V[4];
-          LRB_FOR_ROW(H, i, lr) {
-            const double x = __dadd_rn(vx[lr], __dmul_rn(step, vp[lr]));
-            const double r = __dsub_rn(vr[lr], __dmul_rn(step, vq[lr]));
-            P.x[i] = x;
-            P.r[i] = r;
-            acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
-            if (JAC) {
-              const double z = __dmul_rn(vd[lr], r);
-              P.s[i] = z;
-              acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
-            }
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
+          if (lr >= H.rows) return;
+          const int64_t i = H.row0 + lr;
+          const double x = __dadd_rn(V[1][lr], __dmul_rn(step, V[0][lr]));
+          const double r = __dsub_rn(V[2][lr], __dmul_rn(step, V[3][lr]));
+          P.x[i] = x;
+          P.r[i] = r;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+          if (JAC) {
+            const double z = __dmul_rn(V[4][lr], r);
+            P.s[i] = z;
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
           }
         });
     if (team_failed(T)) break;
@@ -913,14 +763,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       // ---- phase C: true residual |b - A x|
       auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
       stream_phase<1, INL, false>(
-          T, S, ring, red, 3, seq, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
-          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, double (&acc)[1]) {
+          T, S, gseq, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
+          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr,
+              double (&acc)[1]) {
             if (H.tma) {
               const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
               const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
               const double* xw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
               const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
-              const int lr = int(threadIdx.x);
               const int2* slot = slice_slots(st, H, lr >> 5);
               const int n = int(P.n);
               const double ax =
@@ -932,12 +782,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
                 const double d = __dsub_rn(vb[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
               }
-            } else {
-              LRB_FOR_ROW(H, i, lr) {
-                const double ax = row_spmv(P, parts, i, xg);
-                const double d = __dsub_rn(P.b[i], ax);
-                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
-              }
+            } else if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const double ax = row_spmv(P, parts, i, xg);
+              const double d = __dsub_rn(P.b[i], ax);
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
             }
           });
       if (team_failed(T)) break;

@@ -66,7 +66,10 @@ def _owner_parts(asm, pm):
 
 
 @pytest.mark.parametrize("dims,n_cpu,alpha", [((16, 16, 16), 2, 2), ((32, 32, 32), 4, 4),
-                                              ((48, 40, 36), 3, 3), ((24, 24, 24), 8, 2)])
+                                              ((48, 40, 36), 3, 3), ((24, 24, 24), 8, 2),
+                                              # many ring revolutions per CTA (every slot reused by
+                                              # both consumer teams): 1954 / 1458 tiles on 148 SMs
+                                              ((100, 100, 100), 4, 4), ((90, 90, 90), 6, 3)])
 def test_stream_bit_identical_cavity(dims, n_cpu, alpha):
     _, asm, pm = cavity_case(dims, n_cpu, alpha)
     holder = {}
