@@ -274,6 +274,7 @@ def run_ours(args):
         if r == 0:
             p = system.part.plan
             rec["plan"] = (p.n, p.nnz_local + p.nnz_nonlocal, p.n_halo, p.n_buf)
+            rec["kernel_info"] = system.team.kernel_info(method)
         return None
 
     lrb.run_world(n_cpu, program)
@@ -365,6 +366,7 @@ def run_ours_multi(args):
     # roofline on the max-loaded GPU: the largest part
     sizes = max_over_ranks(float(p0.n))
     rec["plan"] = (p0.n, p0.nnz_local + p0.nnz_nonlocal, p0.n_halo, p0.n_buf)
+    rec["kernel_info"] = owner.team.kernel_info(method)
     rec["e2e_update_wall_ms"] = [0.0]
     rec["e2e_solve_wall_ms"] = [0.0]
     rec["e2e_solve_kernel_ms"] = [0.0]
@@ -375,6 +377,15 @@ def run_ours_multi(args):
     dist.barrier()
     dist.destroy_process_group()
     return line if rank == 0 else None
+
+
+def kernel_name(info, method):
+    """The solve kernel that ran (lrb_team_kernel_info): streaming or classic."""
+    jac = "true" if method == "pcg" else "false"
+    if info and info.get("streaming"):
+        return (f"team_cg_stream_kernel<JAC={jac}> (persistent, bulk-copy ring: {info['stages']} x "
+                f"{info['stage_bytes']} B stages, {info['grid']} x {info['block']} threads)")
+    return f"team_cg_kernel<JAC={jac}> (persistent, classic per-thread gathers)"
 
 
 def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
@@ -398,7 +409,8 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
                          "L2-resident (latency-bound)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": "team_cg_kernel<JAC> (persistent, whole solve)",
+                     "kernel": kernel_name(rec.get("kernel_info"), method),
+                     "kernel_geometry": rec.get("kernel_info"),
                      "peak_kind": peak_kind,
                      "alg_bytes_per_launch": int(np.mean(alg)),
                      "kernel_ms": round(float(np.mean(rec["kernel_ms"])), 4)},
@@ -427,6 +439,10 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
                 line["roofline"]["traffic"] = int(t["dram_bytes_per_alg_byte"] *
                                                   line["roofline"]["alg_bytes_per_launch"])
                 line["roofline"]["traffic_note"] = t.get("note")
+                # the same kernel time against the bytes DRAM actually moved
+                dram_gbs = line["roofline"]["traffic"] / (line["roofline"]["kernel_ms"] * 1e-3) / 1e9
+                line["roofline"]["dram_achieved"] = round(dram_gbs, 1)
+                line["roofline"]["dram_frac"] = round(dram_gbs / line["roofline"]["peak"], 4)
         except Exception:  # noqa: BLE001
             pass
     return line
