@@ -299,25 +299,45 @@ __device__ void team_fail(const TeamDev& T, int code) {
 // every local part in fixed order, exchanges part values with the peer devices
 // (NVLink peer stores + release/acquire flags), sums all parts in ascending
 // GPU rank and releases everybody.  Returns the team-reduced values in red[].
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All blocks of this device arrive; the last one reduces the tile partials of
+// every local part in fixed order, exchanges part values with the peer devices
+// (NVLink peer stores + release/acquire flags), sums all parts in ascending
+// GPU rank and releases everybody.  Returns the team-reduced values in red[].
+// Single-device teams keep the part values in shared memory (no global round
+// trip); arrival and release are acq_rel / release atomics (cumulative over
+// the CTA's writes through the preceding __syncthreads).
+constexpr int kSmemParts = 16;
 template <int NR, int LPT>
 __device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = nullptr) {
   __shared__ unsigned s_last, s_gen;
   __shared__ double gs[kRedGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
+  __shared__ double pvals[kSmemParts][kMaxRed];
   __syncthreads();
   if (threadIdx.x == 0) {
-    s_gen = vload(T.bar_gen);
-    if (T.n_dev > 1)
-      __threadfence_system();
-    else
-      __threadfence();
-    const unsigned t = atomicAdd(T.bar_count, 1u);
+    s_gen = ld_acquire_gpu(T.bar_gen);
+    if (T.n_dev > 1) __threadfence_system();
+    const unsigned t = atom_add_acq_rel_gpu(T.bar_count, 1u);
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
+    const bool local = T.n_dev == 1 && T.n_parts <= kSmemParts;
     // Part values are double-buffered by epoch parity: a fast peer may already
     // publish epoch e+1 into our buffer while we still read epoch e (it only
     // needs our flag for e, which we raise before summing).  It cannot reach
@@ -330,9 +350,13 @@ __device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = n
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          T.part_red[pbuf + p * kMaxRed + j] = pv[j];
-          for (int d = 0; d < T.n_dev; ++d)
-            if (d != T.dev_rank) T.peer_part_red[d][pbuf + p * kMaxRed + j] = pv[j];
+          if (local) {
+            pvals[p][j] = pv[j];
+          } else {
+            T.part_red[pbuf + p * kMaxRed + j] = pv[j];
+            for (int d = 0; d < T.n_dev; ++d)
+              if (d != T.dev_rank) T.peer_part_red[d][pbuf + p * kMaxRed + j] = pv[j];
+          }
         }
       }
     }
@@ -358,31 +382,37 @@ __device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = n
       }
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        double s = vload(T.part_red + pbuf + j);
+        double s = local ? pvals[0][j] : vload(T.part_red + pbuf + j);
         for (int p = 1; p < T.n_parts; ++p)
-          s = __dadd_rn(s, vload(T.part_red + pbuf + p * kMaxRed + j));
+          s = __dadd_rn(s, local ? pvals[p][j] : vload(T.part_red + pbuf + p * kMaxRed + j));
         T.red[j] = s;
+        pv[j] = s;
       }
       if (T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
       if (reset_ctr) *reset_ctr = 0;   // every CTA is done grabbing tiles of this phase
       *T.bar_count = 0;
-      __threadfence();
-      atomicAdd(T.bar_gen, 1u);
+      red_add_release_gpu(T.bar_gen, 1u);
     }
-  } else if (threadIdx.x == 0) {
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NR; ++j) red[j] = pv[j];
+    return;
+  }
+  if (threadIdx.x == 0) {
     const long long t0 = global_ns();
-    while (vload(T.bar_gen) == s_gen) {
+    while (ld_acquire_gpu(T.bar_gen) == s_gen) {
       __nanosleep(32);
       if (global_ns() - t0 > T.timeout_ns) {
         team_fail(T, LRB_ETIMEOUT);
         break;
       }
     }
-    __threadfence();
+#pragma unroll
+    for (int j = 0; j < NR; ++j) pv[j] = vload(T.red + j);
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < NR; ++j) red[j] = vload(T.red + j);
+  for (int j = 0; j < NR; ++j) red[j] = pv[j];
 }
 
 // Tile partials.  Canonical tree (shared by the classic and the streaming
