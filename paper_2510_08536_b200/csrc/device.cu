@@ -568,6 +568,8 @@ struct TeamDevice {
   int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
   size_t smem[3] = {0, 0, 0};
   int block[3] = {kTPB, kTPB, kTPB};
+  int stage_bytes[3] = {0, 0, 0};   // streaming ring per method (BiCGStab stages three windows)
+  int n_stages[3] = {0, 0, 0};
   bool streaming[3] = {false, false, false};  // streaming (bulk-copy) kernel for this method
   cudaStream_t stream = nullptr;  // main stream of the first local part
   void* ws = nullptr;             // device workspace (cudaMalloc, create time)
@@ -598,6 +600,7 @@ static const void* solve_kernel(int method, bool inl);
 static const void* stream_kernel(int method, bool inl);
 static int stream_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t smem);
 static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, int* n_stages);
+static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int64_t dev_tile, StageHdr& h);
 static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, int stage_bytes,
                                 std::vector<StageHdr>& out, std::vector<StageTab>& tabs);
 static int solver_choice();
@@ -717,13 +720,41 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
     LRB_CUDA(cudaMemcpy(w + o_hdr, hdr.data(), sizeof(StageHdr) * hdr.size(), cudaMemcpyHostToDevice));
     LRB_CUDA(cudaMemcpy(w + o_rec, rec.data(), sizeof(TileRec) * rec.size(), cudaMemcpyHostToDevice));
   }
+  // BiCGStab's phase 1 stages three windows and the rhat tile: its own, larger
+  // ring over the same stageable tiles (classic kernel if two stages do not fit)
+  int bicg_bytes = 0, bicg_stages = 0;
+  if (use_stream) {
+    int dev_smem = 0;
+    cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, D.device);
+    const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - 1024;
+    int64_t best = 3 * (kHdrBytes + 5 * int64_t(kVecTileBytes));
+    StageHdr h;
+    for (int p : D.parts) {
+      const lrb_part* P = by_index[p];
+      for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
+        const int64_t need = tile_geometry(P, lt, p, 0, h);
+        if (need <= 0 || need > stage_bytes) continue;   // not staged (direct loads)
+        const int64_t base = kRecBytes + h.vbytes, wb = int64_t(h.wtot) * 8;
+        best = std::max(best, base + std::max({3 * wb + kVecTileBytes, 2 * wb, wb + kVecTileBytes}));
+      }
+    }
+    best = (best + 127) & ~int64_t(127);
+    const int64_t n = std::min<int64_t>(kStreamMaxStages, budget / best);
+    if (n >= std::max(kTeams, kIssuers)) {
+      bicg_bytes = int(best);
+      bicg_stages = int(n);
+    }
+  }
   for (int m = 0; m < 3; ++m) {
-    const void* sfn = use_stream ? stream_kernel(m, D.inl) : nullptr;
+    const bool bicg = m == LRB_METHOD_BICGSTAB;
+    const void* sfn = (use_stream && (!bicg || bicg_stages)) ? stream_kernel(m, D.inl) : nullptr;
     if (sfn) {
       D.fn[m] = sfn;
       D.block[m] = kStreamThreads;
       D.streaming[m] = true;
-      D.smem[m] = stream_smem_bytes(stage_bytes, n_stages);
+      D.stage_bytes[m] = bicg ? bicg_bytes : stage_bytes;
+      D.n_stages[m] = bicg ? bicg_stages : n_stages;
+      D.smem[m] = stream_smem_bytes(D.stage_bytes[m], D.n_stages[m]);
       D.grid[m] = stream_grid(sfn, D.device, D.n_tiles, n_share, D.smem[m]);
     } else {
       D.fn[m] = solve_kernel(m, D.inl);
@@ -818,6 +849,9 @@ static const void* stream_kernel(int method, bool inl) {
     case LRB_METHOD_PCG:
       return inl ? (const void*)team_cg_stream_kernel<true, true>
                  : (const void*)team_cg_stream_kernel<true, false>;
+    case LRB_METHOD_BICGSTAB:
+      return inl ? (const void*)team_bicgstab_stream_kernel<true>
+                 : (const void*)team_bicgstab_stream_kernel<false>;
     default:
       return nullptr;
   }
@@ -1262,8 +1296,8 @@ int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out) {
   out[0] = D.streaming[method] ? 1 : 0;
   out[1] = D.grid[method];
   out[2] = D.block[method];
-  out[3] = D.streaming[method] ? D.host.n_stages : 0;
-  out[4] = D.streaming[method] ? D.host.stage_bytes : 0;
+  out[3] = D.streaming[method] ? D.n_stages[method] : 0;
+  out[4] = D.streaming[method] ? D.stage_bytes[method] : 0;
   out[5] = int64_t(D.smem[method]);
   return LRB_OK;
 }
@@ -1462,6 +1496,8 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     TeamDev& H = D.host;
     H.tol = tol;
     H.max_iter = max_iter;
+    H.stage_bytes = D.stage_bytes[method];
+    H.n_stages = D.n_stages[method];
     H.hist = (hist && hist_cap > 0) ? D.hist_dev : nullptr;
     H.hist_cap = hist_cap;
   }

@@ -163,7 +163,7 @@ __device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool 
 struct Spec {
   int nwv;                 // window vectors (0: elementwise phase)
   int ntv;                 // tile vectors
-  const double* wv[2];
+  const double* wv[3];
   const double* tv[5];
 };
 
@@ -283,7 +283,7 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       bulk_g2s(d, P.val + cur.e0, unsigned(cur.vbytes), full, pol_stream);
       d += cur.vbytes;
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
+      for (int v = 0; v < 3; ++v)
 #pragma unroll
         for (int w = 0; w < kMaxWin; ++w)
           if (v < sp.nwv && w < cur.nw)
@@ -377,35 +377,52 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
 // ---------------------------------------------------------------------------
 // Consumers: staged row products
 // ---------------------------------------------------------------------------
-// Operand of a staged window position: NV = 1: w0[q]; NV = 2: the on-the-fly
-// p_new = w0[q] + beta * w1[q] (z and p_old windows, reference rounding).
-template <int NV>
-__device__ __forceinline__ double staged_operand(const double* __restrict__ w0,
-                                                 const double* __restrict__ w1, double beta, int q) {
-  if constexpr (NV == 1) {
-    return w0[q];
-  } else {
-    return __dadd_rn(w0[q], __dmul_rn(beta, w1[q]));
+// Staged operands.  Every SpMV phase reads its operand at staged window
+// position q through one of these (reference rounding, no FMA):
+//   Win1   x = w0[q]
+//   PnewCG p_new = z + beta * p_old            (w0 = z, w1 = p_old)
+//   SBiCG  s = r - alpha * v                   (w0 = r, w1 = v)
+//   PBiCG  p_new = r + beta * (p_old - omega * v_old)   (w0 = r, w1 = p_old, w2 = v_old)
+struct Win1 {
+  const double* __restrict__ w0;
+  __device__ __forceinline__ double operator()(int q) const { return w0[q]; }
+};
+struct PnewCG {
+  const double* __restrict__ w0;
+  const double* __restrict__ w1;
+  double beta;
+  __device__ __forceinline__ double operator()(int q) const { return __dadd_rn(w0[q], __dmul_rn(beta, w1[q])); }
+};
+struct SBiCG {
+  const double* __restrict__ w0;
+  const double* __restrict__ w1;
+  double alpha;
+  __device__ __forceinline__ double operator()(int q) const { return __dsub_rn(w0[q], __dmul_rn(alpha, w1[q])); }
+};
+struct PBiCG {
+  const double* __restrict__ w0;
+  const double* __restrict__ w1;
+  const double* __restrict__ w2;
+  double beta, omega;
+  __device__ __forceinline__ double operator()(int q) const {
+    return __dadd_rn(w0[q], __dmul_rn(beta, __dsub_rn(w1[q], __dmul_rn(omega, w2[q]))));
   }
-}
+};
 
 // Fixed-width row product: WM pattern slots, all operand loads issued
 // before the accumulation chain (slots k >= w and holes are masked to 0:
 // holes hold 0.0 in the SELL layout, so acc + 0 * 0 leaves acc unchanged —
 // acc is never -0.0).
-template <int NV, int WM>
-__device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
-                                            const int2* __restrict__ slot,
-                                            const double* __restrict__ sval,
-                                            const double* __restrict__ w0,
-                                            const double* __restrict__ w1, double beta) {
+template <int WM, class XS>
+__device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk, const int2* __restrict__ slot,
+                                            const double* __restrict__ sval, const XS& xs) {
   double a[WM], x[WM];
 #pragma unroll
   for (int k = 0; k < WM; ++k) {
     const bool on = k < w && ((msk >> k) & 1u);
     const int2 se = slot[k];
     a[k] = on ? sval[eb + k * kSlice] : 0.0;
-    x[k] = on ? staged_operand<NV>(w0, w1, beta, ii + se.y) : 0.0;
+    x[k] = on ? xs(ii + se.y) : 0.0;
   }
   double acc = 0.0;
 #pragma unroll
@@ -418,17 +435,20 @@ __device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
 __device__ __forceinline__ const int2* slice_slots(const char* st, const StageHdr& H, int sl) {
   return reinterpret_cast<const int2*>(st + kHdrBytes) + H.spat[sl] * 16;
 }
+// Staged index of row i's own operand (its diagonal slot).
+__device__ __forceinline__ int diag_pos(const StageHdr& H, const int2* slot, int sl, int64_t i) {
+  return int(i) + slot[H.sdiag[H.spat[sl]]].y;
+}
 
-// Staged SpMV of tile row lr (its 32-row slice is warp-uniform).
-template <int NV, bool HALO, class FH>
+// Staged SpMV of tile row lr (its 32-row slice is warp-uniform); xs(q) is
+// the staged operand, fh(owner part, row) a halo column's operand.
+template <bool HALO, class XS, class FH>
 __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ hpart,
                                                   const int32_t* __restrict__ hidx,
                                                   const PartDev* __restrict__ parts, const StageHdr& H,
                                                   const int2* __restrict__ slot,
                                                   const double* __restrict__ sval,
-                                                  const uint16_t* __restrict__ smask,
-                                                  const double* __restrict__ w0,
-                                                  const double* __restrict__ w1, double beta, int lr,
+                                                  const uint16_t* __restrict__ smask, int lr, const XS& xs,
                                                   FH&& fh) {
   const int lane = threadIdx.x & 31;
   const int rows = H.rows;
@@ -440,9 +460,9 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
   const int ii = int(H.row0) + lr;
   const unsigned msk = lr < rows ? unsigned(smask[lr]) : 0u;
   if constexpr (!HALO) {
-    if (w == 7) return row_fixed<NV, 7>(w, ii, eb, msk, slot, sval, w0, w1, beta);
-    if (w <= 8) return row_fixed<NV, 8>(w, ii, eb, msk, slot, sval, w0, w1, beta);
-    return row_fixed<NV, kPatW>(w, ii, eb, msk, slot, sval, w0, w1, beta);
+    if (w == 7) return row_fixed<7>(w, ii, eb, msk, slot, sval, xs);
+    if (w <= 8) return row_fixed<8>(w, ii, eb, msk, slot, sval, xs);
+    return row_fixed<kPatW>(w, ii, eb, msk, slot, sval, xs);
   } else {
     double acc = 0.0;
     for (int k = 0; k < w; ++k) {
@@ -454,13 +474,48 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
       if (on && c >= n) {
         xv = fh(parts[__ldg(hpart + (c - n))], int64_t(__ldg(hidx + (c - n))));
       } else {
-        xv = staged_operand<NV>(w0, w1, beta, on ? ii + se.y : 0);
+        xv = xs(on ? ii + se.y : 0);
         xv = on ? xv : 0.0;
       }
       acc = __dadd_rn(acc, __dmul_rn(a, xv));
     }
     return acc;
   }
+}
+
+// Staged pointers of an SpMV tile: values, masks, window vector v, tail vector.
+struct StagedTile {
+  const double* sval;
+  const uint16_t* smask;
+  const double* win;     // window vector 0; vector v at win + v * wtot
+  int wtot;
+  int nwv;
+  const char* st;
+  int vbytes;
+  __device__ __forceinline__ const double* w(int v) const { return win + size_t(v) * wtot; }
+  __device__ __forceinline__ const double* tail(int v) const {
+    return reinterpret_cast<const double*>(st + kRecBytes + vbytes + size_t(nwv) * wtot * 8) + size_t(v) * kTile;
+  }
+};
+__device__ __forceinline__ StagedTile staged_tile(const char* st, const StageHdr& H, int nwv) {
+  StagedTile t;
+  t.sval = reinterpret_cast<const double*>(st + kRecBytes);
+  t.smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
+  t.win = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
+  t.wtot = H.wtot;
+  t.nwv = nwv;
+  t.st = st;
+  t.vbytes = H.vbytes;
+  return t;
+}
+// Dispatch on whether the part has halo columns.
+template <class XS, class FH>
+__device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
+                                             const StageHdr& H, const StagedTile& t, const int2* slot, int lr,
+                                             const XS& xs, FH&& fh) {
+  const int n = int(P.n);
+  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh)
+                  : row_spmv_staged<false>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh);
 }
 
 // Vectors of one packed elementwise tile: vector v at base + v * stride.
@@ -689,29 +744,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           if (H.tma) {
-            const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
-            const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
-            const double* zw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
-            const double* pw = zw + H.wtot;   // p_old windows (not staged in the first iteration)
+            const StagedTile t = staged_tile(st, H, first ? 1 : 2);
             const int sl = lr >> 5;
             const int2* slot = slice_slots(st, H, sl);
-            const int n = int(P.n);
-            double qi;
-            if (first) {
-              qi = P.n_halo ? row_spmv_staged<1, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw, pw,
-                                                      beta, lr, pnew_g)
-                            : row_spmv_staged<1, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw,
-                                                       pw, beta, lr, pnew_g);
-            } else {
-              qi = P.n_halo ? row_spmv_staged<2, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw, pw,
-                                                      beta, lr, pnew_g)
-                            : row_spmv_staged<2, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, zw,
-                                                       pw, beta, lr, pnew_g);
-            }
+            const PnewCG pn{t.w(0), t.w(1), beta};
+            const Win1 z1{t.w(0)};
+            const double qi = first ? staged_row(P, parts, H, t, slot, lr, z1, pnew_g)
+                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const int qd = int(i) + slot[H.sdiag[H.spat[sl]]].y;   // the diagonal's operand
-              const double pi = first ? zw[qd] : staged_operand<2>(zw, pw, beta, qd);
+              const int qd = diag_pos(H, slot, sl, i);   // the diagonal's operand
+              const double pi = first ? z1(qd) : pn(qd);
               pout[i] = pi;
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
@@ -767,19 +810,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr,
               double (&acc)[1]) {
             if (H.tma) {
-              const double* sval = reinterpret_cast<const double*>(st + kRecBytes);
-              const uint16_t* smask = reinterpret_cast<const uint16_t*>(st + kHdrBytes + kTabBytes);
-              const double* xw = reinterpret_cast<const double*>(st + kRecBytes + H.vbytes);
-              const double* vb = reinterpret_cast<const double*>(st + stage_tail_offset(H, 1));
+              const StagedTile t = staged_tile(st, H, 1);
               const int2* slot = slice_slots(st, H, lr >> 5);
-              const int n = int(P.n);
-              const double ax =
-                  P.n_halo ? row_spmv_staged<1, true>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, xw, xw,
-                                                     0.0, lr, xg)
-                           : row_spmv_staged<1, false>(n, P.hpart, P.hidx, parts, H, slot, sval, smask, xw,
-                                                      xw, 0.0, lr, xg);
+              const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
-                const double d = __dsub_rn(vb[lr], ax);
+                const double d = __dsub_rn(t.tail(0)[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
               }
             } else if (lr < H.rows) {
@@ -806,6 +841,204 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   if (lead) {
     out->iterations = it > T.max_iter ? T.max_iter : it;
     out->converged = converged ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BiCGStab, streaming (momentum; phases and arithmetic of team_bicgstab_kernel,
+// kernels.cuh).  1: p_new = r + beta (p_old - omega v_old) on the fly (three
+// staged windows), v = A p_new, rhat.v;  2: s = r - alpha v on the fly, t =
+// A s, t.s, t.t;  3: x = (x + alpha p) + omega s, r = s - omega t, r.r,
+// rhat.r;  check: |b - A x|^2.  p and v are double-buffered.
+// ---------------------------------------------------------------------------
+template <bool INL>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    team_bicgstab_stream_kernel(const __grid_constant__ TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  const StreamSmem S = stream_smem(T);
+  stream_init(T, S);
+  int gseq = 0;
+  double red[2];
+  stream_phase<1, INL, true>(
+      T, S, gseq, red, 0, [&](const PartDev& P) { return Spec{0, 1, {nullptr, nullptr}, {P.b}}; },
+      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[1]) {
+        if (lr >= H.rows) return;
+        const int64_t i = H.row0 + lr;
+        const double b = V[0][lr];
+        P.x[i] = 0.0;
+        P.r[i] = b;
+        P.rhat[i] = b;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+      });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  double rho = bb, rho_prev = 1.0, alpha = 1.0, omega = 1.0, beta = 0.0, res = 1.0;
+  int pa = 0;   // p_old/v_old in p0/v0 when pa == 0
+  bool converged = false, breakdown = false;
+  int it = 0;
+  for (it = 1; it <= T.max_iter; ++it) {
+    const bool first = (it == 1);
+    if (!first) beta = __dmul_rn(rho / rho_prev, alpha / omega);
+    // ---- phase 1: p_new, v = A p_new, rhat.v
+    auto pnew_g = [&](const PartDev& Q, int64_t j) -> double {
+      const double r = Q.r[j];
+      if (first) return r;
+      const double po = pa ? Q.p1[j] : Q.p0[j];
+      const double vo = pa ? Q.v1[j] : Q.v0[j];
+      return __dadd_rn(r, __dmul_rn(beta, __dsub_rn(po, __dmul_rn(omega, vo))));
+    };
+    stream_phase<1, INL, false>(
+        T, S, gseq, red, 1,
+        [&](const PartDev& P) {
+          return first ? Spec{1, 1, {P.r, nullptr, nullptr}, {P.rhat}}
+                       : Spec{3, 1, {P.r, pa ? P.p1 : P.p0, pa ? P.v1 : P.v0}, {P.rhat}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
+          double* pout = pa ? P.p0 : P.p1;
+          double* vout = pa ? P.v0 : P.v1;
+          if (H.tma) {
+            const StagedTile t = staged_tile(st, H, first ? 1 : 3);
+            const int sl = lr >> 5;
+            const int2* slot = slice_slots(st, H, sl);
+            const Win1 r1{t.w(0)};
+            const PBiCG pn{t.w(0), t.w(1), t.w(2), beta, omega};
+            const double vi = first ? staged_row(P, parts, H, t, slot, lr, r1, pnew_g)
+                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g);
+            if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const int qd = diag_pos(H, slot, sl, i);
+              const double pi = first ? r1(qd) : pn(qd);
+              pout[i] = pi;
+              vout[i] = vi;
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(t.tail(0)[lr], vi));
+            }
+          } else if (lr < H.rows) {
+            const int64_t i = H.row0 + lr;
+            const double pi = pnew_g(P, i);
+            const double vi = row_spmv(P, parts, i, pnew_g);
+            pout[i] = pi;
+            vout[i] = vi;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(P.rhat[i], vi));
+          }
+        });
+    if (team_failed(T)) break;
+    pa ^= 1;
+    const double rv = red[0];
+    if (rv == 0.0) {
+      breakdown = true;
+      break;
+    }
+    alpha = rho / rv;
+    // ---- phase 2: s = r - alpha v, t = A s, t.s, t.t
+    auto sval_g = [&](const PartDev& Q, int64_t j) -> double {
+      const double v = pa ? Q.v1[j] : Q.v0[j];
+      return __dsub_rn(Q.r[j], __dmul_rn(alpha, v));
+    };
+    stream_phase<2, INL, false>(
+        T, S, gseq, red, 1, [&](const PartDev& P) { return Spec{2, 0, {P.r, pa ? P.v1 : P.v0}, {}}; },
+        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[2]) {
+          if (H.tma) {
+            const StagedTile t = staged_tile(st, H, 2);
+            const int sl = lr >> 5;
+            const int2* slot = slice_slots(st, H, sl);
+            const SBiCG sv{t.w(0), t.w(1), alpha};
+            const double ti = staged_row(P, parts, H, t, slot, lr, sv, sval_g);
+            if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const double si = sv(diag_pos(H, slot, sl, i));
+              P.s[i] = si;
+              P.t[i] = ti;
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(ti, si));
+              acc[1] = __dadd_rn(acc[1], __dmul_rn(ti, ti));
+            }
+          } else if (lr < H.rows) {
+            const int64_t i = H.row0 + lr;
+            const double si = sval_g(P, i);
+            const double ti = row_spmv(P, parts, i, sval_g);
+            P.s[i] = si;
+            P.t[i] = ti;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(ti, si));
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(ti, ti));
+          }
+        });
+    if (team_failed(T)) break;
+    omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
+    // ---- phase 3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r
+    stream_phase<2, INL, true>(
+        T, S, gseq, red, 2,
+        [&](const PartDev& P) {
+          return Spec{0, 5, {nullptr, nullptr}, {pa ? P.p1 : P.p0, P.s, P.x, P.t, P.rhat}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
+          if (lr >= H.rows) return;
+          const int64_t i = H.row0 + lr;
+          const double s = V[1][lr];
+          const double x = __dadd_rn(__dadd_rn(V[2][lr], __dmul_rn(alpha, V[0][lr])), __dmul_rn(omega, s));
+          const double r = __dsub_rn(s, __dmul_rn(omega, V[3][lr]));
+          P.x[i] = x;
+          P.r[i] = r;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+          acc[1] = __dadd_rn(acc[1], __dmul_rn(V[4][lr], r));
+        });
+    if (team_failed(T)) break;
+    const double rr = red[0];
+    rho_prev = rho;
+    rho = red[1];
+    const double rec = sqrt(rr) / bnorm;
+    if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
+    if (rec <= T.tol || it % 10 == 0) {
+      auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
+      stream_phase<1, INL, false>(
+          T, S, gseq, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
+          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr,
+              double (&acc)[1]) {
+            if (H.tma) {
+              const StagedTile t = staged_tile(st, H, 1);
+              const int2* slot = slice_slots(st, H, lr >> 5);
+              const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+              if (lr < H.rows) {
+                const double d = __dsub_rn(t.tail(0)[lr], ax);
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+              }
+            } else if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const double ax = row_spmv(P, parts, i, xg);
+              const double d = __dsub_rn(P.b[i], ax);
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+            }
+          });
+      if (team_failed(T)) break;
+      res = sqrt(red[0]) / bnorm;
+      if (res <= T.tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      res = rec;
+    }
+    if (omega == 0.0 || rho == 0.0) {
+      breakdown = true;
+      break;
+    }
+  }
+  stream_flush_counters(T, S);
+  if (lead) {
+    out->iterations = it > T.max_iter ? T.max_iter : it;
+    out->converged = converged ? 1 : 0;
+    out->breakdown = breakdown ? 1 : 0;
     out->residual = res;
     out->bnorm = bnorm;
   }

@@ -138,3 +138,36 @@ def test_stream_solver_is_default_and_reports_geometry():
     assert info["streaming"] == 1 and info["block"] > 512
     assert info["grid"] >= 1 and info["stage_bytes"] % 128 == 0
     assert info["smem"] >= info["stages"] * info["stage_bytes"]
+
+
+def _momentum(asm, seed=0):
+    """Non-symmetric, diagonally dominant LDU on the cavity addressing."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for m, ifs in asm:
+        eps_u = 0.05 * rng.random(m.n_faces)
+        eps_l = 0.05 * rng.random(m.n_faces)
+        mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, np.full(m.n_cells, 6.5),
+                           -1.0 - eps_l, -1.0 + eps_u)
+        out.append((mm, [lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote,
+                                            b.values * (1.0 + 0.01 * b.neighbor_rank)) for b in ifs]))
+    return out
+
+
+@pytest.mark.parametrize("dims,n_cpu,alpha,dev_ranks", [((24, 24, 24), 4, 2, None),
+                                                        ((20, 20, 20), 4, 1, [0, 0, 1, 1]),
+                                                        ((100, 100, 100), 4, 4, None)])
+def test_stream_bicgstab_bit_identical(dims, n_cpu, alpha, dev_ranks):
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    mom = _momentum(asm)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*mom[ctx.rank], pm, ctx)
+        parts = s.comm.allgather(s.part) if s.is_owner else None
+        if s.is_owner and s.comm.group_rank == 0:
+            holder["r"] = _compare(parts, ("bicgstab",), 1e-10, 300, dev_ranks=dev_ranks, rhs_seed=3)
+        return None
+
+    lrb.run_world(n_cpu, program)
+    assert holder["r"]["bicgstab"].converged
