@@ -292,7 +292,7 @@ def run_ours(args):
 
     lrb.run_world(n_cpu, program)
     log(f"[bench] ours done ({time.monotonic() - t0:.1f}s)")
-    return finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha), N,
+    return finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha, N=N, cells=f"{N ** 3 / 1e6:.3g}M"), N,
                        n_cpu, alpha, sampler)
 
 
@@ -383,7 +383,7 @@ def run_ours_multi(args):
     rec["e2e_update_wall_ms"] = [0.0]
     rec["e2e_solve_wall_ms"] = [0.0]
     rec["e2e_solve_kernel_ms"] = [0.0]
-    line = finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha), N,
+    line = finish_line(args, rec, method, desc.format(n_cpu=n_cpu, n_gpu=n_gpu, alpha=alpha, N=N, cells=f"{N ** 3 / 1e6:.3g}M"), N,
                        n_cpu, alpha, sampler)
     line["config"]["max_part_rows"] = int(sizes)
     line["config"]["parallelism"] = f"{n_gpu} GPU parts, NVLink peer-memory halo + reductions"
@@ -717,7 +717,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": base["value"],
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": desc.format(n_cpu=n_cpu, n_gpu=args.gpus, alpha=args.rpg),
+        "config": {"workload": desc.format(n_cpu=n_cpu, n_gpu=args.gpus, alpha=args.rpg, N=N,
+                                           cells=f"{N ** 3 / 1e6:.3g}M"),
                    "n_cells": N ** 3, "n_cpu": n_cpu, "alpha": args.rpg, "method": method_default,
                    "tol": TOL},
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
