@@ -912,7 +912,12 @@ static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, in
   // grow the stage to pack 3 elementwise tiles when that keeps the ring depth
   const int64_t packed = (3 * (kHdrBytes + 5 * int64_t(kVecTileBytes)) + 127) & ~int64_t(127);
   if (packed > best && std::min<int64_t>(kStreamMaxStages, budget / packed) >= n) best = packed;
-  *n_stages = int(std::min<int64_t>(kStreamMaxStages, budget / best));
+  int64_t stages = std::min<int64_t>(kStreamMaxStages, budget / best);
+  if (const char* e = getenv("LRB_STREAM_STAGES")) {   // experiments: cap the ring depth
+    const int64_t cap_n = atoi(e);
+    if (cap_n >= 2) stages = std::min(stages, cap_n);
+  }
+  *n_stages = int(stages);
   return int(best);
 }
 

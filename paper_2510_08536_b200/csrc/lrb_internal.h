@@ -87,7 +87,7 @@ constexpr int kMaxRed = 4;   // reductions fused into one barrier
 // creation and bulk-copied into the shared-memory stage with the tile's data.
 constexpr int kHdrBytes = 256;
 constexpr int kHdrPats = 4;    // distinct slice patterns a staged tile may hold
-struct alignas(16) StageHdr {
+struct StageHdrFields {
   int64_t row0;          // first row of the tile (part-local)
   int64_t e0;            // first SELL entry of the tile
   int64_t wa[kMaxWin];   // aligned start of each operand window (part-local row)
@@ -105,7 +105,10 @@ struct alignas(16) StageHdr {
   int32_t pat[kTile / kSlice];      // slice pattern ids (dictionary)
   int8_t spat[kTile / kSlice];      // slice -> slot table of the tile's StageTab
   int8_t sdiag[kHdrPats];           // slot of the diagonal (offset 0) per table
-  int32_t reserved_[(kHdrBytes - 248) / 4];
+};
+static_assert(sizeof(StageHdrFields) <= kHdrBytes, "stage header fields exceed kHdrBytes");
+struct alignas(16) StageHdr : StageHdrFields {
+  char reserved_[kHdrBytes - sizeof(StageHdrFields)];
 };
 static_assert(sizeof(StageHdr) == kHdrBytes, "stage header must be exactly kHdrBytes");
 

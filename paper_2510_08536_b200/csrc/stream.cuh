@@ -40,12 +40,12 @@
 
 namespace lrb {
 
-constexpr int kConsumers = kTile;                 // 16 consumer warps in two teams
-constexpr int kTeams = 2;
-constexpr int kTeamThreads = kConsumers / kTeams;
+constexpr int kTeams = 2;                         // 16 consumer warps in two teams
+constexpr int kTeamThreads = kTPB;
+constexpr int kConsumers = kTeams * kTeamThreads;
 constexpr int kTeamWarps = kTeamThreads / 32;
-static_assert(kTeamThreads == kTPB && kTile == kTPB * kRPT && kRPT == 2,
-              "a team thread computes rows t and t + kTPB, like the classic kernels");
+static_assert(kTile == kTPB * kRPT,
+              "a team thread computes rows t + m * kTPB (m < kRPT), like the classic kernels");
 // issuer p fills exactly the stages team p consumes (G % kTeams == p)
 #ifndef LRB_ISSUERS
 #define LRB_ISSUERS 2
@@ -54,7 +54,10 @@ constexpr int kIssuers = LRB_ISSUERS;             // producer warps (alternate s
 static_assert(kIssuers == 1 || kIssuers == kTeams, "one issuer, or one per consumer team");
 constexpr int kStreamThreads = kConsumers + 32 * kIssuers;
 constexpr int kVecTileBytes = kTile * 8;          // one vector's rows of a tile
-constexpr int kStreamMaxStages = 4;
+#ifndef LRB_MAX_STAGES
+#define LRB_MAX_STAGES (kTile <= 256 ? 6 : 4)
+#endif
+constexpr int kStreamMaxStages = LRB_MAX_STAGES;
 constexpr int kMaxPack = 4;                       // tiles per stage in elementwise phases
 constexpr int kSlotRing = 2 * kStreamMaxStages;   // group-sum slots (see consume_phase)
 constexpr int kConsumerBar = 1;                   // named barrier of the consumer warps
@@ -102,6 +105,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a global range by the bulk-copy engine (no shared memory,
+// no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+#ifndef LRB_ISSUER_PREFETCH
+#define LRB_ISSUER_PREFETCH 1
+#endif
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -259,6 +270,18 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
   for (int k = k0; k < count; k += kIssuers) {
     const int64_t tile = blockIdx.x + k * G;
     if (k + kIssuers < count) load_hdr_addr(hdrs + tile + kIssuers * G, nxt);
+    if (LRB_ISSUER_PREFETCH && k + kIssuers < count && nxt.tma) {
+      // this issuer's next tile: bring its values and operand windows toward
+      // L2 while it waits for a free slot (its copies then hit L2)
+      const PartDev& Pn = part_of(T, nxt.part, INL);
+      const Spec spn = spec_of(Pn);
+      bulk_prefetch_l2(Pn.val + nxt.e0, unsigned(nxt.vbytes));
+#pragma unroll
+      for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int w = 0; w < kMaxWin; ++w)
+          if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
+    }
     const RingPos rp = ring_pos(gseq + k, T.n_stages);
     char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
     uint64_t* full = S.full + rp.bar;
