@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ p
 // (v = tid + q * kRedLanes / LPT): the classic kernels (256 threads) LPT = 2,
 // the streaming kernels (512 consumer threads) LPT = 1.  Loads are issued in
 // batches so a lane's chain costs ceil(tiles / kRedLanes / batch) L2 trips.
-constexpr int kRedLanes = 512;
+constexpr int kRedLanes = 2 * kTPB;   // = the streaming consumers (two teams)
 constexpr int kRedGroups = kRedLanes / 32;
 
 template <int NR, int LPT>

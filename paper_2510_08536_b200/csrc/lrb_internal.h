@@ -75,7 +75,10 @@ struct PartDev {
 // Work decomposition of the persistent kernels: a tile is kTPB*kRPT rows of
 // one part.  The per-tile partial dot products are reduced in fixed order,
 // so results do not depend on grid size or scheduling.
-constexpr int kTPB = 256;
+#ifndef LRB_TPB
+#define LRB_TPB 256
+#endif
+constexpr int kTPB = LRB_TPB;   // threads per classic block = rows per streaming team pass
 #ifndef LRB_RPT
 #define LRB_RPT 2
 #endif
