@@ -184,7 +184,6 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   D.pat_off = reinterpret_cast<const int32_t*>(base + L.pat_off);
   D.rmask = reinterpret_cast<const uint16_t*>(base + L.rmask);
   D.tile_win = reinterpret_cast<const int32_t*>(base + L.tile_win);
-  D.max_stage = P.max_stage;
   D.col = reinterpret_cast<const int32_t*>(base + L.col);
   D.src = reinterpret_cast<const int32_t*>(base + L.src);
   D.dpos = reinterpret_cast<const int8_t*>(base + L.dpos);
@@ -640,7 +639,6 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_peer_flags = take(sizeof(void*) * n_dev);
   const size_t o_peer_red = take(sizeof(void*) * n_dev);
   const size_t o_out = take(sizeof(SolveOut));
-  const size_t o_ctr = take(sizeof(unsigned) * 2);
   // streaming solvers: stage size from the largest stageable tile, and the
   // per-tile stage headers
   const bool want_stream = solver_choice() != 1;
@@ -675,7 +673,6 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
   H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
   H.out = D.out_dev;
-  H.tile_ctr = reinterpret_cast<unsigned*>(w + o_ctr);
   {
     const char* env = getenv("LRB_BARRIER_TIMEOUT_S");
     const double s = env ? atof(env) : 20.0;
@@ -1497,7 +1494,6 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
       }
     LRB_CUDA(cudaMemsetAsync(D.out_dev, 0, sizeof(SolveOut), D.stream));
     if (D.prof_dev) LRB_CUDA(cudaMemsetAsync(D.prof_dev, 0, sizeof(long long), D.stream));
-    LRB_CUDA(cudaMemsetAsync(D.host.tile_ctr, 0, sizeof(unsigned) * 2, D.stream));
     TeamDev& H = D.host;
     H.tol = tol;
     H.max_iter = max_iter;

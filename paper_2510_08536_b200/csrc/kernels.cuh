@@ -322,7 +322,7 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // the CTA's writes through the preceding __syncthreads).
 constexpr int kSmemParts = 16;
 template <int NR, int LPT>
-__device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = nullptr) {
+__device__ void team_sync(const TeamDev& T, double* red) {
   __shared__ unsigned s_last, s_gen;
   __shared__ double gs[kRedGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
@@ -389,7 +389,6 @@ __device__ void team_sync(const TeamDev& T, double* red, unsigned* reset_ctr = n
         pv[j] = s;
       }
       if (T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
-      if (reset_ctr) *reset_ctr = 0;   // every CTA is done grabbing tiles of this phase
       *T.bar_count = 0;
       red_add_release_gpu(T.bar_gen, 1u);
     }

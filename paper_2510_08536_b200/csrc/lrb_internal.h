@@ -56,7 +56,6 @@ struct PartDev {
   const int32_t* pat_off;     // [n_pat * kPatW]
   const uint16_t* rmask;      // [n] occupied pattern slots of each row
   const int32_t* tile_win;    // [ntiles_part * kWinStride] staging windows
-  int64_t max_stage;          // max staged doubles over this part's tiles
   const int32_t* col;         // [E]
   const int32_t* src;         // [E] scatter inverse (buffer position or -1)
   const int8_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
@@ -182,7 +181,6 @@ struct TeamDev {
   int32_t max_iter;
   const void* tile_hdr;     // streaming solvers: StageHdr per device tile
   const void* tile_rec;     // streaming solvers: TileRec per device tile (header | tables | masks)
-  unsigned int* tile_ctr;   // streaming solvers: [2] dynamic tile counters (phase parity)
   long long* prof;          // phase-release timestamps (nullable, diagnostics)
   long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)
   int32_t* prof_n;

@@ -178,9 +178,6 @@ struct Spec {
   const double* tv[5];
 };
 
-__device__ __forceinline__ int stage_tail_offset(const StageHdr& H, int nwv) {
-  return nwv ? kRecBytes + H.vbytes + nwv * H.wtot * 8 : kHdrBytes;
-}
 
 // Static stage sequence of a phase for this CTA: stage k holds unit
 // cta + k * grid (a tile in SpMV phases, a chunk of K tiles in elementwise
