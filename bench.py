@@ -112,9 +112,14 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 def solve_bytes(n, nnz, h, iterations, checks, method):
     """Algorithmic HBM bytes of one solve: CG it 12nnz+4(n+1)+88n+8h, PCG +16n,
-    true-residual check 12nnz+4(n+1)+16n+8h, init (b read, x r written) 24n."""
-    it = 12 * nnz + 4 * (n + 1) + 88 * n + 8 * h + (16 * n if method == "pcg" else 0)
+    true-residual check 12nnz+4(n+1)+16n+8h, init (b read, x r written) 24n.
+    pcg1 (single reduction): it 12nnz+4(n+1)+8h + 88n (r, dinv, w, s_old and
+    p, x read; p, x, r, s, w written), init + one SpMV 12nnz+4(n+1)+24n+8h."""
     chk = 12 * nnz + 4 * (n + 1) + 16 * n + 8 * h
+    if method == "pcg1":
+        it = 12 * nnz + 4 * (n + 1) + 88 * n + 8 * h
+        return iterations * it + checks * chk + 24 * n + 12 * nnz + 4 * (n + 1) + 24 * n + 8 * h
+    it = 12 * nnz + 4 * (n + 1) + 88 * n + 8 * h + (16 * n if method == "pcg" else 0)
     return iterations * it + checks * chk + 24 * n
 
 
@@ -394,7 +399,10 @@ def run_ours_multi(args):
 
 def kernel_name(info, method):
     """The solve kernel that ran (lrb_team_kernel_info): streaming or classic."""
-    jac = "true" if method == "pcg" else "false"
+    jac = "true" if method in ("pcg", "pcg1") else "false"
+    if info and info.get("streaming") and method == "pcg1":
+        return (f"team_pcg1_stream_kernel (single-reduction Jacobi-PCG, bulk-copy ring: {info['stages']} x "
+                f"{info['stage_bytes']} B stages, {info['grid']} x {info['block']} threads)")
     if info and info.get("streaming"):
         return (f"team_cg_stream_kernel<JAC={jac}> (persistent, bulk-copy ring: {info['stages']} x "
                 f"{info['stage_bytes']} B stages, {info['grid']} x {info['block']} threads)")
@@ -737,7 +745,7 @@ def main():
     ap.add_argument("--rpg", type=int, default=None, help="CPU ranks per GPU (alpha)")
     ap.add_argument("--n", type=int, default=None, help="cavity edge (c4; default 300)")
     ap.add_argument("--mode", choices=("direct", "staged"), default="direct")
-    ap.add_argument("--method", choices=("cg", "pcg"), default=None)
+    ap.add_argument("--method", choices=("cg", "pcg", "pcg1"), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=60.0)
     args = ap.parse_args()

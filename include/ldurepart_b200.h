@@ -34,6 +34,8 @@ extern "C" {
 #define LRB_METHOD_CG 0        /* solver.py:100-147 (unpreconditioned CG) */
 #define LRB_METHOD_PCG 1       /* Jacobi-PCG */
 #define LRB_METHOD_BICGSTAB 2  /* BiCGStab */
+#define LRB_METHOD_PCG1 3      /* single-reduction (Chronopoulos-Gear) Jacobi-PCG, SURVEY.md §8 f1:
+                                  one team barrier per iteration; CG's iterates up to rounding */
 
 const char* lrb_last_error(void);
 const char* lrb_version(void);

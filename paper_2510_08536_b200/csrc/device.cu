@@ -555,6 +555,25 @@ int lrb_part_elapsed_ms(lrb_part* part, float* ms) {
 // ---------------------------------------------------------------------------
 namespace lrb {
 
+constexpr int kMethods = 4;
+// the streaming kernels' static shared memory (team_sync scratch, ~3.2 KB)
+// shares the opt-in per-block limit with the dynamic ring
+constexpr int64_t kStaticSmemMargin = 4096;
+
+// Largest shared-memory need of any SpMV phase of a method for a staged tile
+// with `base` bytes of record + values and `wb` bytes per window vector.
+static int64_t method_need(int method, int64_t base, int64_t wb) {
+  const int64_t tv = kVecTileBytes;
+  switch (method) {
+    case LRB_METHOD_BICGSTAB:   // phase 1: r, p_old, v_old windows + rhat tile
+      return base + std::max({3 * wb + tv, 2 * wb, wb + tv});
+    case LRB_METHOD_PCG1:       // fused phase: r, dinv, w, s_old windows + p, x tiles
+      return base + std::max({4 * wb + 2 * tv, 2 * wb, wb + tv});
+    default:                    // CG / PCG: z, p_old windows; check: x window + b tile
+      return base + std::max(2 * wb, wb + tv);
+  }
+}
+
 struct TeamDevice {
   int device = 0;       // CUDA device
   int rank = 0;         // device rank in the team
@@ -563,13 +582,13 @@ struct TeamDevice {
   bool inl = false;               // local part descriptors in the kernel parameter
   bool cooperative = true;        // whole device to one team kernel
   size_t ws_bytes = 0;
-  const void* fn[3] = {nullptr, nullptr, nullptr};
-  int grid[3] = {0, 0, 0};        // per method (CG, PCG, BiCGStab)
-  size_t smem[3] = {0, 0, 0};
-  int block[3] = {kTPB, kTPB, kTPB};
-  int stage_bytes[3] = {0, 0, 0};   // streaming ring per method (BiCGStab stages three windows)
-  int n_stages[3] = {0, 0, 0};
-  bool streaming[3] = {false, false, false};  // streaming (bulk-copy) kernel for this method
+  const void* fn[kMethods] = {};
+  int grid[kMethods] = {};          // per method (CG, PCG, BiCGStab, PCG1)
+  size_t smem[kMethods] = {};
+  int block[kMethods] = {kTPB, kTPB, kTPB, kTPB};
+  int stage_bytes[kMethods] = {};   // streaming ring per method (BiCGStab / PCG1 stage more windows)
+  int n_stages[kMethods] = {};
+  bool streaming[kMethods] = {};    // streaming (bulk-copy) kernel for this method
   cudaStream_t stream = nullptr;  // main stream of the first local part
   void* ws = nullptr;             // device workspace (cudaMalloc, create time)
   TeamDev host{};                 // kernel argument
@@ -717,48 +736,54 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
     LRB_CUDA(cudaMemcpy(w + o_hdr, hdr.data(), sizeof(StageHdr) * hdr.size(), cudaMemcpyHostToDevice));
     LRB_CUDA(cudaMemcpy(w + o_rec, rec.data(), sizeof(TileRec) * rec.size(), cudaMemcpyHostToDevice));
   }
-  // BiCGStab's phase 1 stages three windows and the rhat tile: its own, larger
-  // ring over the same stageable tiles (classic kernel if two stages do not fit)
-  int bicg_bytes = 0, bicg_stages = 0;
+  // BiCGStab and PCG1 stage more windows than CG: their own, larger rings over
+  // the same stageable tiles (no streaming kernel if two stages do not fit)
+  int m_bytes[kMethods] = {}, m_stages[kMethods] = {};
   if (use_stream) {
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, D.device);
-    const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - 1024;
-    int64_t best = 3 * (kHdrBytes + 5 * int64_t(kVecTileBytes));
-    StageHdr h;
-    for (int p : D.parts) {
-      const lrb_part* P = by_index[p];
-      for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
-        const int64_t need = tile_geometry(P, lt, p, 0, h);
-        if (need <= 0 || need > stage_bytes) continue;   // not staged (direct loads)
-        const int64_t base = kRecBytes + h.vbytes, wb = int64_t(h.wtot) * 8;
-        best = std::max(best, base + std::max({3 * wb + kVecTileBytes, 2 * wb, wb + kVecTileBytes}));
+    const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - kStaticSmemMargin;
+    for (int m = LRB_METHOD_BICGSTAB; m < kMethods; ++m) {
+      int64_t best = 3 * (kHdrBytes + 5 * int64_t(kVecTileBytes));
+      StageHdr h;
+      for (int p : D.parts) {
+        const lrb_part* P = by_index[p];
+        for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
+          const int64_t need = tile_geometry(P, lt, p, 0, h);
+          if (need <= 0 || need > stage_bytes) continue;   // not staged (direct loads)
+          best = std::max(best, method_need(m, kRecBytes + h.vbytes, int64_t(h.wtot) * 8));
+        }
+      }
+      best = (best + 127) & ~int64_t(127);
+      const int64_t n = std::min<int64_t>(kStreamMaxStages, budget / best);
+      if (n >= std::max(kTeams, kIssuers)) {
+        m_bytes[m] = int(best);
+        m_stages[m] = int(n);
       }
     }
-    best = (best + 127) & ~int64_t(127);
-    const int64_t n = std::min<int64_t>(kStreamMaxStages, budget / best);
-    if (n >= std::max(kTeams, kIssuers)) {
-      bicg_bytes = int(best);
-      bicg_stages = int(n);
-    }
+    m_bytes[LRB_METHOD_CG] = m_bytes[LRB_METHOD_PCG] = stage_bytes;
+    m_stages[LRB_METHOD_CG] = m_stages[LRB_METHOD_PCG] = n_stages;
   }
-  for (int m = 0; m < 3; ++m) {
-    const bool bicg = m == LRB_METHOD_BICGSTAB;
-    const void* sfn = (use_stream && (!bicg || bicg_stages)) ? stream_kernel(m, D.inl) : nullptr;
+  for (int m = 0; m < kMethods; ++m) {
+    const void* sfn = (use_stream && m_stages[m]) ? stream_kernel(m, D.inl) : nullptr;
     if (sfn) {
       D.fn[m] = sfn;
       D.block[m] = kStreamThreads;
       D.streaming[m] = true;
-      D.stage_bytes[m] = bicg ? bicg_bytes : stage_bytes;
-      D.n_stages[m] = bicg ? bicg_stages : n_stages;
+      D.stage_bytes[m] = m_bytes[m];
+      D.n_stages[m] = m_stages[m];
       D.smem[m] = stream_smem_bytes(D.stage_bytes[m], D.n_stages[m]);
       D.grid[m] = stream_grid(sfn, D.device, D.n_tiles, n_share, D.smem[m]);
     } else {
       D.fn[m] = solve_kernel(m, D.inl);
+      if (!D.fn[m]) continue;   // PCG1 exists only as a streaming kernel
       D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
     }
     if (D.grid[m] <= 0) {
-      set_error("lrb_team_create: cannot size the persistent grid (part too large?)");
+      set_error("lrb_team_create: cannot size the persistent grid of method " + std::to_string(m) +
+                " (" + (D.streaming[m] ? "streaming" : "classic") + ", dynamic smem " +
+                std::to_string(D.smem[m]) + " B, status " + std::to_string(D.grid[m]) + ": " +
+                cudaGetErrorString(cudaGetLastError()) + ")");
       return LRB_ERUNTIME;
     }
   }
@@ -796,8 +821,10 @@ static const void* solve_kernel(int method, bool inl) {
       return inl ? (const void*)team_cg_kernel<false, true> : (const void*)team_cg_kernel<false, false>;
     case LRB_METHOD_PCG:
       return inl ? (const void*)team_cg_kernel<true, true> : (const void*)team_cg_kernel<true, false>;
-    default:
+    case LRB_METHOD_BICGSTAB:
       return inl ? (const void*)team_bicgstab_kernel<true> : (const void*)team_bicgstab_kernel<false>;
+    default:
+      return nullptr;
   }
 }
 
@@ -849,6 +876,8 @@ static const void* stream_kernel(int method, bool inl) {
     case LRB_METHOD_BICGSTAB:
       return inl ? (const void*)team_bicgstab_stream_kernel<true>
                  : (const void*)team_bicgstab_stream_kernel<false>;
+    case LRB_METHOD_PCG1:
+      return inl ? (const void*)team_pcg1_stream_kernel<true> : (const void*)team_pcg1_stream_kernel<false>;
     default:
       return nullptr;
   }
@@ -892,7 +921,7 @@ static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int6
 static int stream_stage_bytes(const TeamDevice& D, lrb_part* const* by_index, int* n_stages) {
   int dev_smem = 0;
   cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, D.device);
-  const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - 1024;
+  const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - kStaticSmemMargin;
   const int64_t cap = budget / 2;   // at least double-buffered
   int64_t best = kHdrBytes + 5 * kVecTileBytes;   // elementwise phases
   StageHdr h;
@@ -1290,7 +1319,7 @@ int lrb_team_debug(lrb_team* team, int64_t* out) {
 }
 
 int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out) {
-  if (!team || !out || method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+  if (!team || !out || method < LRB_METHOD_CG || method >= kMethods) {
     set_error("lrb_team_kernel_info: bad arguments");
     return LRB_EVALUE;
   }
@@ -1350,7 +1379,7 @@ int lrb_team_profile_read(lrb_team* team, int64_t* out, int32_t cap) {
 }
 
 int lrb_team_profile_counters(lrb_team* team, int32_t method, int64_t* out, int32_t cap) {
-  if (!team || !out || method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+  if (!team || !out || method < LRB_METHOD_CG || method >= kMethods) {
     set_error("lrb_team_profile_counters: bad arguments");
     return LRB_EVALUE;
   }
@@ -1472,10 +1501,16 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     set_error("tol must be positive");
     return LRB_EVALUE;
   }
-  if (method < LRB_METHOD_CG || method > LRB_METHOD_BICGSTAB) {
+  if (method < LRB_METHOD_CG || method >= kMethods) {
     set_error("lrb_team_solve: unknown method");
     return LRB_EVALUE;
   }
+  for (auto& D : team->devs)
+    if (!D.fn[method]) {
+      set_error("lrb_team_solve: pcg1 (single-reduction PCG) needs the streaming solver "
+                "(unset LRB_SOLVER=classic; stages must fit shared memory)");
+      return LRB_EVALUE;
+    }
   std::lock_guard<std::mutex> lk(team->mu);
   const bool multi = team->devs.size() > 1;
   for (auto& D : team->devs) {

@@ -60,6 +60,7 @@ constexpr int kVecTileBytes = kTile * 8;          // one vector's rows of a tile
 constexpr int kStreamMaxStages = LRB_MAX_STAGES;
 constexpr int kMaxPack = 4;                       // tiles per stage in elementwise phases
 constexpr int kSlotRing = 2 * kStreamMaxStages;   // group-sum slots (see consume_phase)
+constexpr int kSlotNR = 4;                        // reductions a group-sum slot holds
 constexpr int kConsumerBar = 1;                   // named barrier of the consumer warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -146,7 +147,7 @@ struct StreamSmem {
   char* stages;        // n_stages * stage_bytes
   uint64_t* full;      // [kStreamMaxStages][kTeams]
   uint64_t* empty;     // [kStreamMaxStages][kTeams]
-  double* wsum;        // [kSlotRing][kMaxPack][kGroups][2] group sums awaiting their tile sum
+  double* wsum;        // [kSlotRing][kMaxPack][kGroups][kSlotNR] group sums awaiting their tile sum
   unsigned long long* cnt;   // [kCnt]
 };
 
@@ -158,12 +159,12 @@ __device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
   S.full = reinterpret_cast<uint64_t*>(tail);
   S.empty = S.full + kStreamMaxStages * kTeams;
   S.wsum = reinterpret_cast<double*>(S.empty + kStreamMaxStages * kTeams);
-  S.cnt = reinterpret_cast<unsigned long long*>(S.wsum + size_t(kSlotRing) * kMaxPack * kGroups * 2);
+  S.cnt = reinterpret_cast<unsigned long long*>(S.wsum + size_t(kSlotRing) * kMaxPack * kGroups * kSlotNR);
   return S;
 }
 __host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
   return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * kTeams * 8 +
-         size_t(kSlotRing) * kMaxPack * kGroups * 2 * 8 + kCnt * 8;
+         size_t(kSlotRing) * kMaxPack * kGroups * kSlotNR * 8 + kCnt * 8;
 }
 
 __device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool inl) {
@@ -174,7 +175,7 @@ __device__ __forceinline__ const PartDev& part_of(const TeamDev& T, int p, bool 
 struct Spec {
   int nwv;                 // window vectors (0: elementwise phase)
   int ntv;                 // tile vectors
-  const double* wv[3];
+  const double* wv[4];
   const double* tv[5];
 };
 
@@ -274,7 +275,7 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       const Spec spn = spec_of(Pn);
       bulk_prefetch_l2(Pn.val + nxt.e0, unsigned(nxt.vbytes));
 #pragma unroll
-      for (int v = 0; v < 3; ++v)
+      for (int v = 0; v < 4; ++v)
 #pragma unroll
         for (int w = 0; w < kMaxWin; ++w)
           if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
@@ -303,7 +304,7 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       bulk_g2s(d, P.val + cur.e0, unsigned(cur.vbytes), full, pol_stream);
       d += cur.vbytes;
 #pragma unroll
-      for (int v = 0; v < 3; ++v)
+      for (int v = 0; v < 4; ++v)
 #pragma unroll
         for (int w = 0; w < kMaxWin; ++w)
           if (v < sp.nwv && w < cur.nw)
@@ -426,6 +427,23 @@ struct PBiCG {
   double beta, omega;
   __device__ __forceinline__ double operator()(int q) const {
     return __dadd_rn(w0[q], __dmul_rn(beta, __dsub_rn(w1[q], __dmul_rn(omega, w2[q]))));
+  }
+};
+
+// Single-reduction PCG operand: u_new = dinv * (r - alpha * (w + beta * s_old))
+// (w0 = r, w1 = dinv, w2 = w, w3 = s_old; first iteration: s = w).
+struct UCG1 {
+  const double* __restrict__ w0;
+  const double* __restrict__ w1;
+  const double* __restrict__ w2;
+  const double* __restrict__ w3;
+  double alpha, beta;
+  bool first;
+  __device__ __forceinline__ double s(int q) const {
+    return first ? w2[q] : __dadd_rn(w2[q], __dmul_rn(beta, w3[q]));
+  }
+  __device__ __forceinline__ double operator()(int q) const {
+    return __dmul_rn(w1[q], __dsub_rn(w0[q], __dmul_rn(alpha, s(q))));
   }
 };
 
@@ -560,10 +578,10 @@ __device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S,
   const int sl = k % kSlotRing;
   for (int j = 0; j < cnt; ++j) {
     if (my_warp == (warp_sel + j) % n_sel && lane < NR) {
-      const double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups) * 2;
+      const double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups) * kSlotNR;
       double sum = w[lane];
 #pragma unroll
-      for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * 2 + lane]);
+      for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * kSlotNR + lane]);
       T.partials[(tile0 + j) * kMaxRed + lane] = sum;
     }
   }
@@ -581,7 +599,7 @@ __device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S,
 template <int NR, bool INL, bool ELEM, class Body>
 __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, int gseq, int kind,
                                               int ntv, Body&& body) {
-  static_assert(NR <= 2, "group-sum slots hold two reductions");
+  static_assert(NR <= kSlotNR, "group-sum slots hold kSlotNR reductions");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tm = warp / kTeamWarps;             // team
   const int wt = warp - tm * kTeamWarps;        // warp within the team
@@ -629,13 +647,13 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
         body(P, H, st, V, tt + m * kTPB, acc[m]);
       }
       const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      double* ws = S.wsum + size_t(sl * kMaxPack + j) * kGroups * 2;
+      double* ws = S.wsum + size_t(sl * kMaxPack + j) * kGroups * kSlotNR;
 #pragma unroll
       for (int m = 0; m < kRPT; ++m) {
         group_reduce<NR>(acc[m]);
         if (lane == 0)
 #pragma unroll
-          for (int q = 0; q < NR; ++q) ws[(m * kTeamWarps + wt) * 2 + q] = acc[m][q];
+          for (int q = 0; q < NR; ++q) ws[(m * kTeamWarps + wt) * kSlotNR + q] = acc[m][q];
       }
       if (kProf && T.prof_cta && threadIdx.x == 0) {
         const long long c5 = clock64();
@@ -1059,6 +1077,196 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     out->iterations = it > T.max_iter ? T.max_iter : it;
     out->converged = converged ? 1 : 0;
     out->breakdown = breakdown ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single-reduction Jacobi-PCG (Chronopoulos-Gear, method
+// "pcg1"): ONE fused SpMV phase and one team barrier per iteration instead of
+// two.  With u = M r (M = diag^-1), w = A u, s = A p kept as recurrences:
+//   beta = gamma / gamma_prev, eta = delta - beta * gamma / alpha_prev,
+//   alpha = gamma / eta;  p = u + beta p, s = w + beta s,
+//   x += alpha p, r -= alpha s, u = M r, w = A u,
+//   gamma = r.u, delta = w.u, rho = r.r   (one fused reduction)
+// The neighbours' u_new = dinv (r - alpha (w + beta s_old)) is computed on the
+// fly from four staged windows (r, dinv, w, s_old); r, w, s are double-
+// buffered.  Mathematically CG's iterates; rounding differs from the
+// two-phase kernel (parity by tolerance).
+// Buffers: x, p = p0; r in {r, rhat}; w in {v0, v1}; s in {s, t}.
+// ---------------------------------------------------------------------------
+template <bool INL>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    team_pcg1_stream_kernel(const __grid_constant__ TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  const StreamSmem S = stream_smem(T);
+  stream_init(T, S);
+  int gseq = 0;
+  double red[4];
+  auto rbuf = [](const PartDev& Q, int b) -> double* { return b ? Q.rhat : Q.r; };
+  auto wbuf = [](const PartDev& Q, int b) -> double* { return b ? Q.v1 : Q.v0; };
+  auto sbuf = [](const PartDev& Q, int b) -> double* { return b ? Q.t : Q.s; };
+  // ---- phase 0: x = 0, r = b, b.b
+  stream_phase<1, INL, true>(
+      T, S, gseq, red, 0, [&](const PartDev& P) { return Spec{0, 1, {nullptr}, {P.b}}; },
+      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[1]) {
+        if (lr >= H.rows) return;
+        const int64_t i = H.row0 + lr;
+        const double b = V[0][lr];
+        P.x[i] = 0.0;
+        P.r[i] = b;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+      });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  // ---- phase 0b: u0 = M r0, w0 = A u0, gamma = r.u, delta = w.u
+  auto u0_g = [](const PartDev& Q, int64_t j) -> double { return __dmul_rn(Q.dinv[j], Q.r[j]); };
+  stream_phase<2, INL, false>(
+      T, S, gseq, red, 1, [&](const PartDev& P) { return Spec{2, 0, {P.r, P.dinv}, {}}; },
+      [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[2]) {
+        double wi, ui;
+        if (H.tma) {
+          const StagedTile t = staged_tile(st, H, 2);
+          const int sl = lr >> 5;
+          const int2* slot = slice_slots(st, H, sl);
+          const double* rw = t.w(0);
+          const double* dw = t.w(1);
+          auto u = [&](int q) { return __dmul_rn(dw[q], rw[q]); };
+          wi = staged_row(P, parts, H, t, slot, lr, u, u0_g);
+          if (lr >= H.rows) return;
+          ui = u(diag_pos(H, slot, sl, H.row0 + lr));
+        } else {
+          if (lr >= H.rows) return;
+          const int64_t i = H.row0 + lr;
+          wi = row_spmv(P, parts, i, u0_g);
+          ui = u0_g(P, i);
+        }
+        const int64_t i = H.row0 + lr;
+        P.v0[i] = wi;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(P.r[i], ui));
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(wi, ui));
+      });
+  if (team_failed(T)) return;
+  double gamma = red[0], delta = red[1], gamma_prev = 1.0, alpha_prev = 1.0, res = 1.0;
+  int par = 0;   // current r, w, s buffers; the phase writes the other ones
+  bool converged = false;
+  int it = 0;
+  for (it = 1; it <= T.max_iter; ++it) {
+    const bool first = (it == 1);
+    const double beta = first ? 0.0 : gamma / gamma_prev;
+    const double eta = first ? delta : __dsub_rn(delta, __dmul_rn(beta, gamma / alpha_prev));
+    if (eta <= 0.0) {
+      if (lead) team_fail(T, LRB_ENOTPD);
+      break;
+    }
+    const double alpha = gamma / eta;
+    // ---- fused phase: p, s, x, r updates, u_new, w_new = A u_new, three dots
+    auto s_g = [&](const PartDev& Q, int64_t j) -> double {
+      const double w = wbuf(Q, par)[j];
+      return first ? w : __dadd_rn(w, __dmul_rn(beta, sbuf(Q, par)[j]));
+    };
+    auto u_g = [&](const PartDev& Q, int64_t j) -> double {
+      return __dmul_rn(Q.dinv[j], __dsub_rn(rbuf(Q, par)[j], __dmul_rn(alpha, s_g(Q, j))));
+    };
+    stream_phase<3, INL, false>(
+        T, S, gseq, red, 1,
+        [&](const PartDev& P) {
+          return Spec{first ? 3 : 4, 2, {rbuf(P, par), P.dinv, wbuf(P, par), sbuf(P, par)}, {P.p0, P.x}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[3]) {
+          double wn, r_i, s_i, d_i, po, xo;
+          if (H.tma) {
+            const StagedTile t = staged_tile(st, H, first ? 3 : 4);
+            const int sl = lr >> 5;
+            const int2* slot = slice_slots(st, H, sl);
+            const UCG1 u{t.w(0), t.w(1), t.w(2), t.w(3), alpha, beta, first};
+            wn = staged_row(P, parts, H, t, slot, lr, u, u_g);
+            if (lr >= H.rows) return;
+            const int qd = diag_pos(H, slot, sl, H.row0 + lr);
+            r_i = t.w(0)[qd];
+            d_i = t.w(1)[qd];
+            s_i = u.s(qd);
+            po = t.tail(0)[lr];
+            xo = t.tail(1)[lr];
+          } else {
+            if (lr >= H.rows) return;
+            const int64_t i = H.row0 + lr;
+            wn = row_spmv(P, parts, i, u_g);
+            r_i = rbuf(P, par)[i];
+            d_i = P.dinv[i];
+            s_i = s_g(P, i);
+            po = P.p0[i];
+            xo = P.x[i];
+          }
+          const int64_t i = H.row0 + lr;
+          const double u_old = __dmul_rn(d_i, r_i);
+          const double p_i = first ? u_old : __dadd_rn(u_old, __dmul_rn(beta, po));
+          const double r_new = __dsub_rn(r_i, __dmul_rn(alpha, s_i));
+          const double u_new = __dmul_rn(d_i, r_new);
+          P.p0[i] = p_i;
+          P.x[i] = __dadd_rn(xo, __dmul_rn(alpha, p_i));
+          rbuf(P, par ^ 1)[i] = r_new;
+          sbuf(P, par ^ 1)[i] = s_i;
+          wbuf(P, par ^ 1)[i] = wn;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(r_new, u_new));
+          acc[1] = __dadd_rn(acc[1], __dmul_rn(wn, u_new));
+          acc[2] = __dadd_rn(acc[2], __dmul_rn(r_new, r_new));
+        });
+    if (team_failed(T)) break;
+    par ^= 1;
+    gamma_prev = gamma;
+    alpha_prev = alpha;
+    gamma = red[0];
+    delta = red[1];
+    const double rec = sqrt(red[2]) / bnorm;
+    if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
+    if (rec <= T.tol || it % 10 == 0) {
+      auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
+      stream_phase<1, INL, false>(
+          T, S, gseq, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x}, {P.b}}; },
+          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr,
+              double (&acc)[1]) {
+            if (H.tma) {
+              const StagedTile t = staged_tile(st, H, 1);
+              const int2* slot = slice_slots(st, H, lr >> 5);
+              const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+              if (lr < H.rows) {
+                const double d = __dsub_rn(t.tail(0)[lr], ax);
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+              }
+            } else if (lr < H.rows) {
+              const int64_t i = H.row0 + lr;
+              const double ax = row_spmv(P, parts, i, xg);
+              const double d = __dsub_rn(P.b[i], ax);
+              acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+            }
+          });
+      if (team_failed(T)) break;
+      res = sqrt(red[0]) / bnorm;
+      if (res <= T.tol) {
+        converged = true;
+        break;
+      }
+    } else {
+      res = rec;
+    }
+  }
+  stream_flush_counters(T, S);
+  if (lead) {
+    out->iterations = it > T.max_iter ? T.max_iter : it;
+    out->converged = converged ? 1 : 0;
     out->residual = res;
     out->bnorm = bnorm;
   }

@@ -15,7 +15,7 @@ import numpy as np
 
 from .transport import CommGroup
 
-METHODS = ("cg", "pcg", "bicgstab")
+METHODS = ("cg", "pcg", "bicgstab", "pcg1")
 
 
 @dataclass(frozen=True)
@@ -118,7 +118,9 @@ def cg_solve(matrix, plan: HaloPlan, b, tol: float, max_iter: int, comm: CommGro
     """Distributed CG (solver.py:100-147): x0 = 0, true residual every 10
     iterations or when the recurrence residual meets tol, converged only on
     the true residual, max_iter reports instead of raising.  method="pcg"
-    selects Jacobi-PCG (pressure), "bicgstab" BiCGStab (momentum)."""
+    selects Jacobi-PCG (pressure), "bicgstab" BiCGStab (momentum), "pcg1" the
+    single-reduction (Chronopoulos-Gear) Jacobi-PCG: one team barrier per
+    iteration, CG's iterates up to rounding."""
     return krylov_solve(matrix, plan, b, tol, max_iter, comm, method, history)
 
 

@@ -171,3 +171,38 @@ def test_stream_bicgstab_bit_identical(dims, n_cpu, alpha, dev_ranks):
 
     lrb.run_world(n_cpu, program)
     assert holder["r"]["bicgstab"].converged
+
+
+@pytest.mark.parametrize("dims,n_cpu,alpha,dev_ranks", [((24, 24, 24), 4, 2, None),
+                                                        ((20, 20, 20), 4, 1, [0, 0, 1, 1]),
+                                                        ((100, 100, 100), 4, 4, None)])
+def test_pcg1_matches_pcg(dims, n_cpu, alpha, dev_ranks):
+    """Single-reduction PCG: CG's iterates in exact arithmetic, so the same
+    iteration count (+-1) and residual history / solution to rounding."""
+    from paper_2510_08536_b200.device import Team
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 3), "direct")
+        parts = s.comm.allgather(s.part) if s.is_owner else None
+        if s.is_owner and s.comm.group_rank == 0:
+            team = Team(parts, dev_ranks=dev_ranks)
+            assert team.kernel_info("pcg1")["streaming"] == 1
+            bs = [np.ones(p.n) for p in parts]
+            holder["pcg"] = team.solve("pcg", bs, 1e-9, 500, hist_cap=500)
+            holder["pcg1"] = team.solve("pcg1", bs, 1e-9, 500, hist_cap=500)
+            holder["pcg1b"] = team.solve("pcg1", bs, 1e-9, 500, hist_cap=500)
+        return None
+
+    lrb.run_world(n_cpu, program)
+    (xa, ra, ha), (xb, rb, hb), (xc, rc, hc) = holder["pcg"], holder["pcg1"], holder["pcg1b"]
+    assert ra.converged and rb.converged and abs(ra.iterations - rb.iterations) <= 1
+    n = min(len(ha), len(hb))
+    np.testing.assert_allclose(hb[:n], ha[:n], rtol=1e-6, atol=1e-14)
+    xa, xb = np.concatenate(xa), np.concatenate(xb)
+    assert np.linalg.norm(xb - xa) <= 1e-7 * np.linalg.norm(xa)
+    # deterministic run to run
+    assert rc.iterations == rb.iterations and np.array_equal(hc, hb)
+    assert all(np.array_equal(a, b) for a, b in zip(xc, holder["pcg1"][0]))

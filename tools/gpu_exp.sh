@@ -1,6 +1,6 @@
 export LRB_BARRIER_TIMEOUT_S=10
-V=$PWD/paper_2510_08536_b200/var_t448.so
-LRB_LIB=$V timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-LRB_LIB=$PWD/paper_2510_08536_b200/var_t448_prof.so timeout 300 python tools/phase_profile.py 2>/dev/null | head -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('t448', 'stages', d['info']['stages'], d['info']['stage_bytes'], {k:d[k]['us'] for k in ('A','B','C','A_sync','B_sync')}, 'A waits', d['waits_us']['A'])"
-bash tools/variants.sh $PWD/paper_2510_08536_b200/libldurepart_b200.so $V 2>&1 | grep -v "^  \|Traceback\|^json\|^    "
+timeout 900 python -m pytest tests/test_gpu_stream.py -x -q 2>&1 | tail -3
+for w in c1 c2 c3; do for m in pcg pcg1; do
+timeout 600 python bench.py --workload $w --method $m --no-cpu-baseline > gpurun_out/b_${w}_$m.json 2>gpurun_out/b_${w}_$m.err
+python -c "import json; d=json.load(open('gpurun_out/b_${w}_$m.json')); print('$w $m', d['value'], d['roofline']['kernel_ms'], d['roofline']['frac'], d['e2e']['value'], d['breakdown']['iterations'][:4])" || tail -3 gpurun_out/b_${w}_$m.err
+done; done
