@@ -990,7 +990,8 @@ static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, 
           int32_t e = 0;
           for (int w = 0; w < h.nw; ++w)
             if (c >= h.wa[w] && c < h.wa[w] + h.wl[w]) e = int32_t(h.woff[w] - h.wa[w] + off);
-          tb.slot[j][k] = int2_t_{off, e};
+          tb.off[j][k] = off;
+          tb.del[j][k] = e;
           if (off == 0 && h.sdiag[j] < 0) h.sdiag[j] = int8_t(k);
         }
       }

@@ -219,39 +219,39 @@ __global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ p
 // (v = tid + q * kRedLanes / LPT): the classic kernels (256 threads) LPT = 2,
 // the streaming kernels (512 consumer threads) LPT = 1.  Loads are issued in
 // batches so a lane's chain costs ceil(tiles / kRedLanes / batch) L2 trips.
+// Partials are stored reduction-major ([kMaxRed][n_tiles]): this step is
+// bound by ONE SM's L2 bandwidth, and a warp now reads 8 B per tile and
+// reduction as whole 256-B lines (a 200^3 part: 10.4 -> ~2 us per barrier).
 constexpr int kRedLanes = 2 * kTPB;   // = the streaming consumers (two teams)
 constexpr int kRedGroups = kRedLanes / 32;
 
 template <int NR, int LPT>
-__device__ __forceinline__ void part_value(const double* __restrict__ partials, int64_t ntiles,
-                                           double (*gs)[kMaxRed], double* out) {
+__device__ __forceinline__ void part_value(const double* __restrict__ partials, int64_t stride,
+                                           int64_t ntiles, double (*gs)[kMaxRed], double* out) {
   constexpr int kThreads = kRedLanes / LPT;
-  constexpr int kBatch = NR <= 2 ? 16 : 8;
-  constexpr int kH = (NR + 1) / 2;
+  constexpr int kBatch = 16;
   double acc[LPT][NR];
 #pragma unroll
   for (int q = 0; q < LPT; ++q)
 #pragma unroll
     for (int j = 0; j < NR; ++j) acc[q][j] = 0.0;
   if (threadIdx.x < kThreads) {
-    const double2* base = reinterpret_cast<const double2*>(partials);
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       const int64_t v = threadIdx.x + int64_t(q) * kThreads;
       for (int64_t t0 = v; t0 < ntiles; t0 += int64_t(kBatch) * kRedLanes) {
-        double2 x[kBatch][kH];
+        double x[kBatch][NR];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const int64_t t = t0 + int64_t(u) * kRedLanes;
 #pragma unroll
-          for (int h = 0; h < kH; ++h)
-            x[u][h] = t < ntiles ? __ldcg(base + t * (kMaxRed / 2) + h) : make_double2(0.0, 0.0);
+          for (int j = 0; j < NR; ++j) x[u][j] = t < ntiles ? __ldcg(partials + j * stride + t) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           if (t0 + int64_t(u) * kRedLanes >= ntiles) break;
 #pragma unroll
-          for (int j = 0; j < NR; ++j) acc[q][j] = __dadd_rn(acc[q][j], (j & 1) ? x[u][j / 2].y : x[u][j / 2].x);
+          for (int j = 0; j < NR; ++j) acc[q][j] = __dadd_rn(acc[q][j], x[u][j]);
         }
       }
     }
@@ -346,7 +346,10 @@ __device__ void team_sync(const TeamDev& T, double* red) {
     const int64_t pbuf = int64_t(e_next & 1) * T.n_parts * kMaxRed;
     for (int p = T.part_begin; p < T.part_end; ++p) {
       const PartDev& P = T.parts[p];
-      part_value<NR, LPT>(T.partials + P.tile0 * kMaxRed, P.ntiles, gs, pv);
+      part_value<NR, LPT>(T.partials + P.tile0, T.n_tiles, P.ntiles, gs, pv);
+#ifdef LRB_STAMP3
+      if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
+#endif
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
@@ -513,7 +516,7 @@ __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&&
     double s = wsm[(t * kGroups) * kMaxRed + j];
 #pragma unroll
     for (int g = 1; g < kGroups; ++g) s = __dadd_rn(s, wsm[(t * kGroups + g) * kMaxRed + j]);
-    T.partials[tile_of(T, t) * kMaxRed + j] = s;
+    T.partials[j * T.n_tiles + tile_of(T, t)] = s;
   }
   team_sync<NR, kRedLanes / kTPB>(T, red);
 }

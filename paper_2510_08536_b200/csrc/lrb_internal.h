@@ -114,17 +114,16 @@ struct alignas(16) StageHdr : StageHdrFields {
 };
 static_assert(sizeof(StageHdr) == kHdrBytes, "stage header must be exactly kHdrBytes");
 
-struct int2_t_ {
-  int32_t x, y;
-};
-
 // Slot tables of a staged tile: for each distinct pattern and slot k, the
 // column offset (col - row) and the shared-memory delta e such that a row i's
 // operand for that slot sits at staged index i + e (window arithmetic done
 // once on the host instead of per warp and row on the device).
-constexpr int kTabBytes = kHdrPats * 16 * 8;
+// Structure of arrays: a slice's deltas are 16-byte aligned, so a warp reads
+// four slots per vector load.
+constexpr int kTabBytes = kHdrPats * kPatW * 8;
 struct alignas(16) StageTab {
-  int2_t_ slot[kHdrPats][16];
+  int32_t off[kHdrPats][kPatW];
+  int32_t del[kHdrPats][kPatW];
 };
 
 // What a staged SpMV tile carries besides values and windows, as ONE
@@ -165,7 +164,7 @@ struct TeamDev {
   int64_t n_tiles;          // tiles of this device
   PartDev* parts;           // [n_parts] (remote parts carry peer pointers)
   const int32_t* tile_part; // [n_tiles]
-  double* partials;         // [n_tiles * kMaxRed]
+  double* partials;         // [kMaxRed][n_tiles] (one reduction's tiles contiguous)
   double* part_red;         // [2][n_parts][kMaxRed] all parts' values, by epoch parity
   double* red;              // [kMaxRed] team-reduced values (this device)
   unsigned int* bar_count;

@@ -76,14 +76,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is parked by the
+// hardware until the phase completes (or the hint expires) instead of
+// spinning through issue slots the working warps need.
+#ifndef LRB_WAIT_HINT_NS
+#define LRB_WAIT_HINT_NS 1000000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
   uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
+  if constexpr (LRB_WAIT_HINT_NS > 0) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity), "n"(LRB_WAIT_HINT_NS)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
   return ok != 0;
 }
 // Spin on an mbarrier phase.  A ring that never completes is a bug, not a
@@ -94,7 +109,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, long lon
   const long long t0 = global_ns();
   for (unsigned k = 1;; ++k) {
     if (mbar_try_wait(b, parity)) return;
-    if ((k & 1023u) == 0 && global_ns() - t0 > timeout_ns) __trap();
+    if ((k & 15u) == 0 && global_ns() - t0 > timeout_ns) __trap();
   }
 }
 // 1D bulk copy global -> shared (TMA engine), completes tx bytes on bar.
@@ -205,10 +220,33 @@ struct RingPos {
   int bar;           // slot * kTeams + team
   unsigned parity;   // parity of this use of the pair's barriers
 };
-__device__ __forceinline__ RingPos ring_pos(int G, int n_stages) {
-  const int L = (n_stages % kTeams) ? n_stages * kTeams : n_stages;
-  const int slot = G % n_stages, team = G % kTeams;
-  return RingPos{slot, team, slot * kTeams + team, unsigned((G / L) & 1)};
+// The ring's divisors as multiply-high magics (a runtime modulo costs ~20
+// instructions and ring positions are taken once per stage per warp):
+// q = umulhi(G, ceil(2^32 / d)) is exact for G * d < 2^32; stage numbers
+// stay far below that (the host bounds max_iter), and larger G falls back.
+struct Ring {
+  int ns, L;
+  unsigned mns, mL;
+};
+__device__ __forceinline__ Ring make_ring(int n_stages) {
+  Ring R;
+  R.ns = n_stages;
+  R.L = (n_stages % kTeams) ? n_stages * kTeams : n_stages;
+  R.mns = 0xFFFFFFFFu / unsigned(R.ns) + 1u;
+  R.mL = 0xFFFFFFFFu / unsigned(R.L) + 1u;
+  return R;
+}
+__device__ __forceinline__ RingPos ring_pos(int G, const Ring& R) {
+  int qs, qL;
+  if (G < (1 << 26)) {
+    qs = int(__umulhi(unsigned(G), R.mns));
+    qL = int(__umulhi(unsigned(G), R.mL));
+  } else {
+    qs = G / R.ns;
+    qL = G / R.L;
+  }
+  const int slot = G - qs * R.ns, team = G & (kTeams - 1);
+  return RingPos{slot, team, slot * kTeams + team, unsigned(qL & 1)};
 }
 // First phase-local stage k of this CTA with (gseq + k) % m == r.
 __device__ __forceinline__ int first_stage(int gseq, int r, int m) {
@@ -216,10 +254,10 @@ __device__ __forceinline__ int first_stage(int gseq, int r, int m) {
 }
 // Issuer side: before filling stage G, wait until the previous stage in the
 // same slot (G - n_stages, possibly of an earlier phase) was released.
-__device__ __forceinline__ void wait_slot_free(const StreamSmem& S, int G, int n_stages, long long timeout_ns) {
-  const int Gp = G - n_stages;
+__device__ __forceinline__ void wait_slot_free(const StreamSmem& S, int G, const Ring& R, long long timeout_ns) {
+  const int Gp = G - R.ns;
   if (Gp < 0) return;
-  const RingPos pp = ring_pos(Gp, n_stages);
+  const RingPos pp = ring_pos(Gp, R);
   mbar_wait(S.empty + pp.bar, pp.parity, timeout_ns);
 }
 
@@ -249,6 +287,20 @@ __device__ __forceinline__ void load_hdr_addr(const StageHdr* h, HdrAddr& a) {
   a.vbytes = __ldg(&h->vbytes);
 }
 
+#ifndef LRB_PF_DIST
+#define LRB_PF_DIST 1
+#endif
+struct PfAddr {
+  int64_t e0;
+  int32_t vbytes, part, tma;
+};
+__device__ __forceinline__ void load_pf_addr(const StageHdr* h, PfAddr& a) {
+  a.e0 = __ldg(&h->e0);
+  a.vbytes = __ldg(&h->vbytes);
+  a.part = __ldg(&h->part);
+  a.tma = __ldg(&h->tma);
+}
+
 // SpMV phases: issuer pw issues stages k = pw, pw + kIssuers, ... (tile
 // cta + k * grid), reading each tile's header one of its stages ahead.
 template <bool INL, class SpecF>
@@ -262,12 +314,34 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
   const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
   const int64_t G = gridDim.x;
   const int count = stage_count(T.n_tiles);
+  const Ring R = make_ring(T.n_stages);
   HdrAddr cur{}, nxt{};
   const int k0 = first_stage(gseq, pw, kIssuers);
   if (k0 < count) load_hdr_addr(hdrs + blockIdx.x + k0 * G, cur);
+  // Deep L2 prefetch of the values LRB_PF_DIST of this issuer's tiles ahead
+  // (the TMA ring holds ~1 stage in flight per SM; L2 prefetches need no
+  // shared memory).  pf = the header fields of the tile prefetched next.
+  constexpr int kPf = LRB_PF_DIST;
+  PfAddr pf{};
+  if (kPf > 1) {
+#pragma unroll
+    for (int j = 1; j < kPf; ++j) {
+      const int kj = k0 + j * kIssuers;
+      if (kj < count) {
+        PfAddr a;
+        load_pf_addr(hdrs + blockIdx.x + int64_t(kj) * G, a);
+        if (a.tma) bulk_prefetch_l2(part_of(T, a.part, INL).val + a.e0, unsigned(a.vbytes));
+      }
+    }
+    if (k0 + kPf * kIssuers < count) load_pf_addr(hdrs + blockIdx.x + int64_t(k0 + kPf * kIssuers) * G, pf);
+  }
   for (int k = k0; k < count; k += kIssuers) {
     const int64_t tile = blockIdx.x + k * G;
     if (k + kIssuers < count) load_hdr_addr(hdrs + tile + kIssuers * G, nxt);
+    if (kPf > 1 && k + kPf * kIssuers < count) {
+      if (pf.tma) bulk_prefetch_l2(part_of(T, pf.part, INL).val + pf.e0, unsigned(pf.vbytes));
+      if (k + (kPf + 1) * kIssuers < count) load_pf_addr(hdrs + tile + int64_t(kPf + 1) * kIssuers * G, pf);
+    }
     if (LRB_ISSUER_PREFETCH && k + kIssuers < count && nxt.tma) {
       // this issuer's next tile: bring its values and operand windows toward
       // L2 while it waits for a free slot (its copies then hit L2)
@@ -280,12 +354,12 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
         for (int w = 0; w < kMaxWin; ++w)
           if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
     }
-    const RingPos rp = ring_pos(gseq + k, T.n_stages);
+    const RingPos rp = ring_pos(gseq + k, R);
     char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
     uint64_t* full = S.full + rp.bar;
     {
       const long long c0 = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
-      wait_slot_free(S, gseq + k, T.n_stages, T.timeout_ns);
+      wait_slot_free(S, gseq + k, R, T.timeout_ns);
       if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
     const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
@@ -335,14 +409,15 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
   const int ntv = spec_of(part_of(T, T.part_begin, INL)).ntv;
   const int K = pack_factor(T, ntv);
   const int count = stage_count((n_tiles + K - 1) / K);
+  const Ring R = make_ring(T.n_stages);
   for (int k = first_stage(gseq, pw, kIssuers); k < count; k += kIssuers) {
     const int64_t c0 = (int64_t(blockIdx.x) + int64_t(k) * gridDim.x) * K;
-    const RingPos rp = ring_pos(gseq + k, T.n_stages);
+    const RingPos rp = ring_pos(gseq + k, R);
     char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
     uint64_t* full = S.full + rp.bar;
     {
       const long long t0 = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
-      wait_slot_free(S, gseq + k, T.n_stages, T.timeout_ns);
+      wait_slot_free(S, gseq + k, R, T.timeout_ns);
       if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - t0;
     }
     const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
@@ -447,47 +522,85 @@ struct UCG1 {
   }
 };
 
+// Slot table of a slice in the staged StageTab (SoA): for slot k the column
+// offset off[k] (col - row) and the shared-memory delta del[k] such that row
+// i's operand sits at staged index i + del[k].
+struct Slots {
+  const int32_t* off;
+  const int32_t* del;
+};
+__device__ __forceinline__ Slots slice_slots(const char* st, const StageHdr& H, int sl) {
+  const int32_t* tab = reinterpret_cast<const int32_t*>(st + kHdrBytes);
+  const int p = H.spat[sl];
+  return Slots{tab + p * kPatW, tab + (kHdrPats + p) * kPatW};
+}
+// Slot of the diagonal (offset 0) of a slice's pattern; staged index of row
+// i's own operand.
+__device__ __forceinline__ int diag_slot(const StageHdr& H, int sl) { return H.sdiag[H.spat[sl]]; }
+__device__ __forceinline__ int diag_pos(const StageHdr& H, const Slots& slot, int sl, int64_t i) {
+  return int(i) + slot.del[diag_slot(H, sl)];
+}
+
+#ifndef LRB_FASTPATH
+#define LRB_FASTPATH 0
+#endif
+#ifndef LRB_ABENCH      // diagnostics: run phase A LRB_ABENCH times, nothing else
+#define LRB_ABENCH 0
+#endif
+#ifndef LRB_NOCOMPUTE   // diagnostics: SpMV consumers skip the row bodies
+#define LRB_NOCOMPUTE 0
+#endif
 // Fixed-width row product: WM pattern slots, all operand loads issued
-// before the accumulation chain (slots k >= w and holes are masked to 0:
-// holes hold 0.0 in the SELL layout, so acc + 0 * 0 leaves acc unchanged —
-// acc is never -0.0).
-template <int WM, class XS>
-__device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk, const int2* __restrict__ slot,
-                                            const double* __restrict__ sval, const XS& xs) {
+// before the accumulation chain.  MASK: slots k >= w and holes get a zero
+// operand (a hole's value is a finite 0.0 in the SELL layout, so acc + a * 0
+// leaves acc unchanged — acc is never -0.0); !MASK: the whole warp's rows
+// are fully occupied (w == WM), no selects.  xd = the operand of slot dk
+// (the diagonal's, for the phase's own-row update) from the same registers.
+template <int WM, bool MASK, class XS>
+__device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk, const int32_t* __restrict__ del,
+                                            int dk, const double* __restrict__ sval, const XS& xs, double& xd) {
+  constexpr int kQ = (WM + 3) / 4;
+  int d[4 * kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int4 v = reinterpret_cast<const int4*>(del)[q];
+    d[4 * q] = v.x;
+    d[4 * q + 1] = v.y;
+    d[4 * q + 2] = v.z;
+    d[4 * q + 3] = v.w;
+  }
   double a[WM], x[WM];
 #pragma unroll
   for (int k = 0; k < WM; ++k) {
-    const bool on = k < w && ((msk >> k) & 1u);
-    const int2 se = slot[k];
-    a[k] = on ? sval[eb + k * kSlice] : 0.0;
-    x[k] = on ? xs(ii + se.y) : 0.0;
+    if constexpr (MASK) {
+      const bool on = k < w && ((msk >> k) & 1u);
+      a[k] = k < w ? sval[eb + k * kSlice] : 0.0;
+      x[k] = on ? xs(ii + d[k]) : 0.0;
+    } else {
+      a[k] = sval[eb + k * kSlice];
+      x[k] = xs(ii + d[k]);
+    }
   }
+  xd = x[0];
+#pragma unroll
+  for (int k = 1; k < WM; ++k)
+    if (k == dk) xd = x[k];
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < WM; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k], x[k]));
   return acc;
 }
 
-// Slot table of a slice in the staged StageTab: for slot k, (column offset,
-// delta e such that row i's operand sits at staged index i + e).
-__device__ __forceinline__ const int2* slice_slots(const char* st, const StageHdr& H, int sl) {
-  return reinterpret_cast<const int2*>(st + kHdrBytes) + H.spat[sl] * 16;
-}
-// Staged index of row i's own operand (its diagonal slot).
-__device__ __forceinline__ int diag_pos(const StageHdr& H, const int2* slot, int sl, int64_t i) {
-  return int(i) + slot[H.sdiag[H.spat[sl]]].y;
-}
-
-// Staged SpMV of tile row lr (its 32-row slice is warp-uniform); xs(q) is
-// the staged operand, fh(owner part, row) a halo column's operand.
+// Staged SpMV of tile row lr (its 32-row slice is warp-uniform; every lane
+// of the warp calls it); xs(q) is the staged operand, fh(owner part, row) a
+// halo column's operand; xd receives the row's diagonal operand.
 template <bool HALO, class XS, class FH>
 __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ hpart,
                                                   const int32_t* __restrict__ hidx,
                                                   const PartDev* __restrict__ parts, const StageHdr& H,
-                                                  const int2* __restrict__ slot,
-                                                  const double* __restrict__ sval,
+                                                  const Slots& slot, const double* __restrict__ sval,
                                                   const uint16_t* __restrict__ smask, int lr, const XS& xs,
-                                                  FH&& fh) {
+                                                  FH&& fh, double& xd) {
   const int lane = threadIdx.x & 31;
   const int rows = H.rows;
   const int lr0 = lr & ~31;
@@ -497,26 +610,31 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
   const int eb = s0 + lane;
   const int ii = int(H.row0) + lr;
   const unsigned msk = lr < rows ? unsigned(smask[lr]) : 0u;
+  const int dk = diag_slot(H, sl);
   if constexpr (!HALO) {
-    if (w == 7) return row_fixed<7>(w, ii, eb, msk, slot, sval, xs);
-    if (w <= 8) return row_fixed<8>(w, ii, eb, msk, slot, sval, xs);
-    return row_fixed<kPatW>(w, ii, eb, msk, slot, sval, xs);
+    if (w == 7) {
+      if (LRB_FASTPATH && __all_sync(0xffffffffu, msk == 0x7Fu))
+        return row_fixed<7, false>(w, ii, eb, msk, slot.del, dk, sval, xs, xd);
+      return row_fixed<7, true>(w, ii, eb, msk, slot.del, dk, sval, xs, xd);
+    }
+    if (w <= 8) return row_fixed<8, true>(w, ii, eb, msk, slot.del, dk, sval, xs, xd);
+    return row_fixed<kPatW, true>(w, ii, eb, msk, slot.del, dk, sval, xs, xd);
   } else {
     double acc = 0.0;
     for (int k = 0; k < w; ++k) {
-      const int2 se = slot[k];
       const bool on = (msk >> k) & 1u;
       const double a = sval[eb + k * kSlice];
-      const int c = ii + se.x;
+      const int c = ii + slot.off[k];
       double xv;
       if (on && c >= n) {
         xv = fh(parts[__ldg(hpart + (c - n))], int64_t(__ldg(hidx + (c - n))));
       } else {
-        xv = xs(on ? ii + se.y : 0);
+        xv = xs(on ? ii + slot.del[k] : 0);
         xv = on ? xv : 0.0;
       }
       acc = __dadd_rn(acc, __dmul_rn(a, xv));
     }
+    xd = dk >= 0 ? xs(ii + slot.del[dk]) : 0.0;
     return acc;
   }
 }
@@ -549,11 +667,18 @@ __device__ __forceinline__ StagedTile staged_tile(const char* st, const StageHdr
 // Dispatch on whether the part has halo columns.
 template <class XS, class FH>
 __device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
-                                             const StageHdr& H, const StagedTile& t, const int2* slot, int lr,
-                                             const XS& xs, FH&& fh) {
+                                             const StageHdr& H, const StagedTile& t, const Slots& slot, int lr,
+                                             const XS& xs, FH&& fh, double& xd) {
   const int n = int(P.n);
-  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh)
-                  : row_spmv_staged<false>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh);
+  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd)
+                  : row_spmv_staged<false>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd);
+}
+template <class XS, class FH>
+__device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
+                                             const StageHdr& H, const StagedTile& t, const Slots& slot, int lr,
+                                             const XS& xs, FH&& fh) {
+  double xd;
+  return staged_row(P, parts, H, t, slot, lr, xs, fh, xd);
 }
 
 // Vectors of one packed elementwise tile: vector v at base + v * stride.
@@ -570,7 +695,7 @@ struct VecView {
 // ---------------------------------------------------------------------------
 // Tile sums of stage k (slot k % kSlotRing): group g's sum of its tile j was
 // parked at wsum[slot][j][g]; the designated warp adds the 16 group sums in
-// group order (the canonical tile tree) into T.partials[tile].
+// group order (the canonical tile tree) into T.partials[reduction][tile].
 template <int NR>
 __device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S, int k, int64_t tile0,
                                           int cnt, int warp_sel, int n_sel, int my_warp) {
@@ -582,7 +707,7 @@ __device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S,
       double sum = w[lane];
 #pragma unroll
       for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * kSlotNR + lane]);
-      T.partials[(tile0 + j) * kMaxRed + lane] = sum;
+      T.partials[lane * T.n_tiles + tile0 + j] = sum;
     }
   }
 }
@@ -605,6 +730,7 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
   const int wt = warp - tm * kTeamWarps;        // warp within the team
   const int tt = int(threadIdx.x) - tm * kTeamThreads;
   const int ns = T.n_stages;
+  const Ring R = make_ring(ns);
   const int64_t G = gridDim.x;
   const int K = ELEM ? pack_factor(T, ntv) : 1;
   const int64_t n_tiles = T.n_tiles;
@@ -615,7 +741,7 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
     return int(n_tiles - t0 < K ? n_tiles - t0 : K);
   };
   for (int k = first_stage(gseq, tm, kTeams); k < count; k += kTeams) {
-    const RingPos rp = ring_pos(gseq + k, ns);
+    const RingPos rp = ring_pos(gseq + k, R);
     const char* st0 = S.stages + size_t(rp.slot) * T.stage_bytes;
     {
       const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
@@ -644,7 +770,7 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       for (int m = 0; m < kRPT; ++m) {
 #pragma unroll
         for (int q = 0; q < NR; ++q) acc[m][q] = 0.0;
-        body(P, H, st, V, tt + m * kTPB, acc[m]);
+        if (!(LRB_NOCOMPUTE && !ELEM)) body(P, H, st, V, tt + m * kTPB, acc[m]);
       }
       const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       double* ws = S.wsum + size_t(sl * kMaxPack + j) * kGroups * kSlotNR;
@@ -784,15 +910,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           if (H.tma) {
             const StagedTile t = staged_tile(st, H, first ? 1 : 2);
             const int sl = lr >> 5;
-            const int2* slot = slice_slots(st, H, sl);
+            const Slots slot = slice_slots(st, H, sl);
             const PnewCG pn{t.w(0), t.w(1), beta};
             const Win1 z1{t.w(0)};
-            const double qi = first ? staged_row(P, parts, H, t, slot, lr, z1, pnew_g)
-                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g);
+            double pi;   // p_new of the row itself: the diagonal slot's operand
+            const double qi = first ? staged_row(P, parts, H, t, slot, lr, z1, pnew_g, pi)
+                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g, pi);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const int qd = diag_pos(H, slot, sl, i);   // the diagonal's operand
-              const double pi = first ? z1(qd) : pn(qd);
               pout[i] = pi;
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
@@ -807,6 +932,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           }
         });
     if (team_failed(T)) break;
+#if LRB_ABENCH
+    // diagnostics build: phase A alone, back to back (timing only)
+    first = false;
+    beta = 0.5;
+    pa ^= 1;
+    if (it >= LRB_ABENCH) break;
+    continue;
+#endif
     const double pq = red[0];
     if (pq <= 0.0) {
       if (lead) team_fail(T, LRB_ENOTPD);
@@ -849,7 +982,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
               double (&acc)[1]) {
             if (H.tma) {
               const StagedTile t = staged_tile(st, H, 1);
-              const int2* slot = slice_slots(st, H, lr >> 5);
+              const Slots slot = slice_slots(st, H, lr >> 5);
               const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
@@ -950,15 +1083,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           if (H.tma) {
             const StagedTile t = staged_tile(st, H, first ? 1 : 3);
             const int sl = lr >> 5;
-            const int2* slot = slice_slots(st, H, sl);
+            const Slots slot = slice_slots(st, H, sl);
             const Win1 r1{t.w(0)};
             const PBiCG pn{t.w(0), t.w(1), t.w(2), beta, omega};
-            const double vi = first ? staged_row(P, parts, H, t, slot, lr, r1, pnew_g)
-                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g);
+            double pi;
+            const double vi = first ? staged_row(P, parts, H, t, slot, lr, r1, pnew_g, pi)
+                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g, pi);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const int qd = diag_pos(H, slot, sl, i);
-              const double pi = first ? r1(qd) : pn(qd);
               pout[i] = pi;
               vout[i] = vi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(t.tail(0)[lr], vi));
@@ -991,12 +1123,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           if (H.tma) {
             const StagedTile t = staged_tile(st, H, 2);
             const int sl = lr >> 5;
-            const int2* slot = slice_slots(st, H, sl);
+            const Slots slot = slice_slots(st, H, sl);
             const SBiCG sv{t.w(0), t.w(1), alpha};
-            const double ti = staged_row(P, parts, H, t, slot, lr, sv, sval_g);
+            double si;
+            const double ti = staged_row(P, parts, H, t, slot, lr, sv, sval_g, si);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
-              const double si = sv(diag_pos(H, slot, sl, i));
               P.s[i] = si;
               P.t[i] = ti;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(ti, si));
@@ -1045,7 +1177,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
               double (&acc)[1]) {
             if (H.tma) {
               const StagedTile t = staged_tile(st, H, 1);
-              const int2* slot = slice_slots(st, H, lr >> 5);
+              const Slots slot = slice_slots(st, H, lr >> 5);
               const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
@@ -1140,13 +1272,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         if (H.tma) {
           const StagedTile t = staged_tile(st, H, 2);
           const int sl = lr >> 5;
-          const int2* slot = slice_slots(st, H, sl);
+          const Slots slot = slice_slots(st, H, sl);
           const double* rw = t.w(0);
           const double* dw = t.w(1);
           auto u = [&](int q) { return __dmul_rn(dw[q], rw[q]); };
-          wi = staged_row(P, parts, H, t, slot, lr, u, u0_g);
+          wi = staged_row(P, parts, H, t, slot, lr, u, u0_g, ui);
           if (lr >= H.rows) return;
-          ui = u(diag_pos(H, slot, sl, H.row0 + lr));
         } else {
           if (lr >= H.rows) return;
           const int64_t i = H.row0 + lr;
@@ -1190,7 +1321,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
           if (H.tma) {
             const StagedTile t = staged_tile(st, H, first ? 3 : 4);
             const int sl = lr >> 5;
-            const int2* slot = slice_slots(st, H, sl);
+            const Slots slot = slice_slots(st, H, sl);
             const UCG1 u{t.w(0), t.w(1), t.w(2), t.w(3), alpha, beta, first};
             wn = staged_row(P, parts, H, t, slot, lr, u, u_g);
             if (lr >= H.rows) return;
@@ -1240,7 +1371,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
               double (&acc)[1]) {
             if (H.tma) {
               const StagedTile t = staged_tile(st, H, 1);
-              const int2* slot = slice_slots(st, H, lr >> 5);
+              const Slots slot = slice_slots(st, H, lr >> 5);
               const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
