@@ -650,6 +650,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_parts = take(sizeof(PartDev) * n_parts);
   const size_t o_tp = take(sizeof(int32_t) * n_tiles);
   const size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
+  const size_t o_lanes = take(sizeof(double) * kMaxRed * kLanes * D.parts.size());
   const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts * 2);  // epoch parity
   const size_t o_red = take(sizeof(double) * kMaxRed);
   const size_t o_bar = take(sizeof(unsigned) * 2);
@@ -662,7 +663,9 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   // per-tile stage headers
   const bool want_stream = solver_choice() != 1;
   int n_stages = 0;
-  const int stage_bytes = want_stream ? stream_stage_bytes(D, by_index, &n_stages) : 0;
+  // computed for the classic kernels too: the stage geometry fixes the
+  // reduction tree's units (pack_factor), so both families stay bit-identical
+  const int stage_bytes = stream_stage_bytes(D, by_index, &n_stages);
   // the ring needs a stage per issuer and per consumer team in flight
   const bool use_stream = want_stream && n_stages >= std::max(kTeams, kIssuers);
   const size_t o_hdr = use_stream ? take(sizeof(StageHdr) * n_tiles) : 0;
@@ -683,6 +686,8 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.parts = D.parts_dev;
   H.tile_part = reinterpret_cast<int32_t*>(w + o_tp);
   H.partials = reinterpret_cast<double*>(w + o_partials);
+  H.lane_vals = reinterpret_cast<double*>(w + o_lanes);
+  H.lane_fast = 0;
   H.part_red = reinterpret_cast<double*>(w + o_pred);
   H.red = reinterpret_cast<double*>(w + o_red);
   H.bar_count = reinterpret_cast<unsigned*>(w + o_bar);
@@ -739,7 +744,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   // BiCGStab and PCG1 stage more windows than CG: their own, larger rings over
   // the same stageable tiles (no streaming kernel if two stages do not fit)
   int m_bytes[kMethods] = {}, m_stages[kMethods] = {};
-  if (use_stream) {
+  if (n_stages >= std::max(kTeams, kIssuers)) {
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, D.device);
     const int64_t budget = int64_t(dev_smem) - int64_t(stream_smem_bytes(0, 0)) - kStaticSmemMargin;
@@ -775,6 +780,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
       D.smem[m] = stream_smem_bytes(D.stage_bytes[m], D.n_stages[m]);
       D.grid[m] = stream_grid(sfn, D.device, D.n_tiles, n_share, D.smem[m]);
     } else {
+      D.stage_bytes[m] = m_bytes[m];   // the reduction tree's units (classic kernels)
       D.fn[m] = solve_kernel(m, D.inl);
       if (!D.fn[m]) continue;   // PCG1 exists only as a streaming kernel
       D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
@@ -1535,6 +1541,8 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     H.max_iter = max_iter;
     H.stage_bytes = D.stage_bytes[method];
     H.n_stages = D.n_stages[method];
+    // one streaming CTA per SM = one reduction lane per CTA (kernels.cuh)
+    H.lane_fast = (D.streaming[method] && D.grid[method] <= kLanes && D.parts.size() == 1) ? 1 : 0;
     H.hist = (hist && hist_cap > 0) ? D.hist_dev : nullptr;
     H.hist_cap = hist_cap;
   }

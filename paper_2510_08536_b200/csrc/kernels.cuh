@@ -212,68 +212,116 @@ __global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ p
 // ---------------------------------------------------------------------------
 // Team barrier with fused deterministic reduction.
 // ---------------------------------------------------------------------------
-// Part value from its tile partials (canonical order, both solver families):
-// kRedLanes virtual lanes; lane v sums tiles v, v + kRedLanes, ... in order
-// (from 0.0); each group of 32 lanes is butterfly-reduced and the group sums
-// are added in group order.  A block runs it with LPT lanes per thread
-// (v = tid + q * kRedLanes / LPT): the classic kernels (256 threads) LPT = 2,
-// the streaming kernels (512 consumer threads) LPT = 1.  Loads are issued in
-// batches so a lane's chain costs ceil(tiles / kRedLanes / batch) L2 trips.
-// Partials are stored reduction-major ([kMaxRed][n_tiles]): this step is
-// bound by ONE SM's L2 bandwidth, and a warp now reads 8 B per tile and
-// reduction as whole 256-B lines (a 200^3 part: 10.4 -> ~2 us per barrier).
-constexpr int kRedLanes = 2 * kTPB;   // = the streaming consumers (two teams)
-constexpr int kRedGroups = kRedLanes / 32;
+// Canonical reduction tree (both solver families, every phase).  The leaves
+// are tile partials tau_t (t = part-local tile; a tile's value is the
+// canonical tile tree of its rows, below).  Tiles form units of K
+// consecutive tiles (K = the phase's pack factor, 1 for SpMV phases); lane
+// v < kLanes sums, from 0.0 and in ascending t, the tau_t of the units
+// u = v (mod kLanes).  The lane values are reduced in groups of 32
+// (butterfly xor 16..1, lanes >= kLanes hold 0.0), group sums in group order.
+//
+// kLanes = 148, the B200's SM count: with one streaming CTA per SM, CTA c
+// processes exactly the units of lane c (its stage k is unit c + k * 148),
+// so it computes its lane value itself, in stage order (T.lane_vals; the
+// reducer warp, stream.cuh), and the barrier's last CTA only combines 148
+// values per part.  Everywhere else (classic kernels, other grids, several
+// parts per device) the last CTA computes the lanes from the tile partials —
+// the same tree, so all configurations stay bit-identical.  (The previous
+// tree had 512 strided lanes over 32-byte partial records: 500 KB through
+// ONE SM per barrier, 10.4 us of the 10.8 us barrier at 200^3.)
+#ifndef LRB_LANES
+#define LRB_LANES 148
+#endif
+constexpr int kLanes = LRB_LANES;
+constexpr int kLaneGroups = (kLanes + 31) / 32;
+constexpr int kVecTileBytes = kTile * 8;   // one vector's rows of a tile
+constexpr int kMaxPack = 4;                // tiles per stage in elementwise phases
 
-template <int NR, int LPT>
-__device__ __forceinline__ void part_value(const double* __restrict__ partials, int64_t stride,
-                                           int64_t ntiles, double (*gs)[kMaxRed], double* out) {
-  constexpr int kThreads = kRedLanes / LPT;
-  constexpr int kBatch = 16;
-  double acc[LPT][NR];
+// Packing factor of an elementwise phase with ntv vectors (the streaming
+// kernels' stage geometry; the classic kernels use it for the tree's units).
+__device__ __forceinline__ int pack_factor(const TeamDev& T, int ntv) {
+  const int k = T.stage_bytes / (kHdrBytes + ntv * kVecTileBytes);
+  return k < 1 ? 1 : (k > kMaxPack ? kMaxPack : k);
+}
+
+// Does CTA c compute lane c itself in this phase?  Single local part
+// (T.lane_fast, set by the host for streaming single-part teams), and every
+// CTA's units belong to one lane: grid == kLanes, or at most one unit per CTA.
+__device__ __forceinline__ bool lanes_by_cta(const TeamDev& T, int64_t ntiles, int K) {
+  const int64_t units = (ntiles + K - 1) / K;
+  return T.lane_fast && (int(gridDim.x) == kLanes || units <= int64_t(gridDim.x));
+}
+
+// Lane v's value from the tile partials (the slow path): its tiles in
+// ascending order, loads batched so the chain costs ceil(tiles / 16) trips.
+template <int NR>
+__device__ __forceinline__ void lane_from_partials(const TeamDev& T, const PartDev& P, int K, int v,
+                                                   double (&acc)[NR]) {
+  const double* __restrict__ base = T.partials + P.tile0;
+  const int64_t stride = T.n_tiles, ntiles = P.ntiles;
+  int64_t u = v;   // current unit, kk its tile
+  int kk = 0;
+  for (;;) {
+    constexpr int kB = 16;
+    double x[kB][NR];
+    int nb = 0;
 #pragma unroll
-  for (int q = 0; q < LPT; ++q)
+    for (int b = 0; b < kB; ++b) {
+      const int64_t t = u * K + kk;
+      const bool in = t < ntiles;
 #pragma unroll
-    for (int j = 0; j < NR; ++j) acc[q][j] = 0.0;
-  if (threadIdx.x < kThreads) {
-#pragma unroll
-    for (int q = 0; q < LPT; ++q) {
-      const int64_t v = threadIdx.x + int64_t(q) * kThreads;
-      for (int64_t t0 = v; t0 < ntiles; t0 += int64_t(kBatch) * kRedLanes) {
-        double x[kBatch][NR];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int64_t t = t0 + int64_t(u) * kRedLanes;
-#pragma unroll
-          for (int j = 0; j < NR; ++j) x[u][j] = t < ntiles ? __ldcg(partials + j * stride + t) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          if (t0 + int64_t(u) * kRedLanes >= ntiles) break;
-#pragma unroll
-          for (int j = 0; j < NR; ++j) acc[q][j] = __dadd_rn(acc[q][j], x[u][j]);
-        }
+      for (int j = 0; j < NR; ++j) x[b][j] = in ? __ldcg(base + j * stride + t) : 0.0;
+      nb += in ? 1 : 0;
+      if (++kk == K) {
+        kk = 0;
+        u += kLanes;
       }
     }
-  }
-  // all warps shuffle (the extra producer warp with zeros), only lane groups vote
 #pragma unroll
-  for (int q = 0; q < LPT; ++q) {
+    for (int b = 0; b < kB; ++b)
+      if (b < nb)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[j] = __dadd_rn(acc[j], x[b][j]);
+    if (nb < kB) break;
+  }
+}
+
+// Part value (last CTA of the barrier, all threads): lanes, then the group tree.
+template <int NR>
+__device__ __forceinline__ void part_value(const TeamDev& T, int p, int K, double (*gs)[kMaxRed],
+                                           double* out) {
+  const PartDev& P = T.parts[p];
+  double acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+  const int v = threadIdx.x;
+  if (v < kLanes) {
+    if (lanes_by_cta(T, P.ntiles, K)) {
+      // lanes >= grid have no units (lanes_by_cta) and were not written
+      const double* lv = T.lane_vals + (size_t(p - T.part_begin) * kLanes + v) * kMaxRed;
+      if (v < int(gridDim.x))
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[j] = __ldcg(lv + j);
+    } else {
+      lane_from_partials<NR>(T, P, K, v, acc);
+    }
+  }
+  const int warp = threadIdx.x >> 5;
+  if (warp < kLaneGroups) {
 #pragma unroll
     for (int j = 0; j < NR; ++j)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[q][j] = __dadd_rn(acc[q][j], __shfl_xor_sync(0xffffffffu, acc[q][j], o));
-    const int g = int(threadIdx.x >> 5) + q * (kThreads / 32);
-    if ((threadIdx.x & 31) == 0 && threadIdx.x < kThreads)
+      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+    if ((threadIdx.x & 31) == 0)
 #pragma unroll
-      for (int j = 0; j < NR; ++j) gs[g][j] = acc[q][j];
+      for (int j = 0; j < NR; ++j) gs[warp][j] = acc[j];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       double s = gs[0][j];
-      for (int g = 1; g < kRedGroups; ++g) s = __dadd_rn(s, gs[g][j]);
+      for (int g = 1; g < kLaneGroups; ++g) s = __dadd_rn(s, gs[g][j]);
       out[j] = s;
     }
   }
@@ -321,10 +369,10 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // trip); arrival and release are acq_rel / release atomics (cumulative over
 // the CTA's writes through the preceding __syncthreads).
 constexpr int kSmemParts = 16;
-template <int NR, int LPT>
-__device__ void team_sync(const TeamDev& T, double* red) {
+template <int NR>
+__device__ void team_sync(const TeamDev& T, double* red, int K) {
   __shared__ unsigned s_last, s_gen;
-  __shared__ double gs[kRedGroups][kMaxRed];
+  __shared__ double gs[kLaneGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
   __shared__ double pvals[kSmemParts][kMaxRed];
   __syncthreads();
@@ -345,8 +393,7 @@ __device__ void team_sync(const TeamDev& T, double* red) {
     const unsigned long long e_next = (T.n_dev > 1) ? *(volatile unsigned long long*)T.epoch + 1 : 0;
     const int64_t pbuf = int64_t(e_next & 1) * T.n_parts * kMaxRed;
     for (int p = T.part_begin; p < T.part_end; ++p) {
-      const PartDev& P = T.parts[p];
-      part_value<NR, LPT>(T.partials + P.tile0, T.n_tiles, P.ntiles, gs, pv);
+      part_value<NR>(T, p, K, gs, pv);
 #ifdef LRB_STAMP3
       if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
 #endif
@@ -484,8 +531,10 @@ __device__ __forceinline__ SplitBody<NR, Load, Apply> split_body(Load&& l, Apply
 
 // Tile loop of one phase, then the team barrier with the fused reduction.
 // INL: local part descriptors come from the kernel parameter (T.lp).
+// ntv: the streaming kernel's tile vectors for this (elementwise) phase, 0
+// for SpMV phases — it fixes the reduction tree's units (pack_factor).
 template <int NR, bool INL, class Body>
-__device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&& body) {
+__device__ __forceinline__ void team_phase(const TeamDev& T, double* red, int ntv, Body&& body) {
   extern __shared__ double wsm[];   // [tiles of this block][kGroups][kMaxRed]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tl = 0;
@@ -518,14 +567,14 @@ __device__ __forceinline__ void team_phase(const TeamDev& T, double* red, Body&&
     for (int g = 1; g < kGroups; ++g) s = __dadd_rn(s, wsm[(t * kGroups + g) * kMaxRed + j]);
     T.partials[j * T.n_tiles + tile_of(T, t)] = s;
   }
-  team_sync<NR, kRedLanes / kTPB>(T, red);
+  team_sync<NR>(T, red, ntv ? pack_factor(T, ntv) : 1);
 }
 
 // SpMV phase: body(P, i, acc, floc) with floc(c) = vecf(P, c) for local columns.
 template <int NR, bool INL, class VecF, class Body>
 __device__ __forceinline__ void team_phase_spmv(const TeamDev& T, double* red, VecF&& vecf,
                                                 Body&& body) {
-  team_phase<NR, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[NR]) {
+  team_phase<NR, INL>(T, red, 0, [&](const PartDev& P, int64_t i, double (&acc)[NR]) {
     body(P, i, acc, [&](int64_t c) { return vecf(P, c); });
   });
 }
@@ -551,7 +600,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
   // phase 0: x = 0, r = b, partial b.b (and r.z)
-  team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+  team_phase<2, INL>(T, red, JAC ? 2 : 1, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
     const double b = P.b[i];
     P.x[i] = 0.0;
     P.r[i] = b;
@@ -625,9 +674,9 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
           }
         });
 #if LRB_SPLITB
-    team_phase<2, INL>(T, red, phase_b);
+    team_phase<2, INL>(T, red, JAC ? 5 : 4, phase_b);
 #else
-    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, JAC ? 5 : 4, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       phase_b.apply(P, i, phase_b.load(P, i), acc);
     });
 #endif
@@ -677,7 +726,7 @@ template <bool INL>
 __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   double red[2];
-  team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+  team_phase<1, INL>(T, red, 1, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
     const double b = P.b[i];
     P.x[i] = 0.0;
     P.r[i] = b;
@@ -705,7 +754,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __g
     const bool first = (it == 1);
     if (!first) beta = __dmul_rn(rho / rho_prev, alpha / omega);
     // ---- phase 1
-    team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+    team_phase<1, INL>(T, red, 0, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
       auto pnew = [&](const PartDev& Q, int64_t j) -> double {
         const double r = Q.r[j];
         if (first) return r;
@@ -728,7 +777,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __g
     }
     alpha = rho / rv;
     // ---- phase 2
-    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, 0, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       auto sval = [&](const PartDev& Q, int64_t j) -> double {
         const double v = pa ? Q.v1[j] : Q.v0[j];
         return __dsub_rn(Q.r[j], __dmul_rn(alpha, v));
@@ -743,7 +792,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __g
     if (team_failed(T)) break;
     omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
     // ---- phase 3
-    team_phase<2, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, 5, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       const double p = (pa ? P.p1 : P.p0)[i];
       const double s = P.s[i];
       const double x = __dadd_rn(__dadd_rn(P.x[i], __dmul_rn(alpha, p)), __dmul_rn(omega, s));
@@ -760,7 +809,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __g
     const double rec = sqrt(rr) / bnorm;
     if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
     if (rec <= T.tol || it % 10 == 0) {
-      team_phase<1, INL>(T, red, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
+      team_phase<1, INL>(T, red, 0, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
         const double ax =
             row_spmv(P, parts, i, [](const PartDev& Q, int64_t j) { return Q.x[j]; });
         const double d = __dsub_rn(P.b[i], ax);

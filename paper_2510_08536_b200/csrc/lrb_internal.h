@@ -184,9 +184,10 @@ struct TeamDev {
   long long* prof_cta;      // per-CTA wait-cycle counters (nullable, streaming solvers)
   int32_t* prof_n;
   int32_t prof_cap;
-  int32_t pad2_;
-  int32_t stage_bytes;      // streaming solvers: bytes of one shared-memory stage
-  int32_t n_stages;         //   and ring depth (stream.cuh); 0 for the classic kernels
+  int32_t lane_fast;        // CTA c computes reduction lane c itself (kernels.cuh: canonical tree)
+  int32_t stage_bytes;      // streaming solvers: bytes of one shared-memory stage (classic: the
+  int32_t n_stages;         //   streaming geometry, for the tree's units) and ring depth (stream.cuh)
+  double* lane_vals;        // [local parts][kLanes][kMaxRed] lane values (lane_fast)
   double tol;
   long long timeout_ns;
   PartDev lp[kInlineParts];  // local parts [part_begin, part_end) when they fit

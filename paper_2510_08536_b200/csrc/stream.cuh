@@ -52,16 +52,20 @@ static_assert(kTile == kTPB * kRPT,
 #endif
 constexpr int kIssuers = LRB_ISSUERS;             // producer warps (alternate stages)
 static_assert(kIssuers == 1 || kIssuers == kTeams, "one issuer, or one per consumer team");
-constexpr int kStreamThreads = kConsumers + 32 * kIssuers;
-constexpr int kVecTileBytes = kTile * 8;          // one vector's rows of a tile
+// One CTA per SM; 19 warps put 5 on some SM sub-partitions, so a thread
+// gets at most 96 registers (16384 per sub-partition).
+#define LRB_STREAM_BOUNDS __launch_bounds__(kStreamThreads, 1)
+// + one reducer warp: sums each stage's tile partials in stage order (the
+// CTA's reduction lane, kernels.cuh) off the consumers' path
+constexpr int kReducer = kConsumers + 32 * kIssuers;
+constexpr int kStreamThreads = kReducer + 32;
 #ifndef LRB_MAX_STAGES
 #define LRB_MAX_STAGES (kTile <= 256 ? 6 : 4)
 #endif
 constexpr int kStreamMaxStages = LRB_MAX_STAGES;
-constexpr int kMaxPack = 4;                       // tiles per stage in elementwise phases
-constexpr int kSlotRing = 2 * kStreamMaxStages;   // group-sum slots (see consume_phase)
+constexpr int kSlotRing = 8;                      // group-sum slots (a power of two)
+static_assert((kSlotRing & (kSlotRing - 1)) == 0, "group-sum ring is a power of two");
 constexpr int kSlotNR = 4;                        // reductions a group-sum slot holds
-constexpr int kConsumerBar = 1;                   // named barrier of the consumer warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,9 +86,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 #ifndef LRB_WAIT_HINT_NS
 #define LRB_WAIT_HINT_NS 1000000
 #endif
+template <bool HINT = true>
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
   uint32_t ok;
-  if constexpr (LRB_WAIT_HINT_NS > 0) {
+  if constexpr (HINT && LRB_WAIT_HINT_NS > 0) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
@@ -104,11 +109,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
 // Spin on an mbarrier phase.  A ring that never completes is a bug, not a
 // slow peer: after timeout_ns the kernel traps (a clean launch error instead
 // of a hung device).
+template <bool HINT = true>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, long long timeout_ns) {
-  if (mbar_try_wait(b, parity)) return;
+  if (mbar_try_wait<HINT>(b, parity)) return;
   const long long t0 = global_ns();
   for (unsigned k = 1;; ++k) {
-    if (mbar_try_wait(b, parity)) return;
+    if (mbar_try_wait<HINT>(b, parity)) return;
     if ((k & 15u) == 0 && global_ns() - t0 > timeout_ns) __trap();
   }
 }
@@ -142,15 +148,13 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync %0, %1;" ::"n"(kConsumerBar), "n"(kConsumers) : "memory");
-}
 
 // Diagnostic counters per CTA (build with -DLRB_PROF=1; lrb_team_profile_counters):
 // [phase kind (0 init, 1 A, 2 B, 3 C)][what]: 0 consumer thread 0 waiting for
 // data, 1 end-of-phase consumer barrier, 2 issuer 0 waiting for a free stage,
 // 3 team barrier (thread 0, arrival -> release), 4 thread 0 row bodies,
-// 5 thread 0 group reduce + park, 6 thread 0 tile sums, 7 issuer 0 issuing.
+// 5 thread 0 group reduce + park, 6 thread 0 waiting for its group-sum slot,
+// 7 issuer 0 issuing.
 #ifndef LRB_PROF
 #define LRB_PROF 0
 #endif
@@ -162,6 +166,8 @@ struct StreamSmem {
   char* stages;        // n_stages * stage_bytes
   uint64_t* full;      // [kStreamMaxStages][kTeams]
   uint64_t* empty;     // [kStreamMaxStages][kTeams]
+  uint64_t* reduced;   // [kSlotRing] group-sum slot summed by the reducer (count 1)
+  uint64_t* parked;    // [kSlotRing] group sums of the slot's stage parked (count kTeamWarps)
   double* wsum;        // [kSlotRing][kMaxPack][kGroups][kSlotNR] group sums awaiting their tile sum
   unsigned long long* cnt;   // [kCnt]
 };
@@ -173,12 +179,14 @@ __device__ __forceinline__ StreamSmem stream_smem(const TeamDev& T) {
   char* tail = dsm + size_t(T.n_stages) * T.stage_bytes;
   S.full = reinterpret_cast<uint64_t*>(tail);
   S.empty = S.full + kStreamMaxStages * kTeams;
-  S.wsum = reinterpret_cast<double*>(S.empty + kStreamMaxStages * kTeams);
+  S.reduced = S.empty + kStreamMaxStages * kTeams;
+  S.parked = S.reduced + kSlotRing;
+  S.wsum = reinterpret_cast<double*>(S.parked + kSlotRing);
   S.cnt = reinterpret_cast<unsigned long long*>(S.wsum + size_t(kSlotRing) * kMaxPack * kGroups * kSlotNR);
   return S;
 }
 __host__ __device__ constexpr size_t stream_smem_bytes(int stage_bytes, int n_stages) {
-  return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * kTeams * 8 +
+  return size_t(stage_bytes) * n_stages + 2 * kStreamMaxStages * kTeams * 8 + 2 * kSlotRing * 8 +
          size_t(kSlotRing) * kMaxPack * kGroups * kSlotNR * 8 + kCnt * 8;
 }
 
@@ -200,11 +208,6 @@ struct Spec {
 // phases); the CTA's stage count.
 __device__ __forceinline__ int stage_count(int64_t units) {
   return int64_t(blockIdx.x) < units ? int((units - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
-}
-// Packing factor of an elementwise phase with ntv vectors.
-__device__ __forceinline__ int pack_factor(const TeamDev& T, int ntv) {
-  const int k = T.stage_bytes / (kHdrBytes + ntv * kVecTileBytes);
-  return k < 1 ? 1 : (k > kMaxPack ? kMaxPack : k);
 }
 // Ring position of the CTA's global stage number G (G = gseq + phase-local
 // stage; identical in every thread).  Stage G lives in slot G % n_stages and
@@ -247,6 +250,17 @@ __device__ __forceinline__ RingPos ring_pos(int G, const Ring& R) {
   }
   const int slot = G - qs * R.ns, team = G & (kTeams - 1);
   return RingPos{slot, team, slot * kTeams + team, unsigned(qL & 1)};
+}
+// Group-sum slot of stage G: slot G % kSlotRing and the parity of this use of
+// the slot's parked / reduced barriers.  Consumers refill a slot only after
+// the reducer freed its previous use, and the reducer waits on `parked` (not
+// on the ring's empty barriers), so neither side can see a stale phase.
+struct WPos {
+  int slot;
+  unsigned parity;
+};
+__device__ __forceinline__ WPos wsum_pos(int G) {
+  return WPos{G % kSlotRing, unsigned((G / kSlotRing) & 1)};
 }
 // First phase-local stage k of this CTA with (gseq + k) % m == r.
 __device__ __forceinline__ int first_stage(int gseq, int r, int m) {
@@ -693,34 +707,11 @@ struct VecView {
 // ---------------------------------------------------------------------------
 // Consumers: phase loop and deferred tile sums
 // ---------------------------------------------------------------------------
-// Tile sums of stage k (slot k % kSlotRing): group g's sum of its tile j was
-// parked at wsum[slot][j][g]; the designated warp adds the 16 group sums in
-// group order (the canonical tile tree) into T.partials[reduction][tile].
-template <int NR>
-__device__ __forceinline__ void sum_stage(const TeamDev& T, const StreamSmem& S, int k, int64_t tile0,
-                                          int cnt, int warp_sel, int n_sel, int my_warp) {
-  const int lane = threadIdx.x & 31;
-  const int sl = k % kSlotRing;
-  for (int j = 0; j < cnt; ++j) {
-    if (my_warp == (warp_sel + j) % n_sel && lane < NR) {
-      const double* w = S.wsum + (size_t(sl * kMaxPack + j) * kGroups) * kSlotNR;
-      double sum = w[lane];
-#pragma unroll
-      for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * kSlotNR + lane]);
-      T.partials[lane * T.n_tiles + tile0 + j] = sum;
-    }
-  }
-}
-
 // Team tm consumes stages k = tm, tm + 2, ...; per tile each thread computes
 // rows t and t + kTPB (body(P, H, st, V, lr, acc)), butterfly-reduces each into
 // its group (warp w of the team: groups w and w + 8) and parks the group sums
-// in the stage's slot.  No per-tile barrier: a warp that starts stage k knows
-// (through the ring: the producer refilled that slot only after stage
-// k - n_stages was released) that every group sum of stage k - n_stages is
-// written, and a warp of its team sums that stage; the last n_stages stages
-// are summed after one barrier at the end of the phase.  Slots are reused
-// after kSlotRing = 2 * max stages stages, beyond the fastest warp's lead.
+// in the stage's group-sum slot, then releases the stage.  No per-tile
+// barrier and no tile sums here: the reducer warp sums the parked groups.
 template <int NR, bool INL, bool ELEM, class Body>
 __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem& S, int gseq, int kind,
                                               int ntv, Body&& body) {
@@ -729,33 +720,28 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
   const int tm = warp / kTeamWarps;             // team
   const int wt = warp - tm * kTeamWarps;        // warp within the team
   const int tt = int(threadIdx.x) - tm * kTeamThreads;
-  const int ns = T.n_stages;
-  const Ring R = make_ring(ns);
+  const Ring R = make_ring(T.n_stages);
   const int64_t G = gridDim.x;
   const int K = ELEM ? pack_factor(T, ntv) : 1;
   const int64_t n_tiles = T.n_tiles;
   const int count = stage_count(ELEM ? (n_tiles + K - 1) / K : n_tiles);
-  auto first_tile = [&](int k) -> int64_t { return (int64_t(blockIdx.x) + int64_t(k) * G) * K; };
-  auto tiles_in = [&](int k) -> int {
-    const int64_t t0 = first_tile(k);
-    return int(n_tiles - t0 < K ? n_tiles - t0 : K);
-  };
   for (int k = first_stage(gseq, tm, kTeams); k < count; k += kTeams) {
-    const RingPos rp = ring_pos(gseq + k, R);
+    const int Gk = gseq + k;
+    const RingPos rp = ring_pos(Gk, R);
     const char* st0 = S.stages + size_t(rp.slot) * T.stage_bytes;
     {
       const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       mbar_wait(S.full + rp.bar, rp.parity, T.timeout_ns);
       if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
     }
-    if (k >= ns) {
+    const WPos wp = wsum_pos(Gk);
+    if (Gk >= kSlotRing) {   // the slot's previous stage must be summed
       const long long c2 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      const int kd = k - ns;
-      sum_stage<NR>(T, S, kd, first_tile(kd), tiles_in(kd), (kd * kMaxPack) % kTeamWarps, kTeamWarps, wt);
+      mbar_wait(S.reduced + wp.slot, wp.parity ^ 1u, T.timeout_ns);
       if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 6] += clock64() - c2;
     }
-    const int cnt = tiles_in(k);
-    const int sl = k % kSlotRing;
+    const int64_t t0 = (int64_t(blockIdx.x) + int64_t(k) * G) * K;
+    const int cnt = int(n_tiles - t0 < K ? n_tiles - t0 : K);
     for (int j = 0; j < cnt; ++j) {
       // SpMV stages hold one tile at st0; packed elementwise stages hold cnt
       // headers, then each vector's cnt tiles (produce_elementwise)
@@ -773,7 +759,7 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
         if (!(LRB_NOCOMPUTE && !ELEM)) body(P, H, st, V, tt + m * kTPB, acc[m]);
       }
       const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-      double* ws = S.wsum + size_t(sl * kMaxPack + j) * kGroups * kSlotNR;
+      double* ws = S.wsum + size_t(wp.slot * kMaxPack + j) * kGroups * kSlotNR;
 #pragma unroll
       for (int m = 0; m < kRPT; ++m) {
         group_reduce<NR>(acc[m]);
@@ -788,13 +774,52 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(S.empty + rp.bar);   // group sums written before the release
+    if (lane == 0) {
+      mbar_arrive(S.parked + wp.slot);   // group sums written before both arrivals
+      mbar_arrive(S.empty + rp.bar);
+    }
   }
-  const long long c1 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-  consumer_bar();
-  if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 1] += clock64() - c1;
-  for (int kd = (count - ns > 0 ? count - ns : 0); kd < count; ++kd)
-    sum_stage<NR>(T, S, kd, first_tile(kd), tiles_in(kd), (kd * kMaxPack) % kGroups, kGroups, warp);
+}
+
+#ifndef LRB_REDUCER_HINT   // reducer waits without the suspend hint (prompt wake-up)
+#define LRB_REDUCER_HINT 0
+#endif
+// Reducer warp: for every stage of the phase, in stage order, wait until its
+// group sums are parked (8 warps arrive on the slot's `parked` barrier), add
+// each tile's 16 group sums in group
+// order (the canonical tile tree) and free the group-sum slot.  Lane q < NR
+// owns reduction q and keeps the CTA's lane value: with T.lane_fast this CTA
+// IS reduction lane blockIdx.x (kernels.cuh), and its tiles arrive in
+// ascending order, so the running sum is that lane's value; otherwise the
+// tile partials go to T.partials for the last CTA.
+template <int NR, bool ELEM>
+__device__ __forceinline__ void reduce_phase(const TeamDev& T, const StreamSmem& S, int gseq, int ntv) {
+  const int lane = threadIdx.x & 31;
+  const int K = ELEM ? pack_factor(T, ntv) : 1;
+  const int64_t n_tiles = T.n_tiles;
+  const int count = stage_count(ELEM ? (n_tiles + K - 1) / K : n_tiles);
+  const bool fast = lanes_by_cta(T, n_tiles, K);   // single part: its tiles are the device's
+  double lacc = 0.0;
+  for (int k = 0; k < count; ++k) {
+    const int Gk = gseq + k;
+    const WPos wp = wsum_pos(Gk);
+    mbar_wait<LRB_REDUCER_HINT>(S.parked + wp.slot, wp.parity, T.timeout_ns);
+    const int64_t t0 = (int64_t(blockIdx.x) + int64_t(k) * gridDim.x) * K;
+    const int cnt = int(n_tiles - t0 < K ? n_tiles - t0 : K);
+    if (lane < NR) {
+      for (int j = 0; j < cnt; ++j) {
+        const double* w = S.wsum + (size_t(wp.slot * kMaxPack + j) * kGroups) * kSlotNR;
+        double sum = w[lane];
+#pragma unroll
+        for (int g = 1; g < kGroups; ++g) sum = __dadd_rn(sum, w[g * kSlotNR + lane]);
+        if (!fast) T.partials[lane * n_tiles + t0 + j] = sum;
+        lacc = __dadd_rn(lacc, sum);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(S.reduced + wp.slot);
+  }
+  if (fast && lane < NR) T.lane_vals[size_t(blockIdx.x) * kMaxRed + lane] = lacc;
 }
 
 __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& S) {
@@ -802,6 +827,10 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
     for (int b = 0; b < T.n_stages * kTeams; ++b) {
       mbar_init(S.full + b, 1);
       mbar_init(S.empty + b, kTeamWarps);
+    }
+    for (int b = 0; b < kSlotRing; ++b) {
+      mbar_init(S.reduced + b, 1);
+      mbar_init(S.parked + b, kTeamWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -816,7 +845,9 @@ template <int NR, bool INL, bool ELEM, class SpecF, class Body>
 __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, int& gseq, double* red,
                                              int kind, SpecF&& spec_of, Body&& body) {
   const int ntv = ELEM ? spec_of(part_of(T, T.part_begin, INL)).ntv : 0;
-  if (threadIdx.x >= kConsumers) {
+  if (threadIdx.x >= kReducer) {
+    reduce_phase<NR, ELEM>(T, S, gseq, ntv);
+  } else if (threadIdx.x >= kConsumers) {
     fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
     if constexpr (ELEM)
       produce_elementwise<INL>(T, S, gseq, kind, spec_of);
@@ -827,9 +858,9 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
   }
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-  team_sync<NR, kRedLanes / kConsumers>(T, red);
-  if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
   const int K = ELEM ? pack_factor(T, ntv) : 1;
+  team_sync<NR>(T, red, K);
+  if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
   gseq += stage_count(ELEM ? (T.n_tiles + K - 1) / K : T.n_tiles);
 }
 
@@ -846,7 +877,7 @@ __device__ __forceinline__ void stream_flush_counters(const TeamDev& T, const St
 // B = {x, r update, r.r (r.z)}, C = {|b - A x|^2}.
 // ---------------------------------------------------------------------------
 template <bool JAC, bool INL>
-__global__ void __launch_bounds__(kStreamThreads, 1)
+__global__ void LRB_STREAM_BOUNDS
     team_cg_stream_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   const StreamSmem S = stream_smem(T);
@@ -1025,7 +1056,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 // rhat.r;  check: |b - A x|^2.  p and v are double-buffered.
 // ---------------------------------------------------------------------------
 template <bool INL>
-__global__ void __launch_bounds__(kStreamThreads, 1)
+__global__ void LRB_STREAM_BOUNDS
     team_bicgstab_stream_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   const StreamSmem S = stream_smem(T);
@@ -1229,7 +1260,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 // Buffers: x, p = p0; r in {r, rhat}; w in {v0, v1}; s in {s, t}.
 // ---------------------------------------------------------------------------
 template <bool INL>
-__global__ void __launch_bounds__(kStreamThreads, 1)
+__global__ void LRB_STREAM_BOUNDS
     team_pcg1_stream_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
   const StreamSmem S = stream_smem(T);

@@ -87,7 +87,7 @@ def main():
         if cnt.size:
             # mean over CTAs, in us at the sampled SM clock, per phase kind
             mhz = float(os.environ.get("LRB_SM_MHZ", "1965"))
-            names = ("data_wait", "end_bar", "stage_wait", "team_bar", "body", "reduce", "tile_sums",
+            names = ("data_wait", "end_bar", "stage_wait", "team_bar", "body", "reduce", "slot_wait",
                      "issue")
             out["waits_us"] = {kind: {nm: round(float(cnt[:, ki, wi].mean()) / mhz, 1)
                                       for wi, nm in enumerate(names)}
