@@ -70,7 +70,11 @@ def main():
     ap.add_argument("--workload", default="c3")
     args = ap.parse_args()
     lines = [f"# ncu summary `{args.tag}`", ""]
-    step = json.load(open(args.step_json)) if args.step_json else None
+    step = None
+    if args.step_json:   # the JSON line among ncu's own stdout lines
+        for line in open(args.step_json):
+            if line.startswith("{"):
+                step = json.loads(line)
     if step:
         lines += [f"Profiled timestep: step {step['step']}, {step['iterations']} PCG iterations, "
                   f"{step['checks']} true-residual checks; n={step['n']}, nnz={step['nnz']}, "
