@@ -8,9 +8,9 @@ sm_100a CUDA + C++ behind a C ABI, include/ldurepart_b200.h); PyTorch only
 owns device and pinned host memory.  No CPU fallback exists.
 """
 
-from .core import (CooMatrix, DeviceCooMatrix, DistributedCooMatrix, InterfaceBlock, LduMatrix,
-                   PartitionMap, coo_from_entries, gpu_owner, ldu_to_coo, make_partition_map,
-                   validate_ldu)
+from .core import (MM_HEADER, CooMatrix, DeviceCooMatrix, DistributedCooMatrix, InterfaceBlock,
+                   LduMatrix, PartitionMap, coo_from_entries, gpu_owner, ldu_to_coo,
+                   make_partition_map, read_matrix_market, validate_ldu, write_matrix_market)
 from .cavity import (StructuredGrid, SubdomainMesh, assemble_poisson, build_grid,
                      decompose_slab, perturb_coefficients, perturb_diag_into)
 from .transport import (CAT_DEVICE_DIRECT, CAT_DEVICE_STAGED, CAT_RANK, CommGroup,
@@ -26,3 +26,4 @@ from .update import (PackedCoefficients, PatternDriftError, TRANSFER_MODES, appl
                      pack_coefficients, transfer_coefficients, update)
 
 __version__ = "0.1.0"
+from .verify import gather_global, read_curves_csv, write_curves_csv  # noqa: E402

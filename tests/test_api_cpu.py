@@ -182,3 +182,55 @@ def test_random_systems_scatter_is_a_value_preserving_bijection(chunk):
             lo, hi = pm.gpu_range(k)
             want = {key: v for key, v in values.items() if lo <= key[0] < hi}
             assert got == want
+
+
+# ------------------------------------------------ wire formats
+def test_matrix_market_round_trip_and_text(tmp_path):
+    c = lrb.coo_from_entries(3, 4, [2, 0, 0, 1], [3, 1, 0, 2], [0.1, -1.0, 6.0, 1e-300])
+    path = tmp_path / "m.mtx"
+    lrb.write_matrix_market(c, path)
+    text = path.read_text().splitlines()
+    assert text[0] == lrb.MM_HEADER == "%%MatrixMarket matrix coordinate real general"
+    assert text[1] == "3 4 4"
+    # 1-based, row-major, 17 significant digits (the reference's export layout)
+    assert text[2:] == ["1 1 6", "1 2 -1", "2 3 1e-300",
+                        "3 4 0.10000000000000001"]
+    back = lrb.read_matrix_market(path)
+    assert (back.n_rows, back.n_cols) == (3, 4)
+    np.testing.assert_array_equal(back.rows, c.rows)
+    np.testing.assert_array_equal(back.cols, c.cols)
+    np.testing.assert_array_equal(back.vals, c.vals)   # %.17g round-trips every double
+
+
+def test_matrix_market_random_round_trip(tmp_path):
+    rng = np.random.default_rng(11)
+    pm, per_rank, values = random_system(rng)
+    n = pm.total_cells
+    keys = sorted(values)
+    c = lrb.coo_from_entries(n, n, [k[0] for k in keys], [k[1] for k in keys],
+                             [values[k] for k in keys])
+    lrb.write_matrix_market(c, tmp_path / "r.mtx", block=7)
+    back = lrb.read_matrix_market(tmp_path / "r.mtx")
+    np.testing.assert_array_equal(back.vals, c.vals)
+    np.testing.assert_array_equal(back.cols, c.cols)
+
+
+def test_matrix_market_errors(tmp_path):
+    (tmp_path / "a.mtx").write_text("hello\n")
+    with pytest.raises(ValueError, match="not a Matrix Market file"):
+        lrb.read_matrix_market(tmp_path / "a.mtx")
+    (tmp_path / "b.mtx").write_text("%%MatrixMarket matrix array real general\n1 1\n1\n")
+    with pytest.raises(ValueError, match="unsupported Matrix Market header"):
+        lrb.read_matrix_market(tmp_path / "b.mtx")
+
+
+def test_curves_csv(tmp_path):
+    path = tmp_path / "c.csv"
+    lrb.write_curves_csv(path, [(4, 0.5, 0.2), (1, 2.0, 0.2), (2, 1.0, 0.2)])
+    assert path.read_text().splitlines()[0] == "n,t_as,t_ls"
+    n, t_as, t_ls = lrb.read_curves_csv(path)
+    assert n.tolist() == [1, 2, 4] and t_as.tolist() == [2.0, 1.0, 0.5] and t_ls.tolist() == [0.2] * 3
+    with pytest.raises(ValueError, match="n = 1"):
+        lrb.write_curves_csv(path, [(2, 1.0, 1.0)])
+    with pytest.raises(ValueError, match="positive"):
+        lrb.write_curves_csv(path, [(1, 0.0, 1.0)])
