@@ -206,3 +206,26 @@ def test_pcg1_matches_pcg(dims, n_cpu, alpha, dev_ranks):
     # deterministic run to run
     assert rc.iterations == rb.iterations and np.array_equal(hc, hb)
     assert all(np.array_equal(a, b) for a, b in zip(xc, holder["pcg1"][0]))
+
+
+@pytest.mark.parametrize("stages", ["2", "3"])
+def test_stream_ring_depth_variants(stages, monkeypatch):
+    """Two- and three-stage rings (L = lcm(stages, 2) = 2 / 6 ring periods
+    against 8 group-sum slots): the reducer hand-off, the lane tree and the
+    stage bookkeeping stay bit-identical to the classic kernels."""
+    monkeypatch.setenv("LRB_STREAM_STAGES", stages)
+    _, asm, pm = cavity_case((80, 80, 80), 4, 4)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 4), "direct")
+        parts = s.comm.allgather(s.part) if s.is_owner else None
+        if s.is_owner and s.comm.group_rank == 0:
+            from paper_2510_08536_b200.device import Team
+            assert Team(parts).kernel_info("pcg")["stages"] == int(stages)
+            holder["r"] = _compare(parts, ("cg", "pcg"), 1e-9, 400)
+        return None
+
+    lrb.run_world(4, program)
+    assert holder["r"]["pcg"].converged
