@@ -565,8 +565,8 @@ constexpr int64_t kStaticSmemMargin = 4096;
 static int64_t method_need(int method, int64_t base, int64_t wb) {
   const int64_t tv = kVecTileBytes;
   switch (method) {
-    case LRB_METHOD_BICGSTAB:   // phase 1: r, p_old, v_old windows + rhat tile
-      return base + std::max({3 * wb + tv, 2 * wb, wb + tv});
+    case LRB_METHOD_BICGSTAB:   // phase 1: r, u = p_old - omega v_old windows + rhat tile
+      return base + std::max({2 * wb + tv, 2 * wb, wb + tv});
     case LRB_METHOD_PCG1:       // fused phase: r, dinv, w, s_old windows + p, x tiles
       return base + std::max({4 * wb + 2 * tv, 2 * wb, wb + tv});
     default:                    // CG / PCG: z, p_old windows; check: x window + b tile

@@ -791,8 +791,8 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __g
     });
     if (team_failed(T)) break;
     omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
-    // ---- phase 3
-    team_phase<2, INL>(T, red, 5, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    // ---- phase 3 (6: the streaming kernel's tile vectors, incl. u = p - omega v)
+    team_phase<2, INL>(T, red, 6, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       const double p = (pa ? P.p1 : P.p0)[i];
       const double s = P.s[i];
       const double x = __dadd_rn(__dadd_rn(P.x[i], __dmul_rn(alpha, p)), __dmul_rn(omega, s));

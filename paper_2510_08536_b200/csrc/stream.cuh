@@ -199,7 +199,7 @@ struct Spec {
   int nwv;                 // window vectors (0: elementwise phase)
   int ntv;                 // tile vectors
   const double* wv[4];
-  const double* tv[5];
+  const double* tv[6];
 };
 
 
@@ -400,7 +400,7 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
                      unsigned(cur.wl[w] * 8), full, pol_vec);
       d += size_t(sp.nwv) * cur.wtot * 8;
 #pragma unroll
-      for (int v = 0; v < 5; ++v)
+      for (int v = 0; v < 6; ++v)
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + cur.row0, vec_bytes, full, pol_vec);
     }
     if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 7] += clock64() - ci;
@@ -465,7 +465,7 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
     if (merged) {
       const Spec sp = spec_of(part_of(T, part[0], INL));
 #pragma unroll
-      for (int v = 0; v < 5; ++v)
+      for (int v = 0; v < 6; ++v)
         if (v < sp.ntv) bulk_g2s(vbase + v * vstride, sp.tv[v] + row0[0], span, full, pol_vec);
     } else {
 #pragma unroll
@@ -474,7 +474,7 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
           const Spec sp = spec_of(part_of(T, part[j], INL));
           const unsigned vb = unsigned((rows[j] * 8 + 15) & ~15);
 #pragma unroll
-          for (int v = 0; v < 5; ++v)
+          for (int v = 0; v < 6; ++v)
             if (v < sp.ntv)
               bulk_g2s(vbase + v * vstride + size_t(j) * kVecTileBytes, sp.tv[v] + row0[j], vb, full, pol_vec);
         }
@@ -490,9 +490,8 @@ __device__ __forceinline__ void produce_elementwise(const TeamDev& T, const Stre
 // Staged operands.  Every SpMV phase reads its operand at staged window
 // position q through one of these (reference rounding, no FMA):
 //   Win1   x = w0[q]
-//   PnewCG p_new = z + beta * p_old            (w0 = z, w1 = p_old)
+//   PnewCG p_new = z + beta * p_old            (w0 = z, w1 = p_old; BiCGStab: r + beta * u)
 //   SBiCG  s = r - alpha * v                   (w0 = r, w1 = v)
-//   PBiCG  p_new = r + beta * (p_old - omega * v_old)   (w0 = r, w1 = p_old, w2 = v_old)
 struct Win1 {
   const double* __restrict__ w0;
   __device__ __forceinline__ double operator()(int q) const { return w0[q]; }
@@ -508,15 +507,6 @@ struct SBiCG {
   const double* __restrict__ w1;
   double alpha;
   __device__ __forceinline__ double operator()(int q) const { return __dsub_rn(w0[q], __dmul_rn(alpha, w1[q])); }
-};
-struct PBiCG {
-  const double* __restrict__ w0;
-  const double* __restrict__ w1;
-  const double* __restrict__ w2;
-  double beta, omega;
-  __device__ __forceinline__ double operator()(int q) const {
-    return __dadd_rn(w0[q], __dmul_rn(beta, __dsub_rn(w1[q], __dmul_rn(omega, w2[q]))));
-  }
 };
 
 // Single-reduction PCG operand: u_new = dinv * (r - alpha * (w + beta * s_old))
@@ -1095,28 +1085,29 @@ __global__ void LRB_STREAM_BOUNDS
     const bool first = (it == 1);
     if (!first) beta = __dmul_rn(rho / rho_prev, alpha / omega);
     // ---- phase 1: p_new, v = A p_new, rhat.v
+    // u = p_old - omega v_old was stored over p_old by the previous phase 3
+    // (same rounding as forming it here), so p_new needs two windows, not three
     auto pnew_g = [&](const PartDev& Q, int64_t j) -> double {
       const double r = Q.r[j];
       if (first) return r;
-      const double po = pa ? Q.p1[j] : Q.p0[j];
-      const double vo = pa ? Q.v1[j] : Q.v0[j];
-      return __dadd_rn(r, __dmul_rn(beta, __dsub_rn(po, __dmul_rn(omega, vo))));
+      const double u = pa ? Q.p1[j] : Q.p0[j];
+      return __dadd_rn(r, __dmul_rn(beta, u));
     };
     stream_phase<1, INL, false>(
         T, S, gseq, red, 1,
         [&](const PartDev& P) {
-          return first ? Spec{1, 1, {P.r, nullptr, nullptr}, {P.rhat}}
-                       : Spec{3, 1, {P.r, pa ? P.p1 : P.p0, pa ? P.v1 : P.v0}, {P.rhat}};
+          return first ? Spec{1, 1, {P.r, nullptr}, {P.rhat}}
+                       : Spec{2, 1, {P.r, pa ? P.p1 : P.p0}, {P.rhat}};
         },
         [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
           double* vout = pa ? P.v0 : P.v1;
           if (H.tma) {
-            const StagedTile t = staged_tile(st, H, first ? 1 : 3);
+            const StagedTile t = staged_tile(st, H, first ? 1 : 2);
             const int sl = lr >> 5;
             const Slots slot = slice_slots(st, H, sl);
             const Win1 r1{t.w(0)};
-            const PBiCG pn{t.w(0), t.w(1), t.w(2), beta, omega};
+            const PnewCG pn{t.w(0), t.w(1), beta};   // r + beta u
             double pi;
             const double vi = first ? staged_row(P, parts, H, t, slot, lr, r1, pnew_g, pi)
                                     : staged_row(P, parts, H, t, slot, lr, pn, pnew_g, pi);
@@ -1177,11 +1168,13 @@ __global__ void LRB_STREAM_BOUNDS
         });
     if (team_failed(T)) break;
     omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
-    // ---- phase 3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r
+    // ---- phase 3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r;
+    //      u = p - omega v over p (the next phase 1's operand)
     stream_phase<2, INL, true>(
         T, S, gseq, red, 2,
         [&](const PartDev& P) {
-          return Spec{0, 5, {nullptr, nullptr}, {pa ? P.p1 : P.p0, P.s, P.x, P.t, P.rhat}};
+          return Spec{0, 6, {nullptr, nullptr},
+                      {pa ? P.p1 : P.p0, P.s, P.x, P.t, P.rhat, pa ? P.v1 : P.v0}};
         },
         [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
           if (lr >= H.rows) return;
@@ -1189,6 +1182,7 @@ __global__ void LRB_STREAM_BOUNDS
           const double s = V[1][lr];
           const double x = __dadd_rn(__dadd_rn(V[2][lr], __dmul_rn(alpha, V[0][lr])), __dmul_rn(omega, s));
           const double r = __dsub_rn(s, __dmul_rn(omega, V[3][lr]));
+          (pa ? P.p1 : P.p0)[i] = __dsub_rn(V[0][lr], __dmul_rn(omega, V[5][lr]));
           P.x[i] = x;
           P.r[i] = r;
           acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
