@@ -132,6 +132,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+#ifndef LRB_DIAG_NOPLANE
+#define LRB_DIAG_NOPLANE 0
+#endif
 #ifndef LRB_ISSUER_PREFETCH
 #define LRB_ISSUER_PREFETCH 1
 #endif
@@ -385,8 +388,16 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       bulk_g2s(st, hdrs + tile, kHdrBytes, full, pol_vec);
     } else {
       // record (header | slot tables | masks), values, windows, tile vectors
+#if LRB_DIAG_NOPLANE   // diagnostics (timing only, wrong results): no +-plane windows
+      const bool skip_pl = cur.nw == 3;
+      mbar_expect_tx(full, kRecBytes + unsigned(cur.vbytes) +
+                               unsigned(sp.nwv * (skip_pl ? cur.wl[1] : cur.wtot) * 8) +
+                               unsigned(sp.ntv) * vec_bytes);
+#else
+      constexpr bool skip_pl = false;
       mbar_expect_tx(full, kRecBytes + unsigned(cur.vbytes) + unsigned(sp.nwv * cur.wtot * 8) +
                                unsigned(sp.ntv) * vec_bytes);
+#endif
       bulk_g2s(st, recs + tile, kRecBytes, full, pol_vec);
       char* d = st + kRecBytes;
       bulk_g2s(d, P.val + cur.e0, unsigned(cur.vbytes), full, pol_stream);
@@ -395,7 +406,7 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       for (int v = 0; v < 4; ++v)
 #pragma unroll
         for (int w = 0; w < kMaxWin; ++w)
-          if (v < sp.nwv && w < cur.nw)
+          if (v < sp.nwv && w < cur.nw && !(skip_pl && w != 1))
             bulk_g2s(d + (size_t(v) * cur.wtot + cur.woff[w]) * 8, sp.wv[v] + cur.wa[w],
                      unsigned(cur.wl[w] * 8), full, pol_vec);
       d += size_t(sp.nwv) * cur.wtot * 8;
