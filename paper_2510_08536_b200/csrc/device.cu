@@ -569,8 +569,8 @@ static int64_t method_need(int method, int64_t base, int64_t wb) {
       return base + std::max({2 * wb + tv, 2 * wb, wb + tv});
     case LRB_METHOD_PCG1:       // fused phase: r, dinv, w, s_old windows + p, x tiles
       return base + std::max({4 * wb + 2 * tv, 2 * wb, wb + tv});
-    default:                    // CG / PCG: z, p_old windows; check: x window + b tile
-      return base + std::max(2 * wb, wb + tv);
+    default:                    // CG / PCG: z, p_old windows (+ x tile); check: x (+ p) windows + b tile
+      return base + (LRB_LAZY_X ? 2 * wb + tv : std::max(2 * wb, wb + tv));
   }
 }
 
@@ -919,7 +919,10 @@ static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int6
   h.wtot = int32_t(wtot);
   if (h.nw <= 0) return 0;
   const int64_t base = kRecBytes + h.vbytes;
-  return std::max(base + 2 * wtot * 8, base + wtot * 8 + kVecTileBytes);
+  // CG / PCG: z, p_old windows (+ the x tile when its update is pending,
+  // LRB_LAZY_X); the check phase: x (+ p) windows + the b tile
+  return LRB_LAZY_X ? base + 2 * wtot * 8 + kVecTileBytes
+                    : std::max(base + 2 * wtot * 8, base + wtot * 8 + kVecTileBytes);
 }
 
 // Largest stage any phase needs for a stageable tile of this device's parts,

@@ -236,6 +236,17 @@ constexpr int kLanes = LRB_LANES;
 constexpr int kLaneGroups = (kLanes + 31) / 32;
 constexpr int kVecTileBytes = kTile * 8;   // one vector's rows of a tile
 constexpr int kMaxPack = 4;                // tiles per stage in elementwise phases
+// CG's x update: LRB_LAZY_X = 1 moves it out of phase B into the next SpMV
+// phase (stream.cuh); the streaming phase B then stages 3 (PCG) / 2 (CG)
+// tile vectors instead of 5 / 4 — the tree's units follow (pack_factor).
+// Off by default: -8 B/row per iteration, but phase A pays nearly what B
+// saves and the check phases get a window more (C3 -0.5%, C1/C2 +5%;
+// profiles/r1_experiments.md).
+#ifndef LRB_LAZY_X
+#define LRB_LAZY_X 0
+#endif
+template <bool JAC>
+constexpr int kCgBVecs = LRB_LAZY_X ? (JAC ? 3 : 2) : (JAC ? 5 : 4);
 
 // Packing factor of an elementwise phase with ntv vectors (the streaming
 // kernels' stage geometry; the classic kernels use it for the tree's units).
@@ -674,9 +685,9 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
           }
         });
 #if LRB_SPLITB
-    team_phase<2, INL>(T, red, JAC ? 5 : 4, phase_b);
+    team_phase<2, INL>(T, red, kCgBVecs<JAC>, phase_b);
 #else
-    team_phase<2, INL>(T, red, JAC ? 5 : 4, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
+    team_phase<2, INL>(T, red, kCgBVecs<JAC>, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
       phase_b.apply(P, i, phase_b.load(P, i), acc);
     });
 #endif

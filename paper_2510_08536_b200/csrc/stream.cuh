@@ -921,6 +921,12 @@ __global__ void LRB_STREAM_BOUNDS
   double beta = 0.0, res = 1.0;
   int pa = 0;
   bool first = true, converged = false;
+  // lazy x (LRB_LAZY_X): phase B leaves x += step * p pending; the next
+  // phase A applies it to its own rows (it stages p_old anyway), phase C
+  // forms x + step * p on the fly, a last elementwise pass applies it at exit.
+  // Same operations, same rounding as updating x in B: 8 B/row less traffic.
+  bool pend = false;
+  double step_x = 0.0;
   int it = 0;
   for (it = 1; it <= T.max_iter; ++it) {
     // ---- phase A: p_new = z + beta p_old (staged windows), q = A p_new, p.q
@@ -935,7 +941,8 @@ __global__ void LRB_STREAM_BOUNDS
         [&](const PartDev& P) {
           const double* z = JAC ? P.s : P.r;
           const double* po = pa ? P.p1 : P.p0;
-          return first ? Spec{1, 0, {z, nullptr}, {}} : Spec{2, 0, {z, po}, {}};
+          return first ? Spec{1, 0, {z, nullptr}, {}}
+                       : (pend ? Spec{2, 1, {z, po}, {P.x}} : Spec{2, 0, {z, po}, {}});
         },
         [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
           double* pout = pa ? P.p0 : P.p1;
@@ -953,6 +960,10 @@ __global__ void LRB_STREAM_BOUNDS
               pout[i] = pi;
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
+              if (pend) {   // the pending x update: p_old of the row itself
+                const double po = t.w(1)[diag_pos(H, slot, sl, i)];
+                P.x[i] = __dadd_rn(t.tail(0)[lr], __dmul_rn(step_x, po));
+              }
             }
           } else if (lr < H.rows) {
             const int64_t i = H.row0 + lr;
@@ -961,8 +972,10 @@ __global__ void LRB_STREAM_BOUNDS
             pout[i] = pi;
             P.q[i] = qi;
             acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
+            if (pend) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(step_x, (pa ? P.p1 : P.p0)[i]));
           }
         });
+    pend = false;
     if (team_failed(T)) break;
 #if LRB_ABENCH
     // diagnostics build: phase A alone, back to back (timing only)
@@ -979,11 +992,33 @@ __global__ void LRB_STREAM_BOUNDS
     }
     const double step = rho / pq;
     pa ^= 1;
+#if LRB_LAZY_X
+    // ---- phase B: r -= step q, r.r (, z = dinv r, r.z); x += step p pending
+    stream_phase<2, INL, true>(
+        T, S, gseq, red, 2,
+        [&](const PartDev& P) {
+          return Spec{0, kCgBVecs<JAC>, {nullptr, nullptr}, {P.r, P.q, JAC ? P.dinv : nullptr}};
+        },
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
+          if (lr >= H.rows) return;
+          const int64_t i = H.row0 + lr;
+          const double r = __dsub_rn(V[0][lr], __dmul_rn(step, V[1][lr]));
+          P.r[i] = r;
+          acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
+          if (JAC) {
+            const double z = __dmul_rn(V[2][lr], r);
+            P.s[i] = z;
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
+          }
+        });
+    pend = true;
+    step_x = step;
+#else
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
     stream_phase<2, INL, true>(
         T, S, gseq, red, 2,
         [&](const PartDev& P) {
-          return Spec{0, JAC ? 5 : 4, {nullptr, nullptr},
+          return Spec{0, kCgBVecs<JAC>, {nullptr, nullptr},
                       {pa ? P.p1 : P.p0, P.x, P.r, P.q, JAC ? P.dinv : nullptr}};
         },
         [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[2]) {
@@ -1000,22 +1035,30 @@ __global__ void LRB_STREAM_BOUNDS
             acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
           }
         });
+#endif
     if (team_failed(T)) break;
     const double rr_new = red[0];
     const double rho_new = JAC ? red[1] : rr_new;
     const double rec = sqrt(rr_new) / bnorm;
     if (lead && T.hist && it <= T.hist_cap) T.hist[it - 1] = rec;
     if (rec <= T.tol || it % 10 == 0) {
-      // ---- phase C: true residual |b - A x|
-      auto xg = [](const PartDev& Q, int64_t j) -> double { return Q.x[j]; };
+      // ---- phase C: true residual |b - A x| (x with its pending update formed
+      //      on the fly: x is read by neighbours here, so it is not written)
+      auto xg = [&](const PartDev& Q, int64_t j) -> double {
+        return pend ? __dadd_rn(Q.x[j], __dmul_rn(step_x, (pa ? Q.p1 : Q.p0)[j])) : Q.x[j];
+      };
       stream_phase<1, INL, false>(
-          T, S, gseq, red, 3, [&](const PartDev& P) { return Spec{1, 1, {P.x, nullptr}, {P.b}}; },
+          T, S, gseq, red, 3,
+          [&](const PartDev& P) {
+            return pend ? Spec{2, 1, {P.x, pa ? P.p1 : P.p0}, {P.b}} : Spec{1, 1, {P.x, nullptr}, {P.b}};
+          },
           [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr,
               double (&acc)[1]) {
             if (H.tma) {
-              const StagedTile t = staged_tile(st, H, 1);
+              const StagedTile t = staged_tile(st, H, pend ? 2 : 1);
               const Slots slot = slice_slots(st, H, lr >> 5);
-              const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+              const double ax = pend ? staged_row(P, parts, H, t, slot, lr, PnewCG{t.w(0), t.w(1), step_x}, xg)
+                                     : staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
@@ -1039,6 +1082,16 @@ __global__ void LRB_STREAM_BOUNDS
     beta = rho_new / rho;
     rho = rho_new;
     first = false;
+  }
+  if (pend && !team_failed(T)) {
+    // ---- the last pending x update (x is the solver's output)
+    stream_phase<1, INL, true>(
+        T, S, gseq, red, 2,
+        [&](const PartDev& P) { return Spec{0, 2, {nullptr, nullptr}, {P.x, pa ? P.p1 : P.p0}}; },
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&)[1]) {
+          if (lr >= H.rows) return;
+          P.x[H.row0 + lr] = __dadd_rn(V[0][lr], __dmul_rn(step_x, V[1][lr]));
+        });
   }
   stream_flush_counters(T, S);
   if (lead) {

@@ -76,6 +76,7 @@ def main():
             _, rep, hist = team.solve(args.method, bs, TOL, MAX_ITER, want_x=False, hist_cap=MAX_ITER)
             ts = team.phase_times_ns().reshape(-1, 2)   # (last arrival, release) per phase
             kinds = phase_kinds(hist, rep.iterations, TOL)
+            kinds += ["X"] * (len(ts) - len(kinds))   # the lazy-x final update phase
             for q in range(1, len(ts)):
                 k = kinds[q]
                 per.setdefault(k, []).append((ts[q, 1] - ts[q - 1, 1]) / 1e3)
