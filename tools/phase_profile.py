@@ -38,21 +38,24 @@ def main():
     ap.add_argument("--step", type=int, default=6)
     ap.add_argument("--method", default="pcg")
     ap.add_argument("--repeat", type=int, default=3)
+    ap.add_argument("--alpha", type=int, default=None, help="ranks per GPU part (default: all -> 1 part)")
     args = ap.parse_args()
     import paper_2510_08536_b200 as lrb
     from paper_2510_08536_b200.device import Team
     prob = Problem(args.n, args.ranks, range(args.ranks))
-    pm = lrb.make_partition_map(prob.cells, args.ranks)
-    holder = {}
+    pm = lrb.make_partition_map(prob.cells, args.alpha or args.ranks)
+    holder = {"keep": []}
 
     def program(ctx):
         s = lrb.repartition(*prob.base[ctx.rank], pm, ctx)
         lrb.update(s, *prob.produce(ctx.rank, args.step), "direct")
         if s.is_owner:
             s.part.sync()
-            holder["parts"] = [s.part]
-            holder["plan"] = s.part.plan
-            holder["keep"] = s
+            parts = s.comm.allgather(s.part)   # every owner part on this one GPU
+            holder["keep"].append(s)
+            if s.comm.group_rank == 0:
+                holder["parts"] = parts
+                holder["plan"] = parts[0].plan
         return None
 
     lrb.run_world(args.ranks, program)
