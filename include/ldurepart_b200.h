@@ -89,7 +89,7 @@ int lrb_plan_export_halo(const lrb_plan* plan, int32_t* hpart, int32_t* hidx);
 /* The device layout (SELL-32) as built on the host: slice_ptr[n_slices+1],
  * col/src[sell_entries] (col >= n: halo slot col-n; -1: padding), dpos[n]. */
 int lrb_plan_export_sell(const lrb_plan* plan, int64_t* slice_ptr, int32_t* col, int32_t* src,
-                         int8_t* dpos);
+                         int16_t* dpos);
 void lrb_plan_destroy(lrb_plan* plan);
 
 /* ------------------------------------------------------------------------
@@ -217,7 +217,11 @@ typedef struct lrb_report {
 
 /* Krylov solve (cg_solve, solver.py:100-147; PCG/BiCGStab per SURVEY App. A).
  * b_host/x_host per part (nullable: b already on device / leave x on device).
- * hist (nullable) receives the recurrence residual per iteration. */
+ * hist (nullable) receives the recurrence residual per iteration.
+ * LRB_ETIMEOUT: a cross-device barrier waited longer than
+ * LRB_BARRIER_TIMEOUT_S (default 20 s) for a peer; the team is then poisoned
+ * (its devices' barrier epochs disagree) and every later solve on it fails
+ * with LRB_ETIMEOUT until it is destroyed and recreated. */
 int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
                    double* const* x_host, double tol, int32_t max_iter, lrb_report* rep,
                    double* hist, int32_t hist_cap);

@@ -73,7 +73,7 @@ static Layout layout_of(const Plan& P) {
   L.tile_win = take(4 * int64_t(P.tile_win.size()));
   L.col = take(4 * E);
   L.src = take(4 * E);
-  L.dpos = take(P.n);
+  L.dpos = take(2 * P.n);
   L.hpart = take(4 * h);
   L.hidx = take(4 * h);
   L.val = take(8 * E);
@@ -186,7 +186,7 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   D.tile_win = reinterpret_cast<const int32_t*>(base + L.tile_win);
   D.col = reinterpret_cast<const int32_t*>(base + L.col);
   D.src = reinterpret_cast<const int32_t*>(base + L.src);
-  D.dpos = reinterpret_cast<const int8_t*>(base + L.dpos);
+  D.dpos = reinterpret_cast<const int16_t*>(base + L.dpos);
   D.hpart = reinterpret_cast<const int32_t*>(base + L.hpart);
   D.hidx = reinterpret_cast<const int32_t*>(base + L.hidx);
   D.val = reinterpret_cast<double*>(base + L.val);
@@ -256,7 +256,7 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
     LRB_CUDA(cudaMemcpyAsync(base + L.col, P.sell_col.data(), 4 * E, cudaMemcpyHostToDevice, st));
     LRB_CUDA(cudaMemcpyAsync(base + L.src, P.sell_src.data(), 4 * E, cudaMemcpyHostToDevice, st));
   }
-  if (P.n) LRB_CUDA(cudaMemcpyAsync(base + L.dpos, P.dpos.data(), P.n, cudaMemcpyHostToDevice, st));
+  if (P.n) LRB_CUDA(cudaMemcpyAsync(base + L.dpos, P.dpos.data(), 2 * P.n, cudaMemcpyHostToDevice, st));
   if (D.n_halo) {
     LRB_CUDA(cudaMemcpyAsync(base + L.hpart, P.hpart.data(), 4 * D.n_halo, cudaMemcpyHostToDevice, st));
     LRB_CUDA(cudaMemcpyAsync(base + L.hidx, P.hidx.data(), 4 * D.n_halo, cudaMemcpyHostToDevice, st));
@@ -609,6 +609,9 @@ struct lrb_team {
   std::vector<int> dev_of_part;
   std::vector<void*> ipc_opened;    // peer allocations opened via CUDA IPC
   int ipc_dev = -1;
+  // set when a cross-device barrier timed out: the devices' barrier epochs and
+  // flags no longer agree, so a later solve could pair stale part values
+  bool poisoned = false;
   std::mutex mu;
 };
 
@@ -1522,6 +1525,11 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
       return LRB_EVALUE;
     }
   std::lock_guard<std::mutex> lk(team->mu);
+  if (team->poisoned) {
+    set_error("team poisoned: a cross-device barrier timed out in an earlier solve; "
+              "destroy and recreate the team");
+    return LRB_ETIMEOUT;
+  }
   const bool multi = team->devs.size() > 1;
   for (auto& D : team->devs) {
     int rc = team_prologue(team, D);
@@ -1612,6 +1620,7 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     return LRB_ENOTPD;
   }
   if (so.status == LRB_ETIMEOUT) {
+    team->poisoned = true;
     set_error("team barrier timed out (a device of the team did not arrive)");
     return LRB_ETIMEOUT;
   }

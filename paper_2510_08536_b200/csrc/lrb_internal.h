@@ -58,7 +58,7 @@ struct PartDev {
   const int32_t* tile_win;    // [ntiles_part * kWinStride] staging windows
   const int32_t* col;         // [E]
   const int32_t* src;         // [E] scatter inverse (buffer position or -1)
-  const int8_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
+  const int16_t* dpos;         // [n] slot k of the diagonal in the row, -1 if none
   const int32_t* hpart;       // [n_halo] team part that owns halo slot
   const int32_t* hidx;        // [n_halo] row of that part
   double* val;                // [E]
@@ -209,7 +209,7 @@ struct Plan {
   int64_t n_slices = 0;
   std::vector<int64_t> slice_ptr;
   std::vector<int32_t> sell_col, sell_src;
-  std::vector<int8_t> dpos;
+  std::vector<int16_t> dpos;
   std::vector<int32_t> slice_pat;           // [n_slices]
   std::vector<int32_t> pat_off;             // [n_pat * kPatW]
   std::vector<uint16_t> rmask;              // [n] occupied slots of a pattern row

@@ -431,6 +431,7 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
   P.rmask.assign(n, 0);
   P.loc_sell.assign(nnz_l, 0);
   P.nl_sell.assign(nnz_n, 0);
+  std::atomic<bool> dpos_overflow{false};
   parallel_for(n, n_threads, [&](int64_t r0, int64_t r1) {
     std::vector<int32_t> ro;
     for (int64_t r = r0; r < r1; ++r) {
@@ -450,7 +451,10 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
           P.sell_col[e] = P.loc_col[j];
           P.sell_src[e] = P.loc_src[j];
           P.loc_sell[j] = int32_t(e);
-          if (P.loc_col[j] == r && slot < 127) P.dpos[r] = int8_t(slot);
+          if (P.loc_col[j] == r) {
+            if (slot > 32767) dpos_overflow = true;
+            else P.dpos[r] = int16_t(slot);
+          }
         } else {
           const int64_t j = P.nl_ptr[r] + (k - nloc);
           P.sell_col[e] = int32_t(n + P.nl_col[j]);
@@ -462,6 +466,10 @@ int build(Plan& P, int64_t total, int64_t lo, int64_t hi, int64_t n_buf,
       if (pid >= 0) P.rmask[r] = uint16_t(mask);
     }
   });
+  if (dpos_overflow) {   // Jacobi reads the diagonal through an int16 slot index
+    set_error("row too long: diagonal beyond SELL slot 32767");
+    return LRB_EVALUE;
+  }
   build_tile_windows(P);
   return LRB_OK;
 }
@@ -621,7 +629,7 @@ extern "C" int lrb_plan_export_halo(const lrb_plan* plan, int32_t* hpart, int32_
 }
 
 extern "C" int lrb_plan_export_sell(const lrb_plan* plan, int64_t* slice_ptr, int32_t* col,
-                                    int32_t* src, int8_t* dpos) {
+                                    int32_t* src, int16_t* dpos) {
   if (!plan) {
     lrb::set_error("lrb_plan_export_sell: null plan");
     return LRB_EVALUE;

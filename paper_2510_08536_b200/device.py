@@ -84,7 +84,7 @@ class Plan:
         sp = np.empty(self.n_slices + 1, np.int64)
         col = np.empty(self.sell_entries, np.int32)
         src = np.empty(self.sell_entries, np.int32)
-        dpos = np.empty(self.n, np.int8)
+        dpos = np.empty(self.n, np.int16)
         N.check(N.lrb_plan_export_sell(self.h, N.ptr(sp), N.ptr(col), N.ptr(src), N.ptr(dpos)))
         return sp, col, src, dpos
 

@@ -79,8 +79,9 @@ class DistributedOwner:
     """This process's owner part(s) and source ranks: create once, then
     update + solve per timestep through the C ABI with host buffers."""
 
-    def __init__(self, layout: ProcessLayout, problems, group=None, n_threads=0):
-        """``problems``: {cpu_rank: (LduMatrix, [InterfaceBlock])} for this process."""
+    def __init__(self, layout: ProcessLayout, problems, group=None, n_threads=0, solve=True):
+        """``problems``: {cpu_rank: (LduMatrix, [InterfaceBlock])} for this process.
+        ``solve=False``: update-only owner (no solve team is connected)."""
         self.layout = layout
         pm = layout.pm
         self.fingerprints = {r: sparsity_fingerprint(*problems[r]) for r in layout.cpu_ranks}
@@ -92,7 +93,7 @@ class DistributedOwner:
             plan = _owner_plan(srcs, pm, k)
             self.plans.append(plan)
             self.parts.append(DevicePart(plan, dev))
-        self.team = Team.across_processes(self.parts, layout.part_begin, pm.n_gpu, layout.rank,
+        self.team = None if not solve else Team.across_processes(self.parts, layout.part_begin, pm.n_gpu, layout.rank,
                                           layout.world, lambda b: allgather_bytes(b, group))
         self.pool = ThreadPoolExecutor(max(1, len(layout.cpu_ranks)))
         self.update(problems, "direct")
@@ -118,7 +119,13 @@ class DistributedOwner:
             else:
                 p.update_staged_from_stage()
 
-    def solve(self, method, b_local, tol, max_iter, hist_cap=0):
+    def solve(self, method, b_local, tol, max_iter, hist_cap=0, group=None):
+        """One solve of the whole team.  A process barrier first bounds the launch
+        skew between processes, so the kernels' cross-device barrier timeout
+        (LRB_BARRIER_TIMEOUT_S) measures a missing peer, not a late launch."""
+        import torch.distributed as dist
+        if self.layout.world > 1:
+            dist.barrier(group)
         bs = [None] * self.layout.pm.n_gpu
         for i, k in enumerate(self.layout.parts):
             bs[k] = b_local[i] if b_local is not None else None

@@ -16,7 +16,7 @@ from .core import DeviceCooMatrix, DistributedCooMatrix, InterfaceBlock, LduMatr
     PartitionMap, gpu_owner
 from .device import DevicePart, Plan, Team, device_count
 from .solver import HaloPlan, build_halo_plan
-from .transport import CAT_DEVICE_DIRECT, CommGroup, DeviceBuffer, RankContext, split_active
+from .transport import CAT_DEVICE_DIRECT, CAT_RANK, CommGroup, DeviceBuffer, RankContext, split_active
 
 
 @dataclass(frozen=True)
@@ -241,6 +241,10 @@ def repartition(m: LduMatrix, ifaces, pm: PartitionMap, ctx: RankContext) -> Rep
     k = gpu_owner(ctx.rank, pm)
     owner = pm.alpha * k
     ctx.send(owner, src)
+    # bytes of the reference's pattern message (4 int64 arrays + row_lo/hi,
+    # repart.py:185-187); _Source itself travels by reference
+    n_loc = m.n_cells + 2 * m.n_faces
+    ctx.world._account(CAT_RANK, 16 * n_loc + 16 * (src.n_entries - n_loc) + 16, messages=0)
     comm = split_active(ctx, pm)
     system = RepartitionedSystem(ctx=ctx, pm=pm, comm=comm, update_pattern=up,
                                  fingerprint=sparsity_fingerprint(m, ifaces))
@@ -260,7 +264,7 @@ def repartition(m: LduMatrix, ifaces, pm: PartitionMap, ctx: RankContext) -> Rep
     # initial fill is always direct (repart.py:349-350)
     pieces = _pieces(m, ifaces)
     system.part.update_segment(system.segment, pieces)
-    ctx.world.traffic[CAT_DEVICE_DIRECT].bytes_sent += 8 * src.n_entries
+    ctx.world._account(CAT_DEVICE_DIRECT, 8 + 8 * src.n_entries)
     _group_barrier(ctx, pm, "create")
     if system.is_owner:
         system.device.transfer_count += pm.alpha

@@ -113,3 +113,40 @@ def spmv_inputs(name, total):
     if seed is None:
         return None
     return np.random.default_rng(seed).normal(size=(3, total))
+
+
+HIST_RTOL = 1e-10
+
+
+def ref_history(log, iterations, tol):
+    """sqrt(rr)/|b| per iteration from the reference's allreduce log
+    ``[b.b, (p.q, r.r, [|b-Ax|^2 when rec<=tol or it%10==0])...]``."""
+    bb = log[0]
+    out, i = [], 1
+    for it in range(1, iterations + 1):
+        rec = np.sqrt(log[i + 1]) / np.sqrt(bb)
+        out.append(rec)
+        i += 2
+        if rec <= tol or it % 10 == 0:
+            i += 1
+    return np.array(out)
+
+
+def history_ok(ours, ref, rtol=HIST_RTOL, floor=1e-12):
+    """Recurrence residuals within rtol relative; below the rounding floor
+    (tiny systems reach exact convergence, e.g. the 8-cell chain) both must
+    simply be negligible."""
+    n = min(len(ours), len(ref))
+    a, r = np.asarray(ours[:n]), np.asarray(ref[:n])
+    ok = (np.abs(a - r) <= rtol * r) | ((r < floor) & (a < floor))
+    return bool(ok.all()), n
+
+
+LARGE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@lru_cache(maxsize=None)
+def large(name):
+    """tests/golden/golden_large_<name>.npz (tests/golden/make_golden_large.py)."""
+    with np.load(os.path.join(LARGE_DIR, f"golden_large_{name}.npz")) as z:
+        return {k: z[k] for k in z.files}

@@ -69,3 +69,25 @@ def sell_spmv(plan, vals_sell, x_local, x_halo):
             acc = np.where(live, acc + prod, acc)
         y[rows] = acc
     return y
+
+
+_PINNED = []
+
+
+def pinned_ldu(m, ifs):
+    """(LduMatrix, [InterfaceBlock], diag) whose value arrays live in pinned host
+    memory, as bench.py's producer builds them (the zero-copy update branch)."""
+    import torch
+
+    def pin(a):
+        t = torch.empty(len(a), dtype=torch.float64, pin_memory=True)
+        _PINNED.append(t)
+        out = t.numpy()
+        out[:] = a
+        return out
+
+    diag = pin(m.diag)
+    mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, diag, pin(m.lower_val),
+                       pin(m.upper_val))
+    ifp = [lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote, pin(b.values)) for b in ifs]
+    return mm, ifp, diag

@@ -1,0 +1,169 @@
+"""GPU parity at the BASELINE sizes, through the exact bench path.
+
+Goldens: tests/golden/golden_large_<case>.npz, made by running the REFERENCE
+itself (tests/golden/make_golden_large.py): sha256 digests of its integer
+artifacts and scattered values, and the allreduce logs of its cg_solve.
+
+* C3  200^3, 8 ranks -> 1 part (the bench headline): the bench's producer
+  (perturb_diag_into into PINNED arrays -> the zero-copy direct update branch),
+  staged mode and the reference generator's pageable output; value digests at
+  timesteps 2 and 3, every integer digest, and the Jacobi-PCG (bench method)
+  and CG recurrence-residual histories of timesteps 2..21 within 1e-10 of the
+  reference's CG, iterations within +-1.
+* C3  200^3, 16 ranks -> 8 parts on one GPU (alpha 2): multi-part team.
+* C5  200^3, 128 ranks -> 8 parts (alpha 16): digests of every owner.
+* C4  300^3, 16 ranks -> 1 part: value digest, CG/PCG histories of steps 2, 3.
+
+Anchors: update.py:105-112 (values), solver.py:100-147 (CG).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2510_08536_b200 as lrb
+from golden_cases import digest, history_ok, large, ref_history
+from helpers_b200 import cavity_case, pinned_ldu
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6
+
+
+def _int_digests(system):
+    mat = system.matrix
+    return {"local_rows": digest(mat.local.rows), "local_cols": digest(mat.local.cols),
+            "nl_rows": digest(mat.non_local.rows), "nl_cols": digest(mat.non_local.cols),
+            "to_local": digest(system.scatter.to_local.astype(np.bool_)),
+            "index": digest(system.scatter.index.astype(np.int64))}
+
+
+def _val_digests(system):
+    return (digest(system.matrix.local.vals), digest(system.matrix.non_local.vals))
+
+
+def _check_ints(g, k, got, full=True):
+    assert np.array_equal(got["recv_offsets"], g[f"k{k}__recv_offsets"])
+    assert np.array_equal(got["halo_cols"], g[f"k{k}__halo_cols"])
+    if full:
+        for key, d in got["ints"].items():
+            assert d == str(g[f"k{k}__{key}__sha256"]), (k, key)
+
+
+def _check_history(g, k, step, rep, exact_iters=False):
+    log = g[f"k{k}__cg_{step}_log"]
+    it_ref = int(g[f"k{k}__cg_{step}_rep"][0])
+    ref = ref_history(log, it_ref, TOL)
+    assert abs(rep.iterations - it_ref) <= 1, (step, rep.iterations, it_ref)
+    if exact_iters:
+        assert rep.iterations == it_ref, (step, rep.iterations, it_ref)
+    ok, n = history_ok(rep.history, ref)
+    assert ok and n >= min(len(ref), rep.iterations) - 1, (step, rep.history, ref)
+    assert rep.converged
+
+
+def _run(N, n_cpu, alpha, steps, mode="direct", producer="pinned", solve_steps=(),
+         methods=("pcg",), want_ints=True):
+    _, assembled, pm = cavity_case((N, N, N), n_cpu, alpha)
+    live = [pinned_ldu(m, ifs) for m, ifs in assembled] if producer == "pinned" else None
+
+    def program(ctx):
+        m, ifs = assembled[ctx.rank]
+        system = lrb.repartition(m, ifs, pm, ctx)
+        out = {}
+        if system.is_owner:
+            out["recv_offsets"] = system.update_pattern.recv_offsets[system.gpu_rank].copy()
+            out["halo_cols"] = np.asarray(system.matrix.halo_cols).copy()
+            if want_ints:
+                out["ints"] = _int_digests(system)
+        for s in sorted(set(steps) | set(solve_steps)):
+            if producer == "pinned":
+                mm, ifp, diag = live[ctx.rank]
+                lrb.perturb_diag_into(m.diag, s, diag)     # the bench's producer
+                lrb.update(system, mm, ifp, mode)
+            else:
+                lrb.update(system, *lrb.perturb_coefficients(m, ifs, s), mode)
+            if not system.is_owner:
+                continue
+            if s in steps:
+                out[f"vals_{s}"] = _val_digests(system)
+            if s in solve_steps:
+                b = np.ones(system.matrix.n_owned)
+                for meth in methods:
+                    _, rep = lrb.cg_solve(system.matrix, system.halo, b, TOL, 2000, system.comm,
+                                          method=meth, history=True)
+                    out[f"{meth}_{s}"] = rep
+        if system.is_owner:
+            out["stats"] = system.part.stats()
+        return out
+
+    res = lrb.run_world(n_cpu, program, timeout=3600)
+    return pm, {k: res[alpha * k] for k in range(pm.n_gpu)}
+
+
+def test_c3_bench_path_pinned_direct():
+    """The headline configuration through the bench's exact update branch:
+    pinned arrays -> zero-copy per-piece H2D + segment scatter."""
+    g = large("c3")
+    pm, owners = _run(200, 8, 8, steps=(2, 3), solve_steps=tuple(range(2, 22)),
+                      methods=("pcg", "cg"))
+    out = owners[0]
+    _check_ints(g, 0, out)
+    for s in (2, 3):
+        assert out[f"vals_{s}"] == (str(g[f"k0__vals_{s}_local__sha256"]),
+                                    str(g[f"k0__vals_{s}_nl__sha256"])), s
+    assert out["stats"]["pageable_pieces"] == 0 and out["stats"]["pinned_pieces"] > 0
+    for s in range(2, 22):
+        _check_history(g, 0, s, out[f"pcg_{s}"])            # bench method vs reference CG
+        _check_history(g, 0, s, out[f"cg_{s}"], exact_iters=True)
+
+
+@pytest.mark.parametrize("mode,producer", [("staged", "pinned"), ("direct", "pageable"),
+                                           ("staged", "pageable")])
+def test_c3_values_other_update_branches(mode, producer):
+    g = large("c3")
+    _, owners = _run(200, 8, 8, steps=(2, 3), mode=mode, producer=producer, want_ints=False)
+    out = owners[0]
+    for s in (2, 3):
+        assert out[f"vals_{s}"] == (str(g[f"k0__vals_{s}_local__sha256"]),
+                                    str(g[f"k0__vals_{s}_nl__sha256"])), (mode, producer, s)
+    if producer == "pageable" and mode == "direct":
+        assert out["stats"]["pageable_pieces"] > 0
+
+
+def test_c3_r16_a2_multipart_team():
+    """8 parts (one per would-be GPU) in one persistent kernel: values and the
+    CG/PCG history of timestep 2 against the reference's 8-owner run."""
+    g = large("c3r16a2")
+    pm, owners = _run(200, 16, 2, steps=(2,), solve_steps=(2,), methods=("pcg", "cg"),
+                      want_ints=False)
+    assert pm.n_gpu == 8
+    for k, out in owners.items():
+        _check_ints(g, k, out, full=False)
+        assert out["vals_2"] == (str(g[f"k{k}__vals_2_local__sha256"]),
+                                 str(g[f"k{k}__vals_2_nl__sha256"])), k
+    _check_history(g, 0, 2, owners[0]["pcg_2"])
+    _check_history(g, 0, 2, owners[0]["cg_2"])
+
+
+@pytest.mark.parametrize("mode", ["direct", "staged"])
+def test_c5_update_only_all_owners(mode):
+    g = large("c5")
+    pm, owners = _run(200, 128, 16, steps=(2, 3), mode=mode, want_ints=(mode == "direct"))
+    assert pm.n_gpu == 8
+    for k, out in owners.items():
+        _check_ints(g, k, out, full=(mode == "direct"))
+        for s in (2, 3):
+            assert out[f"vals_{s}"] == (str(g[f"k{k}__vals_{s}_local__sha256"]),
+                                        str(g[f"k{k}__vals_{s}_nl__sha256"])), (k, s)
+
+
+def test_c4_pressure_values_and_history():
+    g = large("c4")
+    _, owners = _run(300, 16, 16, steps=(2,), solve_steps=(2, 3), methods=("pcg", "cg"),
+                     want_ints=False)
+    out = owners[0]
+    _check_ints(g, 0, out, full=False)
+    assert out["vals_2"] == (str(g["k0__vals_2_local__sha256"]), str(g["k0__vals_2_nl__sha256"]))
+    for s in (2, 3):
+        _check_history(g, 0, s, out[f"pcg_{s}"])
+        _check_history(g, 0, s, out[f"cg_{s}"])

@@ -9,37 +9,14 @@ import numpy as np
 import pytest
 
 import paper_2510_08536_b200 as lrb
-from golden_cases import case_config, case_meta, case_names, get, matches, spmv_inputs
+from golden_cases import (case_config, case_meta, case_names, get, history_ok, matches, ref_history,
+                          spmv_inputs)
 from helpers_b200 import golden_inputs
 
 pytestmark = pytest.mark.gpu
 
 CASES = case_names()
-SMALL = [c for c in CASES if c not in ("c2",)]
-HIST_RTOL = 1e-10
-
-
-def history_ok(ours, ref, rtol=HIST_RTOL, floor=1e-12):
-    """Recurrence residuals within rtol relative; below the rounding floor
-    (tiny systems reach exact convergence, e.g. the 8-cell chain) both must
-    simply be negligible."""
-    n = min(len(ours), len(ref))
-    a, r = np.asarray(ours[:n]), np.asarray(ref[:n])
-    ok = (np.abs(a - r) <= rtol * r) | ((r < floor) & (a < floor))
-    return bool(ok.all()), n
-
-
-def ref_history(log, iterations, tol):
-    """sqrt(rr)/|b| per iteration from the reference's allreduce log."""
-    bb = log[0]
-    out, i = [], 1
-    for it in range(1, iterations + 1):
-        rec = np.sqrt(log[i + 1]) / np.sqrt(bb)
-        out.append(rec)
-        i += 2
-        if rec <= tol or it % 10 == 0:
-            i += 1
-    return np.array(out)
+SMALL = CASES   # every case incl. C2 (100^3, 64 ranks -> 8 parts, value digests)
 
 
 def run_case(name, mode="direct", solve=True, method="cg"):
