@@ -61,6 +61,14 @@ def _check_history(g, k, step, rep, exact_iters=False):
     assert rep.converged
 
 
+def _check_x(g, k, step, x):
+    """Solutions are tolerance-matched: the strided sample and the norm of x
+    against the reference's (same iterations, histories within 1e-10)."""
+    sample, norm = x
+    np.testing.assert_allclose(sample, g[f"k{k}__cg_{step}_x__sample997"], rtol=1e-7)
+    assert abs(norm - float(g[f"k{k}__cg_{step}_x__norm"])) <= 1e-8 * norm
+
+
 def _run(N, n_cpu, alpha, steps, mode="direct", producer="pinned", solve_steps=(),
          methods=("pcg",), want_ints=True):
     _, assembled, pm = cavity_case((N, N, N), n_cpu, alpha)
@@ -75,6 +83,7 @@ def _run(N, n_cpu, alpha, steps, mode="direct", producer="pinned", solve_steps=(
             out["halo_cols"] = np.asarray(system.matrix.halo_cols).copy()
             if want_ints:
                 out["ints"] = _int_digests(system)
+            stats0 = system.part.stats()   # the create path's initial fill is pageable
         for s in sorted(set(steps) | set(solve_steps)):
             if producer == "pinned":
                 mm, ifp, diag = live[ctx.rank]
@@ -89,11 +98,13 @@ def _run(N, n_cpu, alpha, steps, mode="direct", producer="pinned", solve_steps=(
             if s in solve_steps:
                 b = np.ones(system.matrix.n_owned)
                 for meth in methods:
-                    _, rep = lrb.cg_solve(system.matrix, system.halo, b, TOL, 2000, system.comm,
+                    x, rep = lrb.cg_solve(system.matrix, system.halo, b, TOL, 2000, system.comm,
                                           method=meth, history=True)
                     out[f"{meth}_{s}"] = rep
+                    out[f"{meth}_{s}_x"] = (x[::997].copy(), float(np.linalg.norm(x)))
         if system.is_owner:
-            out["stats"] = system.part.stats()
+            st = system.part.stats()
+            out["stats"] = {key: st[key] - stats0[key] for key in st}
         return out
 
     res = lrb.run_world(n_cpu, program, timeout=3600)
@@ -115,6 +126,7 @@ def test_c3_bench_path_pinned_direct():
     for s in range(2, 22):
         _check_history(g, 0, s, out[f"pcg_{s}"])            # bench method vs reference CG
         _check_history(g, 0, s, out[f"cg_{s}"], exact_iters=True)
+        _check_x(g, 0, s, out[f"cg_{s}_x"])
 
 
 @pytest.mark.parametrize("mode,producer", [("staged", "pinned"), ("direct", "pageable"),
@@ -167,3 +179,4 @@ def test_c4_pressure_values_and_history():
     for s in (2, 3):
         _check_history(g, 0, s, out[f"pcg_{s}"])
         _check_history(g, 0, s, out[f"cg_{s}"])
+        _check_x(g, 0, s, out[f"cg_{s}_x"])
