@@ -2,9 +2,10 @@
 
 CG follows the reference solver.py:80-147 operation by operation (ordered
 allreduce in ascending owner rank, transport.py:450-458; true residual every
-10 iterations or when the recurrence residual meets tol).  Jacobi-PCG and
-BiCGStab are not in the reference; they follow SURVEY.md Appendix A with the
-same stopping rule and reduction order.  Every elementwise update is written
+10 iterations or when the recurrence residual meets tol).  Jacobi-PCG,
+BiCGStab and the single-reduction (Chronopoulos-Gear) Jacobi-PCG are not in
+the reference; they follow SURVEY.md Appendix A / §8 f1 with the same
+stopping rule and reduction order.  Every elementwise update is written
 as separate numpy operations so each product/sum is rounded once, exactly as
 the CUDA kernels do (no FMA).  Test infrastructure only.
 """
@@ -195,4 +196,68 @@ def bicgstab(S: DistSystem, bs, tol, max_iter):
             res = rec
         if omega == 0.0 or rho == 0.0:
             break
+    return xs, Report(it, float(res), converged, hist, log)
+
+
+def pcg1(S: DistSystem, bs, tol, max_iter):
+    """Single-reduction Jacobi-PCG (Chronopoulos-Gear).
+
+    CG's iterates with the two reductions of an iteration fused into one:
+    u = M r (M = diag^-1), w = A u, s = A p kept as recurrences,
+      beta = gamma / gamma_prev, eta = delta - beta * (gamma / alpha_prev),
+      alpha = gamma / eta;  p = u + beta p,  s = w + beta s,
+      x += alpha p,  r -= alpha s,  u = M r,  w = A u,
+      (gamma, delta, rho) = (r.u, w.u, r.r)    -- one fused allreduce.
+    Same stopping rule as cg_solve (solver.py:136-142): recurrence residual
+    sqrt(rho)/|b|, true residual when it meets tol or every 10 iterations.
+    eta <= 0 raises like the reference's p.q <= 0 (solver.py:129-130).
+    """
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    log, hist = [], []
+    xs = [np.zeros(len(b)) for b in bs]
+    bb = S.dot(bs, bs)
+    log.append(bb)
+    if bb == 0.0:
+        return xs, Report(0, 0.0, True, hist, log)
+    bnorm = math.sqrt(bb)
+    dinv = S.dinv()
+    rs = [b.astype(np.float64).copy() for b in bs]
+    us = [d * r for d, r in zip(dinv, rs)]
+    ws = S.spmv(us)
+    gamma, delta = S.dot(rs, us), S.dot(ws, us)
+    log += [gamma, delta]
+    gamma_prev = alpha_prev = 1.0
+    ps = ss = None
+    res, converged, it = 1.0, False, 0
+    for it in range(1, max_iter + 1):
+        first = it == 1
+        beta = 0.0 if first else gamma / gamma_prev
+        eta = delta if first else delta - beta * (gamma / alpha_prev)
+        if eta <= 0.0:
+            raise ValueError("cg: matrix is not positive definite")
+        alpha = gamma / eta
+        if first:
+            ps = [u.copy() for u in us]
+            ss = [w.copy() for w in ws]
+        else:
+            ps = [u + beta * p for u, p in zip(us, ps)]
+            ss = [w + beta * s_ for w, s_ in zip(ws, ss)]
+        for x, p in zip(xs, ps):
+            x += alpha * p
+        rs = [r - alpha * s_ for r, s_ in zip(rs, ss)]
+        us = [d * r for d, r in zip(dinv, rs)]
+        ws = S.spmv(us)
+        gamma_prev, alpha_prev = gamma, alpha
+        gamma, delta, rr = S.dot(rs, us), S.dot(ws, us), S.dot(rs, rs)
+        log += [gamma, delta, rr]
+        rec = math.sqrt(rr) / bnorm
+        hist.append(rec)
+        if rec <= tol or it % 10 == 0:
+            res = _true_residual(S, bs, xs, bnorm, log)
+            if res <= tol:
+                converged = True
+                break
+        else:
+            res = rec
     return xs, Report(it, float(res), converged, hist, log)

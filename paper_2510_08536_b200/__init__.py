@@ -19,7 +19,8 @@ from .transport import (CAT_DEVICE_DIRECT, CAT_DEVICE_STAGED, CAT_RANK, CommGrou
 from .solver import (HaloPlan, SolveReport, bicgstab_solve, build_halo_plan, cg_solve,
                      krylov_solve, pcg_solve, spmv)
 from .repart import (RepartitionedSystem, ScatterMap, SparsityPattern, UpdatePattern,
-                     build_scatter_map, build_update_pattern, exchange_patterns,
+                     build_scatter_map, build_update_pattern, dump_scatter, dump_sparsity,
+                     exchange_patterns,
                      extract_sparsity, fuse_patterns, pack_order_pairs, repartition,
                      sparsity_fingerprint)
 from .update import (PackedCoefficients, PatternDriftError, TRANSFER_MODES, apply_scatter,

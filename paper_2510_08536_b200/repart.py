@@ -374,3 +374,22 @@ def build_scatter_map(received, local_pattern, nonlocal_pattern, pm: PartitionMa
             and np.array_equal(nr, nonlocal_pattern[0]) and np.array_equal(nc, nonlocal_pattern[1])):
         raise RuntimeError("scatter map: buffer entries do not match the fused pattern slots")
     return ScatterMap(plan=plan)
+
+
+# ---------------------------------------------------------------------------
+# text dumps for test fixtures (repart.py:357-369): same line formats
+# ---------------------------------------------------------------------------
+def dump_sparsity(sp: SparsityPattern) -> str:
+    """``rows lo hi`` then one ``local r c`` / ``nonlocal r c`` line per entry."""
+    out = [f"rows {sp.row_lo} {sp.row_hi}\n"]
+    for tag, rows, cols in (("local", sp.local_rows, sp.local_cols),
+                            ("nonlocal", sp.nonlocal_rows, sp.nonlocal_cols)):
+        out.extend(f"{tag} {r} {c}\n" for r, c in zip(rows.tolist(), cols.tolist()))
+    return "".join(out)
+
+
+def dump_scatter(sm: ScatterMap) -> str:
+    """One ``b -> local|nonlocal slot`` line per receive-buffer position."""
+    tags = ("nonlocal", "local")
+    return "".join(f"{b} -> {tags[int(t)]} {i}\n"
+                   for b, (t, i) in enumerate(zip(sm.to_local.tolist(), sm.index.tolist())))

@@ -91,3 +91,26 @@ def pinned_ldu(m, ifs):
                        pin(m.upper_val))
     ifp = [lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote, pin(b.values)) for b in ifs]
     return mm, ifp, diag
+
+
+def momentum_ldu(asm, seed=0):
+    """Non-symmetric, diagonally dominant LDU on the cavity addressing:
+    upper -1+eps, lower -1-eps, eps in [0, 0.05), diag 6.5."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for m, ifs in asm:
+        eps_u = 0.05 * rng.random(m.n_faces)
+        eps_l = 0.05 * rng.random(m.n_faces)
+        mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, np.full(m.n_cells, 6.5),
+                           -1.0 - eps_l, -1.0 + eps_u)
+        out.append((mm, ifs))
+    return out
+
+
+def oracle_problems(per_rank):
+    """The same per-rank LDU inputs as oracle RankProblems."""
+    from oracle import cavity as ocav
+    return [ocav.RankProblem(m.n_cells, m.lower_addr, m.upper_addr, m.diag, m.lower_val,
+                             m.upper_val, tuple(ocav.Block(b.neighbor_rank, b.rows, b.cols_remote,
+                                                           b.values) for b in ifs))
+            for m, ifs in per_rank]

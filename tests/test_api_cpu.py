@@ -234,3 +234,22 @@ def test_curves_csv(tmp_path):
         lrb.write_curves_csv(path, [(2, 1.0, 1.0)])
     with pytest.raises(ValueError, match="positive"):
         lrb.write_curves_csv(path, [(1, 0.0, 1.0)])
+
+
+def test_dump_fixtures():
+    """Known answers of the reference's tests/test_repart.py:297-313 (W1 chain,
+    4 ranks, alpha 2): the sparsity dump of rank 1 and the scatter-map dump."""
+    _, _, assembled, pm = chain_setup(4, 8, 2)
+    sp = lrb.extract_sparsity(*assembled[1], pm, 1)
+    assert lrb.dump_sparsity(sp) == ("rows 2 4\n"
+                                     "local 2 2\nlocal 2 3\nlocal 3 2\nlocal 3 3\n"
+                                     "nonlocal 2 1\nnonlocal 3 4\n")
+    received = [lrb.extract_sparsity(*assembled[r], pm, r) for r in (0, 1)]
+    local, nonlocal_ = lrb.fuse_patterns(received, pm, 0)
+    sm = lrb.build_scatter_map(received, local, nonlocal_, pm)
+    lines = lrb.dump_scatter(sm).splitlines()
+    assert len(lines) == 11
+    assert lines[0] == "0 -> local 0" and lines[10] == "10 -> nonlocal 0"
+    for b, line in enumerate(lines):
+        dest = "local" if sm.to_local[b] else "nonlocal"
+        assert line == f"{b} -> {dest} {sm.index[b]}"

@@ -118,6 +118,23 @@ def test_oracle_pcg_matches_reference_cg_on_cavity():
         np.testing.assert_allclose(rep.history[:n], ref_hist[:n], rtol=1e-10)
 
 
+@pytest.mark.parametrize("name", ["c1", "cav12x12x12_r8_a2", "cav7x9x11_r6_a3"])
+def test_oracle_pcg1_matches_reference_cg_on_cavity(name):
+    """The single-reduction restatement (krylov.pcg1) is pinned to
+    the reference's CG: on the uniform-diagonal cavity its recurrence residuals
+    follow the reference's CG history within 1e-10, iterations +-1."""
+    probs, offsets, alpha = problems_of(name)
+    pipe = OraclePipeline(probs, offsets, alpha)
+    for s in (2, 3):
+        pipe.update([cavity.perturb(p, s) for p in probs])
+        _, rep = pipe.solve("pcg1", 1e-6, 2000)
+        it = int(get(name, 0, f"cg_{s}_rep")[0])
+        assert abs(rep.iterations - it) <= 1 and rep.converged
+        ref_hist = _recurrence_history(get(name, 0, f"cg_{s}_log"), it)
+        n = min(len(ref_hist), len(rep.history))
+        np.testing.assert_allclose(rep.history[:n], ref_hist[:n], rtol=1e-10)
+
+
 def _recurrence_history(log, iterations, tol=1e-6):
     """Extract sqrt(rr)/|b| per iteration from a reference allreduce log."""
     bb = log[0]
@@ -146,3 +163,24 @@ def test_oracle_bicgstab_solves_nonsymmetric():
     ys = pipe.system.spmv(xs)
     r = np.concatenate([1 - y for y in ys])
     assert np.linalg.norm(r) / np.sqrt(len(r)) <= 1e-10
+
+
+def test_oracle_bicgstab_dot_order_envelope():
+    """Calibration behind tests/test_gpu_krylov.py BICG_RTOL: BiCGStab's history
+    moves by far more than 1e-10 when only the dot-product order changes
+    (here: owner partition alpha 2 vs 8 at 48^3), unlike CG's."""
+    probs = cavity.cavity_problems((48, 48, 48), 8)
+    rng = np.random.default_rng(0)
+    mom = []
+    for p in probs:
+        eu, el = 0.05 * rng.random(len(p.lower)), 0.05 * rng.random(len(p.lower))
+        mom.append(p._replace(diag=np.full(p.n, 6.5), lval=-1.0 - el, uval=-1.0 + eu))
+    offsets = np.concatenate(([0], np.cumsum([p.n for p in mom])))
+    hs = []
+    for alpha in (2, 8):
+        _, rep = OraclePipeline(mom, offsets, alpha).solve("bicgstab", 1e-6, 2000)
+        assert rep.converged
+        hs.append(np.asarray(rep.history))
+    n = min(map(len, hs))
+    dev = np.max(np.abs(hs[0][:n] - hs[1][:n]) / hs[0][:n])
+    assert 1e-10 < dev < 5e-9, dev
