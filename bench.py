@@ -702,6 +702,7 @@ def run_c4(args):
                 tot = 0.0
                 kms = 0.0
                 alg = 0
+                alg_k = {"scatter": 0, "bicgstab": 0, "pcg": 0}
                 pln = sm.part.plan
                 n, nnz, h = pln.n, pln.nnz_local + pln.nnz_nonlocal, pln.n_halo
                 for part, team, method, rhs in ((sm.part, sm.team, "bicgstab", bs),
@@ -712,6 +713,7 @@ def run_c4(args):
                     part.mark()
                     tot += part.elapsed_ms()
                     alg += 20 * pln.n_buf
+                    alg_k["scatter"] += 20 * pln.n_buf
                     for b in rhs:
                         _, rep, hist = team.solve(method, [b], TOL, MAX_ITER, want_x=False,
                                                   hist_cap=MAX_ITER)
@@ -721,6 +723,7 @@ def run_c4(args):
                         a = (bicgstab_bytes(n, nnz, h, rep.iterations, ck) if method == "bicgstab"
                              else solve_bytes(n, nnz, h, rep.iterations, ck, "pcg"))
                         alg += a
+                        alg_k[method] += a
                         if method == "pcg" and i >= W:
                             rec["press_ms"].append(rep.device_ms)
                             rec["press_alg"].append(a)
@@ -728,6 +731,7 @@ def run_c4(args):
                     rec["value_ms"].append(tot)
                     rec["kernel_ms"].append(kms)
                     rec["alg"].append(alg)
+                    rec.setdefault("alg_k", []).append(alg_k)
             ctx.barrier()
         if r == 0:
             p = sp.part.plan
@@ -772,12 +776,17 @@ def run_c4(args):
         "gpu_launches": int(rec["launches"]),
         "clocks": sampler.summary(),
     }
-    t = traffic_ratio("c4")
-    if t:
-        line["roofline"]["traffic"] = int(t["dram_bytes_per_alg_byte"] *
-                                          line["roofline"]["alg_bytes_per_launch"])
-        line["roofline"]["traffic_note"] = t.get("note")
-        dram = line["roofline"]["traffic"] / (line["roofline"]["kernel_ms"] * 1e-3) / 1e9
+    tb, tp = traffic_ratio("c4_bicgstab"), traffic_ratio("c4_pcg")
+    if tb and tp:
+        # ncu DRAM bytes per algorithmic byte of each solve kernel at 300^3; the
+        # scatters are counted at their algorithmic bytes (DRAM/alg ~1 for a
+        # whole-part launch, profiles/r2_c3_scatter_summary.md)
+        ak = {k: float(np.mean([a[k] for a in rec["alg_k"]])) for k in rec["alg_k"][0]}
+        traffic = (tb["dram_bytes_per_alg_byte"] * ak["bicgstab"] +
+                   tp["dram_bytes_per_alg_byte"] * ak["pcg"] + ak["scatter"])
+        line["roofline"]["traffic"] = int(traffic)
+        line["roofline"]["traffic_note"] = "; ".join([tb.get("note", ""), tp.get("note", "")])
+        dram = traffic / (value * 1e-3) / 1e9
         line["roofline"]["dram_achieved"] = round(dram, 1)
         line["roofline"]["dram_frac"] = round(dram / peak, 4)
     return line

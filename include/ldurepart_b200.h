@@ -226,6 +226,44 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
                    double* const* x_host, double tol, int32_t max_iter, lrb_report* rep,
                    double* hist, int32_t hist_cap);
 
+/* ------------------------------------------------------------------------
+ * Stream-ordered entry points for a GPU-resident caller (the OGL lduMatrix
+ * solver plugin role; SURVEY.md §8(b) lrb_update_h2d /
+ * lrb_krylov).  Nothing here synchronises the host: the work is enqueued
+ * after everything already on the caller's stream, and the caller's stream
+ * is made to wait for it.  lrb_stream_t is cudaStream_t (NULL = the legacy
+ * default stream).
+ * ------------------------------------------------------------------------ */
+typedef struct CUstream_st* lrb_stream_t;
+
+/* Direct update of one source segment (update.py:72-83 + apply_scatter,
+ * update.py:105-112) ordered on `stream`: the pieces (pinned host or device
+ * memory — pageable host memory is rejected with LRB_EVALUE, it cannot be
+ * copied stream-ordered) are copied into segment `seg` of the receive
+ * buffer, then that segment's scatter runs on the same stream.  The pieces
+ * must stay valid until the stream reaches the copy.  The next solve on the
+ * part waits for it. */
+int lrb_update_segment_async(lrb_part* part, int32_t seg, int32_t n_pieces,
+                             const double* const* pieces, const int64_t* piece_len,
+                             lrb_stream_t stream);
+
+/* Krylov solve (cg_solve, solver.py:100-147) ordered on streams[dev_rank]
+ * (streams nullable; a NULL array means each device's team stream with no
+ * caller ordering).  b_dev / x_dev: one DEVICE pointer per team part on the
+ * part's GPU (nullable array: b already in the part / x left in the part).
+ * rep_out (nullable): pinned host or device memory; the report is written
+ * stream-ordered after the solve (device_ms = -1: no host timing).  Status
+ * codes of the solve itself (not positive definite, barrier timeout) land in
+ * rep_out->status.  Single-process teams only. */
+int lrb_team_solve_async(lrb_team* team, int32_t method, const double* const* b_dev,
+                         double* const* x_dev, double tol, int32_t max_iter,
+                         const lrb_stream_t* streams, lrb_report* rep_out);
+
+/* Distributed SpMV y = A x (solver.py:80-97) on device pointers, ordered on
+ * streams[dev_rank] like lrb_team_solve_async.  Single-process teams only. */
+int lrb_team_spmv_async(lrb_team* team, const double* const* x_dev, double* const* y_dev,
+                        const lrb_stream_t* streams);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,9 @@ lrb_team_profile = _sig("lrb_team_profile", C.c_int, P, I32)
 lrb_team_profile_read = _sig("lrb_team_profile_read", C.c_int, P, P, I32)
 lrb_team_profile_counters = _sig("lrb_team_profile_counters", C.c_int, P, I32, P, I32)
 lrb_team_solve = _sig("lrb_team_solve", C.c_int, P, I32, P, P, D, I32, C.POINTER(Report), P, I32)
+lrb_update_segment_async = _sig("lrb_update_segment_async", C.c_int, P, I32, I32, P, P, P)
+lrb_team_solve_async = _sig("lrb_team_solve_async", C.c_int, P, I32, P, P, D, I32, P, P)
+lrb_team_spmv_async = _sig("lrb_team_spmv_async", C.c_int, P, P, P, P)
 
 EXPORTED = [
     "lrb_last_error", "lrb_version", "lrb_device_count", "lrb_launch_count",
@@ -113,6 +116,7 @@ EXPORTED = [
     "lrb_team_spmv", "lrb_team_solve", "lrb_part_export", "lrb_team_create_ipc",
     "lrb_team_connect_ipc", "lrb_team_read_vector", "lrb_team_debug", "lrb_team_kernel_info",
     "lrb_team_profile", "lrb_team_profile_read", "lrb_team_profile_counters",
+    "lrb_update_segment_async", "lrb_team_solve_async", "lrb_team_spmv_async",
 ]
 
 

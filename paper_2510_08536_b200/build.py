@@ -13,12 +13,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libldurepart_b200.so")
-SOURCES = ["plan.cpp", "device.cu"]
-HEADERS = ["lrb_internal.h", "kernels.cuh", "stream.cuh"]
+# separately compiled translation units (built in parallel, then linked)
+SOURCES = ["plan.cpp", "device.cu", "scatter.cu", "solve_cg.cu", "solve_bicgstab.cu", "solve_pcg1.cu"]
+HEADERS = ["lrb_internal.h", "kernels.cuh", "stream.cuh", "launch.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-              "-Xcompiler", "-fPIC,-O3,-pthread,-Wall,-Wno-unused-function", "-shared"]
+COMPILE_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                 "-Xcompiler", "-fPIC,-O3,-pthread,-Wall,-Wno-unused-function"]
 
 
 def nvcc() -> str:
@@ -38,21 +39,41 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
-    """Compile the library; ``out``/``extra`` build tuning variants (e.g. -DLRB_MINB=3)."""
+    """Compile the library; ``out``/``extra`` build tuning variants (e.g. -DLRB_MINB=3).
+    Each translation unit is compiled by its own nvcc process (in parallel),
+    then the objects are linked into one shared library."""
     lib = out or LIB
     if not force and out is None and not _stale():
         return LIB
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES],
-           "-o", lib + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    tag = os.path.basename(lib).replace(".so", "")
+    objdir = os.path.join(HERE, "build", tag)
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [nvcc(), *ARCH, *COMPILE_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                 text=True)))
+    logs, objs, failed = [], [], False
+    for src, obj, p in procs:
+        out_s, err_s = p.communicate()
+        logs.append(f"==== {src}\n{out_s}{err_s}")
+        objs.append(obj)
+        if p.returncode != 0:
+            failed = True
+            sys.stderr.write(out_s + err_s)
+    if failed:
+        raise RuntimeError("ldurepart_b200 native build failed")
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-Xcompiler", "-pthread", *objs, "-o", lib + ".tmp"],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("ldurepart_b200 native build failed")
-    log = os.path.join(HERE, "csrc", "ptxas.log")
-    with open(log, "w") as fh:
-        fh.write(res.stderr)
+        raise RuntimeError("ldurepart_b200 native link failed")
+    if out is None:
+        with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as fh:
+            fh.write("\n".join(logs))
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(logs))
     os.replace(lib + ".tmp", lib)
     return lib
 

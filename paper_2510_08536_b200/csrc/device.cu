@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/ldurepart_b200.h"
+#include "launch.h"
 #include "stream.cuh"
 #include "lrb_internal.h"
 
@@ -127,13 +128,9 @@ static bool is_pinned(const void* p) {
 
 static int launch_scatter(lrb_part* P, int64_t r0, int64_t r1, cudaStream_t st) {
   if (r1 <= r0) return LRB_OK;
-  const int64_t first = r0 & ~int64_t(31);
-  const int64_t threads = r1 - first;
-  const int64_t blocks = (threads + 255) / 256;
-  scatter_rows_kernel<<<unsigned(blocks), 256, 0, st>>>(P->d, r0, r1);
+  LRB_CUDA(scatter_launch(P->d, r0, r1, st));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   P->stats[3] += 1;
-  LRB_CUDA(cudaGetLastError());
   return LRB_OK;
 }
 
@@ -599,6 +596,7 @@ struct TeamDevice {
   long long* prof_dev = nullptr;  // phase timestamps (lrb_team_profile), [0] holds the count
   int prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;   // stream-ordered entry points
 };
 
 }  // namespace lrb
@@ -711,6 +709,8 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   LRB_CUDA(cudaMemcpy((void*)H.tile_part, tp.data(), sizeof(int32_t) * n_tiles, cudaMemcpyHostToDevice));
   LRB_CUDA(cudaEventCreate(&D.t0));
   LRB_CUDA(cudaEventCreate(&D.t1));
+  LRB_CUDA(cudaEventCreateWithFlags(&D.ev_in, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventCreateWithFlags(&D.ev_out, cudaEventDisableTiming));
   D.inl = int(D.parts.size()) <= kInlineParts;
   if (D.inl)
     for (size_t q = 0; q < D.parts.size(); ++q) H.lp[q] = table[D.parts[q]];
@@ -827,11 +827,11 @@ static int team_hist_capacity(TeamDevice& D, int cap) {
 static const void* solve_kernel(int method, bool inl) {
   switch (method) {
     case LRB_METHOD_CG:
-      return inl ? (const void*)team_cg_kernel<false, true> : (const void*)team_cg_kernel<false, false>;
+      return cg_classic_kernel(false, inl);
     case LRB_METHOD_PCG:
-      return inl ? (const void*)team_cg_kernel<true, true> : (const void*)team_cg_kernel<true, false>;
+      return cg_classic_kernel(true, inl);
     case LRB_METHOD_BICGSTAB:
-      return inl ? (const void*)team_bicgstab_kernel<true> : (const void*)team_bicgstab_kernel<false>;
+      return bicgstab_classic_kernel(inl);
     default:
       return nullptr;
   }
@@ -877,16 +877,13 @@ static int solver_choice() {
 static const void* stream_kernel(int method, bool inl) {
   switch (method) {
     case LRB_METHOD_CG:
-      return inl ? (const void*)team_cg_stream_kernel<false, true>
-                 : (const void*)team_cg_stream_kernel<false, false>;
+      return cg_stream_kernel(false, inl);
     case LRB_METHOD_PCG:
-      return inl ? (const void*)team_cg_stream_kernel<true, true>
-                 : (const void*)team_cg_stream_kernel<true, false>;
+      return cg_stream_kernel(true, inl);
     case LRB_METHOD_BICGSTAB:
-      return inl ? (const void*)team_bicgstab_stream_kernel<true>
-                 : (const void*)team_bicgstab_stream_kernel<false>;
+      return bicgstab_stream_kernel(inl);
     case LRB_METHOD_PCG1:
-      return inl ? (const void*)team_pcg1_stream_kernel<true> : (const void*)team_pcg1_stream_kernel<false>;
+      return pcg1_stream_kernel(inl);
     default:
       return nullptr;
   }
@@ -1422,6 +1419,8 @@ void lrb_team_destroy(lrb_team* team) {
     if (D.prof_dev) cudaFree(D.prof_dev);
     if (D.t0) cudaEventDestroy(D.t0);
     if (D.t1) cudaEventDestroy(D.t1);
+    if (D.ev_in) cudaEventDestroy(D.ev_in);
+    if (D.ev_out) cudaEventDestroy(D.ev_out);
   }
   if (team->ipc_dev >= 0) {
     DeviceGuard g(team->ipc_dev);
@@ -1488,7 +1487,7 @@ int lrb_team_spmv(lrb_team* team, const double* const* x_host, double* const* y_
     for (int p : D.parts) {
       lrb_part* P = team->parts[p];
       if (!P->d.n) continue;
-      spmv_kernel<<<unsigned((P->d.n + 255) / 256), 256, 0, D.stream>>>(D.parts_dev, p);
+      spmv_kernel<><<<unsigned((P->d.n + 255) / 256), 256, 0, D.stream>>>(D.parts_dev, p);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       LRB_CUDA(cudaGetLastError());
       LRB_CUDA(cudaMemcpyAsync(y_host[p], P->d.t, 8 * P->d.n, cudaMemcpyDeviceToHost, D.stream));
@@ -1625,6 +1624,243 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
     return LRB_ETIMEOUT;
   }
   return LRB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Stream-ordered entry points (GPU-resident caller)
+// ---------------------------------------------------------------------------
+namespace lrb {
+
+__global__ void report_kernel(const SolveOut* __restrict__ o, lrb_report* __restrict__ r) {
+  r->iterations = o->iterations;
+  r->converged = o->converged;
+  r->breakdown = o->breakdown;
+  r->status = o->status;
+  r->residual = o->residual;
+  r->bnorm = o->bnorm;
+  r->device_ms = -1.0;
+}
+
+static bool is_device_or_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type != cudaMemoryTypeUnregistered;
+}
+
+// The caller's stream of device rank r (NULL array: none).
+static cudaStream_t caller_stream(const lrb_stream_t* streams, int r) {
+  return streams ? reinterpret_cast<cudaStream_t>(streams[r]) : nullptr;
+}
+
+// Device streams wait for the callers' streams (and, for multi-device teams,
+// for every device's inputs: a device must not read peers' halo operands
+// before their copies land — the async form of lrb_team_solve's host sync).
+static int order_after_callers(lrb_team* team, const lrb_stream_t* streams) {
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    if (streams) {
+      LRB_CUDA(cudaEventRecord(D.ev_in, caller_stream(streams, D.rank)));
+      LRB_CUDA(cudaStreamWaitEvent(D.stream, D.ev_in, 0));
+    }
+  }
+  return LRB_OK;
+}
+
+static int join_devices(lrb_team* team) {
+  if (team->devs.size() < 2) return LRB_OK;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaEventRecord(D.ev_in, D.stream));
+  }
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    for (auto& E : team->devs)
+      if (&E != &D) LRB_CUDA(cudaStreamWaitEvent(D.stream, E.ev_in, 0));
+  }
+  return LRB_OK;
+}
+
+static int callers_wait(lrb_team* team, const lrb_stream_t* streams) {
+  for (auto& D : team->devs) {
+    int rc = team_epilogue(team, D);
+    if (rc) return rc;
+    if (!streams) continue;
+    DeviceGuard g(D.device);
+    LRB_CUDA(cudaEventRecord(D.ev_out, D.stream));
+    LRB_CUDA(cudaStreamWaitEvent(caller_stream(streams, D.rank), D.ev_out, 0));
+  }
+  return LRB_OK;
+}
+
+}  // namespace lrb
+
+extern "C" {
+
+int lrb_update_segment_async(lrb_part* part, int32_t seg, int32_t n_pieces,
+                             const double* const* pieces, const int64_t* piece_len,
+                             lrb_stream_t stream) {
+  if (!part || seg < 0 || seg >= int(part->seg_stream.size())) {
+    set_error("lrb_update_segment_async: bad segment");
+    return LRB_EVALUE;
+  }
+  const int64_t off = part->seg_off[seg], len = part->seg_off[seg + 1] - off;
+  int rc = check_pieces(part, len, n_pieces, piece_len, "segment", seg);
+  if (rc) return rc;
+  for (int i = 0; i < n_pieces; ++i)
+    if (piece_len[i] && !is_device_or_pinned(pieces[i])) {
+      set_error("lrb_update_segment_async: piece " + std::to_string(i) +
+                " is pageable host memory (stream-ordered copies need pinned or device memory)");
+      return LRB_EVALUE;
+    }
+  DeviceGuard g(part->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LRB_CUDA(cudaStreamWaitEvent(st, part->main_done, 0));
+  double* dst = part->d.recv + off;
+  int64_t o = 0;
+  for (int i = 0; i < n_pieces; ++i) {
+    if (piece_len[i])
+      LRB_CUDA(cudaMemcpyAsync(dst + o, pieces[i], 8 * piece_len[i], cudaMemcpyDefault, st));
+    o += piece_len[i];
+  }
+  part->stats[0] += n_pieces;
+  part->stats[2] += 8 * len;
+  if (!part->seg_rows.empty()) {
+    rc = launch_scatter(part, part->seg_rows[seg], part->seg_rows[seg + 1], st);
+    if (rc) return rc;
+  }
+  std::lock_guard<std::mutex> lk(part->mu);
+  LRB_CUDA(cudaEventRecord(part->seg_done[seg], st));
+  part->seg_pending[seg] = 1;
+  return LRB_OK;
+}
+
+int lrb_team_solve_async(lrb_team* team, int32_t method, const double* const* b_dev,
+                         double* const* x_dev, double tol, int32_t max_iter,
+                         const lrb_stream_t* streams, lrb_report* rep_out) {
+  if (!team) {
+    set_error("lrb_team_solve_async: null team");
+    return LRB_EVALUE;
+  }
+  if (!(tol > 0)) {
+    set_error("tol must be positive");
+    return LRB_EVALUE;
+  }
+  if (method < LRB_METHOD_CG || method >= kMethods) {
+    set_error("lrb_team_solve_async: unknown method");
+    return LRB_EVALUE;
+  }
+  if (team->ipc_dev >= 0) {
+    set_error("lrb_team_solve_async: single-process teams only (use lrb_team_solve)");
+    return LRB_EVALUE;
+  }
+  for (auto& D : team->devs)
+    if (!D.fn[method]) {
+      set_error("lrb_team_solve_async: pcg1 needs the streaming solver");
+      return LRB_EVALUE;
+    }
+  std::lock_guard<std::mutex> lk(team->mu);
+  if (team->poisoned) {
+    set_error("team poisoned: a cross-device barrier timed out in an earlier solve; "
+              "destroy and recreate the team");
+    return LRB_ETIMEOUT;
+  }
+  int rc = order_after_callers(team, streams);
+  if (rc) return rc;
+  for (auto& D : team->devs) {
+    rc = team_prologue(team, D);
+    if (rc) return rc;
+    DeviceGuard g(D.device);
+    if (b_dev)
+      for (int p : D.parts) {
+        lrb_part* P = team->parts[p];
+        if (P->d.n && b_dev[p] && b_dev[p] != P->d.b)
+          LRB_CUDA(cudaMemcpyAsync(P->d.b, b_dev[p], 8 * P->d.n, cudaMemcpyDeviceToDevice, D.stream));
+      }
+    LRB_CUDA(cudaMemsetAsync(D.out_dev, 0, sizeof(SolveOut), D.stream));
+  }
+  rc = join_devices(team);
+  if (rc) return rc;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    TeamDev H = D.host;   // by-value kernel argument: the stored one stays as is
+    H.tol = tol;
+    H.max_iter = max_iter;
+    H.stage_bytes = D.stage_bytes[method];
+    H.n_stages = D.n_stages[method];
+    H.lane_fast = (D.streaming[method] && D.grid[method] <= kLanes && D.parts.size() == 1) ? 1 : 0;
+    H.hist = nullptr;
+    H.hist_cap = 0;
+    H.prof = nullptr;   // diagnostics belong to the synchronous entry point
+    H.prof_cta = nullptr;
+    H.prof_cap = 0;
+    void* args[] = {&H};
+    if (!D.cooperative)
+      LRB_CUDA(cudaLaunchKernel(D.fn[method], dim3(D.grid[method]), dim3(D.block[method]), args,
+                                D.smem[method], D.stream));
+    else
+      LRB_CUDA(cudaLaunchCooperativeKernel(D.fn[method], dim3(D.grid[method]), dim3(D.block[method]),
+                                           args, D.smem[method], D.stream));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (x_dev)
+      for (int p : D.parts) {
+        lrb_part* P = team->parts[p];
+        if (P->d.n && x_dev[p] && x_dev[p] != P->d.x)
+          LRB_CUDA(cudaMemcpyAsync(x_dev[p], P->d.x, 8 * P->d.n, cudaMemcpyDeviceToDevice, D.stream));
+      }
+    if (rep_out && D.rank == 0) {
+      report_kernel<<<1, 1, 0, D.stream>>>(D.out_dev, rep_out);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      LRB_CUDA(cudaGetLastError());
+    }
+  }
+  return callers_wait(team, streams);
+}
+
+int lrb_team_spmv_async(lrb_team* team, const double* const* x_dev, double* const* y_dev,
+                        const lrb_stream_t* streams) {
+  if (!team || !x_dev || !y_dev) {
+    set_error("lrb_team_spmv_async: null argument");
+    return LRB_EVALUE;
+  }
+  if (team->ipc_dev >= 0) {
+    set_error("lrb_team_spmv_async: single-process teams only");
+    return LRB_EVALUE;
+  }
+  std::lock_guard<std::mutex> lk(team->mu);
+  int rc = order_after_callers(team, streams);
+  if (rc) return rc;
+  for (auto& D : team->devs) {
+    rc = team_prologue(team, D);
+    if (rc) return rc;
+    DeviceGuard g(D.device);
+    for (int p : D.parts) {
+      lrb_part* P = team->parts[p];
+      if (P->d.n)
+        LRB_CUDA(cudaMemcpyAsync(P->d.s, x_dev[p], 8 * P->d.n, cudaMemcpyDeviceToDevice, D.stream));
+    }
+  }
+  rc = join_devices(team);
+  if (rc) return rc;
+  for (auto& D : team->devs) {
+    DeviceGuard g(D.device);
+    for (int p : D.parts) {
+      lrb_part* P = team->parts[p];
+      if (!P->d.n) continue;
+      spmv_kernel<><<<unsigned((P->d.n + 255) / 256), 256, 0, D.stream>>>(D.parts_dev, p);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      LRB_CUDA(cudaGetLastError());
+      LRB_CUDA(cudaMemcpyAsync(y_dev[p], P->d.t, 8 * P->d.n, cudaMemcpyDeviceToDevice, D.stream));
+    }
+  }
+  // a later call rewrites s: no device may still be reading a peer's s
+  rc = join_devices(team);
+  if (rc) return rc;
+  return callers_wait(team, streams);
 }
 
 }  // extern "C"

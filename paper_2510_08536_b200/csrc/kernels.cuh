@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/ldurepart_b200.h"
 #include "lrb_internal.h"
 
 namespace lrb {
@@ -170,41 +171,11 @@ __device__ __forceinline__ double row_spmv2(const PartDev& P, const PartDev* __r
 }
 
 // ---------------------------------------------------------------------------
-// Update: gather-permute one segment's rows from the receive buffer
-// (apply_scatter, update.py:105-112).  One thread per row; a warp covers one
-// SELL slice so the value stores and index loads are 128/256-byte coalesced.
-// Also refreshes dinv for Jacobi (1/diag, correctly rounded like numpy).
-// ---------------------------------------------------------------------------
-#ifndef LRB_SCATTER_CHUNK   // slots per pass: 8 covers a 7-point stencil row in one pass
-#define LRB_SCATTER_CHUNK 8
-#endif
-constexpr int kScChunk = LRB_SCATTER_CHUNK;
-__global__ void __launch_bounds__(256) scatter_rows_kernel(PartDev P, int64_t r0, int64_t r1) {
-  const int64_t i = (r0 & ~int64_t(31)) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < r0 || i >= r1) return;
-  const RowRef rr = row_ref(P, i);
-  const int dk = __ldg(P.dpos + i);
-  for (int k0 = 0; k0 < rr.w; k0 += kScChunk) {
-    int b[kScChunk];
-    double v[kScChunk];
-#pragma unroll
-    for (int u = 0; u < kScChunk; ++u)
-      b[u] = (k0 + u < rr.w) ? __ldg(P.src + rr.base + int64_t(k0 + u) * kSlice) : -1;
-#pragma unroll
-    for (int u = 0; u < kScChunk; ++u) v[u] = b[u] >= 0 ? __ldg(P.recv + b[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < kScChunk; ++u) {
-      if (b[u] < 0) continue;
-      P.val[rr.base + int64_t(k0 + u) * kSlice] = v[u];
-      if (k0 + u == dk) P.dinv[i] = 1.0 / v[u];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Distributed SpMV y = A x for the API spmv(): x in part.s, y in part.t
 // (halo read straight from the owner's x, any device of the team).
 // ---------------------------------------------------------------------------
+// (a template so that only the TU launching it instantiates it)
+template <int = 0>
 __global__ void __launch_bounds__(256) spmv_kernel(const PartDev* __restrict__ parts, int p) {
   const PartDev& P = parts[p];
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -354,7 +325,7 @@ __device__ __forceinline__ int64_t tile_of(const TeamDev& T, int t) {
   return tile_first(T) + int64_t(t) * tile_step();
 }
 
-__device__ void team_fail(const TeamDev& T, int code) {
+static __device__ void team_fail(const TeamDev& T, int code) {
   atomicCAS((int*)&T.out->status, 0, code);
 }
 

@@ -1,0 +1,24 @@
+// Kernel entry points of the separately compiled CUDA translation units
+// (scatter.cu, solve_cg.cu, solve_bicgstab.cu, solve_pcg1.cu), for the host
+// side in device.cu.  Internal; not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lrb_internal.h"
+
+namespace lrb {
+
+// Scatter of rows [r0, r1) of part P on stream st (scatter.cu).
+cudaError_t scatter_launch(const PartDev& P, int64_t r0, int64_t r1, cudaStream_t st);
+
+// Host stubs of the persistent team solvers (kernel function pointers for
+// cudaLaunch[Cooperative]Kernel / occupancy queries).
+const void* cg_classic_kernel(bool jac, bool inl);       // solve_cg.cu
+const void* cg_stream_kernel(bool jac, bool inl);        // solve_cg.cu
+const void* bicgstab_classic_kernel(bool inl);           // solve_bicgstab.cu
+const void* bicgstab_stream_kernel(bool inl);            // solve_bicgstab.cu
+const void* pcg1_stream_kernel(bool inl);                // solve_pcg1.cu
+
+}  // namespace lrb

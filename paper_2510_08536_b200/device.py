@@ -136,6 +136,15 @@ class DevicePart:
         N.check(N.lrb_update_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
         self._touch()
 
+    def update_segment_async(self, seg, pieces, stream=0):
+        """Stream-ordered direct update (lrb_update_segment_async): pieces are
+        pinned host or CUDA torch tensors (float64, contiguous); no host sync.
+        ``stream`` is a raw cudaStream_t (e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+        ptrs = N.ptr_array([t.data_ptr() for t in pieces])
+        lens = np.array([t.numel() for t in pieces], dtype=np.int64)
+        N.check(N.lrb_update_segment_async(self.h, seg, len(pieces), ptrs, N.ptr(lens), int(stream)))
+        self._touch()
+
     def stage_segment(self, seg, pieces):
         arrs, ptrs, lens = self._pieces(pieces)
         N.check(N.lrb_stage_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
@@ -328,6 +337,33 @@ class Team:
                               C.byref(rep), N.ptr(hist) if hist_cap > 0 else None, int(hist_cap))
         N.check(rc)
         return xs, rep, hist[:max(min(rep.iterations, hist_cap), 0)]
+
+    @staticmethod
+    def _streams(streams):
+        return None if streams is None else (C.c_void_p * len(streams))(*[int(s) or None for s in streams])
+
+    def solve_async(self, method, b_dev, x_dev, tol, max_iter, streams=None, report=None):
+        """Stream-ordered solve on device tensors (lrb_team_solve_async):
+        ``b_dev``/``x_dev`` one CUDA float64 tensor per part (or None lists),
+        ``streams`` one raw cudaStream_t per device rank, ``report`` a pinned
+        or CUDA uint8 tensor of >= 40 bytes receiving an lrb_report."""
+        bp = None if b_dev is None else N.ptr_array([0 if b is None else b.data_ptr() for b in b_dev])
+        xp = None if x_dev is None else N.ptr_array([0 if x is None else x.data_ptr() for x in x_dev])
+        N.check(N.lrb_team_solve_async(self.h, N.METHODS[method], bp, xp, float(tol), int(max_iter),
+                                       self._streams(streams),
+                                       None if report is None else report.data_ptr()))
+
+    @staticmethod
+    def report_from(buf):
+        """Decode an lrb_report written by solve_async (host copy of ``buf``)."""
+        raw = bytes(buf.cpu().numpy().tobytes()[:C.sizeof(N.Report)])
+        return N.Report.from_buffer_copy(raw)
+
+    def spmv_async(self, x_dev, y_dev, streams=None):
+        """Stream-ordered distributed SpMV on device tensors (lrb_team_spmv_async)."""
+        N.check(N.lrb_team_spmv_async(self.h, N.ptr_array([x.data_ptr() for x in x_dev]),
+                                      N.ptr_array([y.data_ptr() for y in y_dev]),
+                                      self._streams(streams)))
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None

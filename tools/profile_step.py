@@ -1,4 +1,6 @@
 """One C3 timestep under ncu: update (8 segment scatters) + one PCG solve.
+(``--n 300 --ranks 16 --method bicgstab``: one C4 momentum BiCGStab solve on
+the bench's momentum coefficients, right-hand side Ux.)
 
     ncu --set full -k regex:team_cg -c 1 -o gpurun_out/prof python tools/profile_step.py --step 5
     ncu --metrics gpu__time_duration.sum --csv --log-file ... python tools/profile_step.py
@@ -17,7 +19,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from bench import MAX_ITER, TOL, Problem, n_checks, solve_bytes  # noqa: E402
+from bench import (MAX_ITER, TOL, Problem, bicgstab_bytes, momentum_eps, momentum_rhs,  # noqa: E402
+                   momentum_values_into, n_checks, solve_bytes)
 
 
 def main():
@@ -32,19 +35,36 @@ def main():
     pm = lrb.make_partition_map(prob.cells, args.ranks)
     out = {}
 
+    mom = args.method == "bicgstab"
+
+    def inputs(r):
+        if not mom:
+            return prob.produce(r, args.step)
+        m, ifs = prob.base[r]
+        eu, el = momentum_eps(m, r)
+        up, lo = np.zeros(m.n_faces), np.zeros(m.n_faces)
+        momentum_values_into(eu, el, args.step, up, lo)
+        return lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, np.full(m.n_cells, 6.5), lo,
+                             up), ifs
+
     def program(ctx):
         r = ctx.rank
         s = lrb.repartition(*prob.base[r], pm, ctx)
-        lrb.update(s, *prob.produce(r, args.step), "direct")
+        lrb.update(s, *inputs(r), "direct")
         if s.is_owner:
-            x, rep = lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), TOL, MAX_ITER,
-                                  s.comm, method=args.method, history=True)
+            b = momentum_rhs(s.matrix.n_owned, 0) if mom else np.ones(s.matrix.n_owned)
+            solve = lrb.bicgstab_solve if mom else lrb.cg_solve
+            kw = {} if mom else {"method": args.method}
+            x, rep = solve(s.matrix, s.halo, b, TOL, MAX_ITER, s.comm, history=True, **kw)
             p = s.part.plan
             nnz = p.nnz_local + p.nnz_nonlocal
             ck = n_checks(rep.history, rep.iterations, TOL)
+            alg = (bicgstab_bytes(p.n, nnz, p.n_halo, rep.iterations, ck) if mom else
+                   solve_bytes(p.n, nnz, p.n_halo, rep.iterations, ck, args.method))
             out.update(step=args.step, iterations=rep.iterations, checks=ck, n=p.n, nnz=nnz,
+                       method=args.method,
                        sell_entries=p.sell_entries, uniform_entries=p.uniform_entries,
-                       alg_bytes=solve_bytes(p.n, nnz, p.n_halo, rep.iterations, ck, args.method),
+                       alg_bytes=alg,
                        scatter_alg_bytes=20 * p.n_buf, device_ms=rep.device_ms)
 
     lrb.run_world(args.ranks, program)
