@@ -587,6 +587,14 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
         dram_gbs = line["roofline"]["traffic"] / (line["roofline"]["kernel_ms"] * 1e-3) / 1e9
         line["roofline"]["dram_achieved"] = round(dram_gbs, 1)
         line["roofline"]["dram_frac"] = round(dram_gbs / line["roofline"]["peak"], 4)
+    ts = traffic_ratio(args.workload + "_scatter")
+    if ts:
+        # the whole-part scatter's DRAM bytes per algorithmic byte (ncu), applied
+        # to this run's scatter time
+        sd = scatter_gbs * ts["dram_bytes_per_alg_byte"]
+        line["breakdown"]["scatter_dram_gbs"] = round(sd, 1)
+        line["breakdown"]["scatter_dram_frac"] = round(sd / line["roofline"]["peak"], 4)
+        line["breakdown"]["scatter_traffic_note"] = ts.get("note")
     return line
 
 
@@ -915,7 +923,9 @@ def run_c5(args):
                                 "link_gbs": round(8 * n_buf / (pg * 1e-3) / 1e9, 1),
                                 "inputs": "perturb_coefficients output (pageable numpy); host "
                                           "copy into the pinned stage counted"}
-    t = traffic_ratio("c5")
+    # the same kernel's whole-part DRAM/algorithmic ratio from ncu at C3 (the 8
+    # concurrent part launches move 1.1 GB, well past L2, like the C3 launch)
+    t = traffic_ratio("c5") or traffic_ratio("c3_scatter")
     if t:
         line["roofline"]["traffic"] = int(t["dram_bytes_per_alg_byte"] *
                                           line["roofline"]["alg_bytes_per_launch"])

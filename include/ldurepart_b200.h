@@ -133,6 +133,11 @@ int lrb_part_read_buffer(lrb_part* part, double* out);
 /* Read the fused values in the reference's row-major local / non-local order
  * (DistributedCooMatrix.local.vals / non_local.vals). */
 int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_vals);
+/* Write values in the reference's row-major local / non-local order into the
+ * part (either pointer nullable: that block is kept), then refresh the Jacobi
+ * diagonal.  Backs the drop-in's writable DistributedCooMatrix .vals (the
+ * reference keeps CooMatrix values writable by design, tests/test_core.py:121). */
+int lrb_part_write_values(lrb_part* part, const double* local_vals, const double* nonlocal_vals);
 /* Make the part's solve stream wait for all pending segment scatters. */
 int lrb_part_join(lrb_part* part);
 int lrb_part_sync(lrb_part* part);
@@ -184,9 +189,12 @@ int lrb_team_debug(lrb_team* team, int64_t* out);
 /* Launch geometry of the solve kernel of `method` on device rank 0:
  * out[0] = 1 streaming (bulk-copy, stream.cuh) / 0 classic (kernels.cuh),
  * out[1] = grid, out[2] = block, out[3] = ring stages, out[4] = stage bytes,
- * out[5] = dynamic shared memory bytes.  LRB_SOLVER=classic at team creation
+ * out[5] = dynamic shared memory bytes, out[6] = 1 if halo mirrors are on
+ * (owners push boundary rows into the readers' mirrors; the streaming CG /
+ * PCG / BiCGStab kernels read halo operands locally; LRB_HALO=direct at team
+ * creation turns them off), out[7] = halo push runs of device rank 0's parts.  LRB_SOLVER=classic at team creation
  * selects the classic kernels. */
-int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out);
+int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out /* [8] */);
 /* Phase profiling (diagnostics): with cap > 0 every later solve records the
  * globaltimer (ns) at each team-barrier release, up to cap entries (cap = 0
  * turns it off).  lrb_team_profile_read copies the last solve's timestamps of

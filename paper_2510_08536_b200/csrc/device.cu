@@ -52,8 +52,8 @@ static int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 
 // Arena layout of one part (all sections 256-byte aligned).
 struct Layout {
-  int64_t slice_ptr, slice_pat, pat_off, rmask, tile_win, col, src, dpos, hpart, hidx, val, recv,
-      vec, total;
+  int64_t slice_ptr, slice_pat, pat_off, rmask, tile_win, col, src, dpos, hpart, hidx, hm, val,
+      recv, vec, total;
   static constexpr int kVecs = 12;
 };
 
@@ -77,6 +77,7 @@ static Layout layout_of(const Plan& P) {
   L.dpos = take(2 * P.n);
   L.hpart = take(4 * h);
   L.hidx = take(4 * h);
+  L.hm = take(8 * kMirVecs * h);
   L.val = take(8 * E);
   L.recv = take(8 * P.n_buf);
   L.vec = o;
@@ -186,6 +187,7 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   D.dpos = reinterpret_cast<const int16_t*>(base + L.dpos);
   D.hpart = reinterpret_cast<const int32_t*>(base + L.hpart);
   D.hidx = reinterpret_cast<const int32_t*>(base + L.hidx);
+  D.hm = D.n_halo ? reinterpret_cast<double*>(base + L.hm) : nullptr;
   D.val = reinterpret_cast<double*>(base + L.val);
   D.recv = reinterpret_cast<double*>(base + L.recv);
   double* vecs[Layout::kVecs];
@@ -500,6 +502,30 @@ int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_va
   return LRB_OK;
 }
 
+int lrb_part_write_values(lrb_part* part, const double* local_vals, const double* nonlocal_vals) {
+  if (!part) {
+    set_error("lrb_part_write_values: null part");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  const int64_t E = part->slice_ptr.back();
+  std::vector<double> sell(E);
+  if (E) LRB_CUDA(cudaMemcpyAsync(sell.data(), part->d.val, 8 * E, cudaMemcpyDeviceToHost, part->main));
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  if (local_vals)
+    for (size_t j = 0; j < part->loc_sell.size(); ++j) sell[part->loc_sell[j]] = local_vals[j];
+  if (nonlocal_vals)
+    for (size_t j = 0; j < part->nl_sell.size(); ++j) sell[part->nl_sell[j]] = nonlocal_vals[j];
+  if (E) LRB_CUDA(cudaMemcpyAsync(part->d.val, sell.data(), 8 * E, cudaMemcpyHostToDevice, part->main));
+  LRB_CUDA(dinv_refresh_launch(part->d, part->main));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  LRB_CUDA(cudaEventRecord(part->main_done, part->main));
+  return LRB_OK;
+}
+
 int lrb_part_sync(lrb_part* part) {
   if (!part) {
     set_error("lrb_part_sync: null part");
@@ -597,6 +623,8 @@ struct TeamDevice {
   int prof_cap = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;   // stream-ordered entry points
+  bool mirrors = false;           // halo mirrors on (streaming CG/PCG/BiCGStab push, read locally)
+  int64_t push_runs = 0;          // halo push runs of the local parts
 };
 
 }  // namespace lrb
@@ -626,17 +654,84 @@ static int solver_choice();
 static int max_grid(const void* kernel, int device, int64_t n_tiles, int n_share,
                     int64_t stage_doubles, size_t* smem);
 
+// Halo push plan of a team (SURVEY §8 e: the halo exchange).  For every part
+// p, the runs of its rows that other parts read as halo operands, from the
+// readers' hpart/hidx tables (device, peer or IPC memory; read once at team
+// creation): {row_lo, row_hi, reader part, reader's halo slot of row_lo},
+// rows and slots consecutive along a run.  Mirrors are on for the team iff
+// every part has at most kMaxSndRuns runs (slab partitions: <= 2 per
+// neighbour); the decision depends only on team-wide data, so every process
+// of a multi-process team takes the same one.  LRB_HALO=direct turns them
+// off (remote loads inside the SpMV, the round-1 data path).
+struct HaloPush {
+  bool on = false;
+  std::vector<std::vector<int64_t>> runs;            // [part] 4 per run
+  std::vector<std::pair<int64_t, int64_t>> quiet;    // [part] largest row range with no run
+};
+
+static int plan_halo_push(const std::vector<PartDev>& table, HaloPush& hp) {
+  const int np = int(table.size());
+  hp.runs.assign(np, {});
+  hp.quiet.assign(np, {0, 0});
+  const char* env = getenv("LRB_HALO");
+  hp.on = !(env && std::strcmp(env, "direct") == 0);
+  for (int q = 0; q < np && hp.on; ++q) {
+    const PartDev& Q = table[q];
+    if (!Q.n_halo) continue;
+    if (!Q.hm) {
+      hp.on = false;
+      break;
+    }
+    std::vector<int32_t> hpart(Q.n_halo), hidx(Q.n_halo);
+    LRB_CUDA(cudaMemcpy(hpart.data(), Q.hpart, sizeof(int32_t) * Q.n_halo, cudaMemcpyDefault));
+    LRB_CUDA(cudaMemcpy(hidx.data(), Q.hidx, sizeof(int32_t) * Q.n_halo, cudaMemcpyDefault));
+    for (int64_t h = 0; h < Q.n_halo;) {
+      const int p = hpart[h];
+      int64_t e = h + 1;
+      while (e < Q.n_halo && hpart[e] == p && int64_t(hidx[e]) == hidx[h] + (e - h)) ++e;
+      if (p < 0 || p >= np || p == q) {
+        set_error("lrb_team_create: halo slot owned by an invalid part");
+        return LRB_EVALUE;
+      }
+      auto& R = hp.runs[p];
+      R.insert(R.end(), {int64_t(hidx[h]), int64_t(hidx[h]) + (e - h), int64_t(q), h});
+      if (int64_t(R.size()) / 4 > kMaxSndRuns) hp.on = false;
+      h = e;
+    }
+  }
+  if (!hp.on) {
+    for (auto& R : hp.runs) R.clear();
+    return LRB_OK;
+  }
+  for (int p = 0; p < np; ++p) {   // largest gap between the runs: the no-push interval
+    std::vector<std::pair<int64_t, int64_t>> iv;
+    for (size_t k = 0; k < hp.runs[p].size(); k += 4) iv.emplace_back(hp.runs[p][k], hp.runs[p][k + 1]);
+    std::sort(iv.begin(), iv.end());
+    int64_t cur = 0, best_lo = 0, best_hi = 0;
+    for (auto& r : iv) {
+      if (r.first - cur > best_hi - best_lo) best_lo = cur, best_hi = r.first;
+      cur = std::max(cur, r.second);
+    }
+    if (table[p].n - cur > best_hi - best_lo) best_lo = cur, best_hi = table[p].n;
+    hp.quiet[p] = {best_lo, best_hi};
+  }
+  return LRB_OK;
+}
+
 // Workspace, tile map, launch geometry of one device of a team.  table holds
 // every team part's descriptor; local parts get their tile ranges here.
 static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* const* by_index,
-                        int n_parts, int n_dev, int n_share) {
+                        int n_parts, int n_dev, int n_share, const HaloPush& hp) {
   int64_t t = 0;
+  int64_t n_runs = 0;
   for (int p : D.parts) {
     lrb_part* P = by_index[p];
     P->d.tile0 = t;
     P->d.ntiles = (P->d.n + kTile - 1) / kTile;
     t += P->d.ntiles;
     table[p] = P->d;
+    table[p].mir = hp.on && table[p].n_halo > 0;
+    n_runs += hp.on ? int64_t(hp.runs[p].size()) / 4 : 0;
   }
   D.n_tiles = t;
   DeviceGuard g(D.device);
@@ -660,6 +755,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_peer_flags = take(sizeof(void*) * n_dev);
   const size_t o_peer_red = take(sizeof(void*) * n_dev);
   const size_t o_out = take(sizeof(SolveOut));
+  const size_t o_snd = take(sizeof(int64_t) * 4 * std::max<int64_t>(n_runs, 1));
   // streaming solvers: stage size from the largest stageable tile, and the
   // per-tile stage headers
   const bool want_stream = solver_choice() != 1;
@@ -698,6 +794,25 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);
   H.peer_part_red = reinterpret_cast<double**>(w + o_peer_red);
   H.out = D.out_dev;
+  // halo push runs of the local parts
+  {
+    int64_t* snd = reinterpret_cast<int64_t*>(w + o_snd);
+    int64_t at = 0;
+    for (size_t q = 0; q < D.parts.size(); ++q) {
+      const int p = D.parts[q];
+      PartDev& E = table[p];
+      const int64_t nr = hp.on ? int64_t(hp.runs[p].size()) / 4 : 0;
+      E.snd = nr ? snd + 4 * at : nullptr;
+      E.n_snd = int32_t(nr);
+      E.sq_lo = hp.on ? hp.quiet[p].first : 0;
+      E.sq_hi = hp.on ? hp.quiet[p].second : E.n;
+      if (nr)
+        LRB_CUDA(cudaMemcpy(snd + 4 * at, hp.runs[p].data(), sizeof(int64_t) * 4 * nr, cudaMemcpyHostToDevice));
+      at += nr;
+    }
+    D.mirrors = hp.on;
+    D.push_runs = at;
+  }
   {
     const char* env = getenv("LRB_BARRIER_TIMEOUT_S");
     const double s = env ? atof(env) : 20.0;
@@ -1085,8 +1200,12 @@ int lrb_team_create_ex(int32_t n_parts, lrb_part* const* parts, const int32_t* d
       }
   // per-device workspace, then the shared part / peer tables
   std::vector<PartDev> table(n_parts);
+  for (int p = 0; p < n_parts; ++p) table[p] = parts[p]->d;
+  HaloPush hp;
+  int rc0 = plan_halo_push(table, hp);
+  if (rc0) return rc0;
   for (auto& D : team->devs) {
-    int rc = setup_device(D, table, parts, n_parts, n_dev, share[D.device]);
+    int rc = setup_device(D, table, parts, n_parts, n_dev, share[D.device], hp);
     if (rc) return rc;
   }
   std::vector<void*> pf(n_dev), pr(n_dev);
@@ -1181,6 +1300,7 @@ int lrb_part_export(const lrb_part* part, void* blob) {
   d.dpos = rebase(d.dpos, arena, zero);
   d.hpart = rebase(d.hpart, arena, zero);
   d.hidx = rebase(d.hidx, arena, zero);
+  d.hm = rebase(d.hm, arena, zero);
   d.val = rebase(d.val, arena, zero);
   d.recv = rebase(d.recv, arena, zero);
   for (double** v : {&d.x, &d.r, &d.p0, &d.p1, &d.q, &d.b, &d.dinv, &d.rhat, &d.v0, &d.v1, &d.s, &d.t})
@@ -1233,6 +1353,7 @@ int lrb_team_create_ipc(int32_t n_parts, int32_t part_begin, int32_t n_local,
     d.dpos = rebase(d.dpos, zero, arena);
     d.hpart = rebase(d.hpart, zero, arena);
     d.hidx = rebase(d.hidx, zero, arena);
+    d.hm = rebase(d.hm, zero, arena);
     d.val = rebase(d.val, zero, arena);
     d.recv = rebase(d.recv, zero, arena);
     for (double** v : {&d.x, &d.r, &d.p0, &d.p1, &d.q, &d.b, &d.dinv, &d.rhat, &d.v0, &d.v1, &d.s, &d.t})
@@ -1245,7 +1366,12 @@ int lrb_team_create_ipc(int32_t n_parts, int32_t part_begin, int32_t n_local,
   D.rank = dev_rank;
   for (int i = 0; i < n_local; ++i) D.parts.push_back(part_begin + i);
   team->dev_of_part.assign(n_parts, -1);
-  int rc = setup_device(D, table, team->parts.data(), n_parts, n_dev, 1);
+  for (int i = 0; i < n_local; ++i) table[part_begin + i] = local_parts[i]->d;
+  HaloPush hp;
+  int rc = plan_halo_push(table, hp);
+  if (rc) return rc;
+  for (int p = 0; p < n_parts; ++p) table[p].mir = hp.on && table[p].n_halo > 0;
+  rc = setup_device(D, table, team->parts.data(), n_parts, n_dev, 1, hp);
   if (rc) return rc;
   // local table now; peer tables after connect
   LRB_CUDA(cudaMemcpy(D.parts_dev, table.data(), sizeof(PartDev) * n_parts, cudaMemcpyHostToDevice));
@@ -1340,6 +1466,8 @@ int lrb_team_kernel_info(lrb_team* team, int32_t method, int64_t* out) {
   out[3] = D.streaming[method] ? D.n_stages[method] : 0;
   out[4] = D.streaming[method] ? D.stage_bytes[method] : 0;
   out[5] = int64_t(D.smem[method]);
+  out[6] = D.mirrors ? 1 : 0;
+  out[7] = D.push_runs;
   return LRB_OK;
 }
 

@@ -51,6 +51,24 @@ __device__ __forceinline__ RowRef row_ref(const PartDev& P, int64_t i) {
   return RowRef{b + (i & 31), int((e - b) >> 5)};
 }
 
+// Halo push (PartDev::hm): the owner of row i stores v, its new value of
+// mirrored vector vid, into the halo mirror of every part that reads row i
+// (peer memory for parts on other GPUs).  Interior rows return after two
+// compares.  Ordering: the team barrier's system-scope fence (team_sync)
+// publishes the pushes together with the phase's other writes.
+__device__ __forceinline__ void hpush(const PartDev& P, const PartDev* __restrict__ parts, int vid,
+                                      int64_t i, double v) {
+  if (i >= P.sq_lo && i < P.sq_hi) return;
+  for (int k = 0; k < P.n_snd; ++k) {
+    const int64_t* s = P.snd + 4 * k;
+    const int64_t lo = __ldg(s), hi = __ldg(s + 1);
+    if (i >= lo && i < hi) {
+      const PartDev& Q = parts[__ldg(s + 2)];
+      Q.hm[int64_t(vid) * Q.n_halo + __ldg(s + 3) + (i - lo)] = v;
+    }
+  }
+}
+
 // y_i = sum_k a_ik * f(col_k), reference order, no FMA.  f(Q, j) returns the
 // vector value at row j of part Q (local part or halo owner).
 //

@@ -12,6 +12,8 @@ namespace lrb {
 
 // Scatter of rows [r0, r1) of part P on stream st (scatter.cu).
 cudaError_t scatter_launch(const PartDev& P, int64_t r0, int64_t r1, cudaStream_t st);
+// dinv from the diagonal values (after lrb_part_write_values).
+cudaError_t dinv_refresh_launch(const PartDev& P, cudaStream_t st);
 
 // Host stubs of the persistent team solvers (kernel function pointers for
 // cudaLaunch[Cooperative]Kernel / occupancy queries).

@@ -69,7 +69,24 @@ struct PartDev {
   // tiling inside the team kernel
   int64_t tile0;      // first tile of this part in its device's tile space
   int64_t ntiles;
+  // Halo mirror (arena-resident, [kMirVecs][n_halo]): the owners of this
+  // part's halo rows push their new values of the mirrored Krylov vectors
+  // here while they compute them (peer stores over NVLink for other GPUs), so
+  // the next SpMV reads its halo operands from local memory instead of
+  // issuing remote loads on its critical path (solver.py:86-90: the halo is
+  // filled before the multiply).
+  double* hm;
+  // Team-level fields (set at team creation in the team's part table):
+  const int64_t* snd;   // [n_snd][4] push runs of THIS part's rows: {row_lo, row_hi, reader part,
+                        //   reader halo slot of row_lo}; slots are consecutive along a run
+  int32_t n_snd;
+  int32_t mir;          // 1: the streaming solvers read halo operands from hm (mirrors on)
+  int64_t sq_lo, sq_hi; // rows in [sq_lo, sq_hi) are in no run (interior: nothing to push)
 };
+
+// Mirrored vectors (halo mirror slot ids).
+enum MirVec { kMx = 0, kMr = 1, kMp0 = 2, kMp1 = 3, kMs = 4, kMv0 = 5, kMv1 = 6, kMirVecs = 7 };
+constexpr int kMaxSndRuns = 32;   // more push runs for a part: mirrors off for the team
 
 // Work decomposition of the persistent kernels: a tile is kTPB*kRPT rows of
 // one part.  The per-tile partial dot products are reduced in fixed order,

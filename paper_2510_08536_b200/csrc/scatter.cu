@@ -58,6 +58,23 @@ __global__ void __launch_bounds__(kScTPB) scatter_rows_kernel(PartDev P, int64_t
   scatter_row(P, i);
 }
 
+// Jacobi refresh after values were written directly (lrb_part_write_values):
+// dinv[i] = 1 / val[diagonal slot of row i].
+__global__ void __launch_bounds__(kScTPB) dinv_refresh_kernel(PartDev P) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const int dk = __ldg(P.dpos + i);
+  if (dk < 0) return;
+  const RowRef rr = row_ref(P, i);
+  P.dinv[i] = 1.0 / P.val[rr.base + int64_t(dk) * kSlice];
+}
+
+cudaError_t dinv_refresh_launch(const PartDev& P, cudaStream_t st) {
+  if (P.n <= 0) return cudaSuccess;
+  dinv_refresh_kernel<<<unsigned((P.n + kScTPB - 1) / kScTPB), kScTPB, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
 // Launch the scatter of rows [r0, r1) of part P on stream st.
 cudaError_t scatter_launch(const PartDev& P, int64_t r0, int64_t r1, cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;

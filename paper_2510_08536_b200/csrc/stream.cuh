@@ -606,12 +606,27 @@ __device__ __forceinline__ double row_fixed(int w, int ii, int eb, unsigned msk,
   return acc;
 }
 
+// The halo mirror of part P seen as a part whose mirrored vectors have one
+// element per halo slot (operand lambdas index it with the slot).
+__device__ __forceinline__ PartDev mirror_of(const PartDev& P) {
+  PartDev M;
+  const int64_t h = P.n_halo;
+  M.x = P.hm + kMx * h;
+  M.r = P.hm + kMr * h;
+  M.p0 = P.hm + kMp0 * h;
+  M.p1 = P.hm + kMp1 * h;
+  M.s = P.hm + kMs * h;
+  M.v0 = P.hm + kMv0 * h;
+  M.v1 = P.hm + kMv1 * h;
+  return M;
+}
+
 // Staged SpMV of tile row lr (its 32-row slice is warp-uniform; every lane
 // of the warp calls it); xs(q) is the staged operand, fh(owner part, row) a
 // halo column's operand; xd receives the row's diagonal operand.
 template <bool HALO, class XS, class FH>
 __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __restrict__ hpart,
-                                                  const int32_t* __restrict__ hidx,
+                                                  const int32_t* __restrict__ hidx, const PartDev* mp,
                                                   const PartDev* __restrict__ parts, const StageHdr& H,
                                                   const Slots& slot, const double* __restrict__ sval,
                                                   const uint16_t* __restrict__ smask, int lr, const XS& xs,
@@ -642,7 +657,10 @@ __device__ __forceinline__ double row_spmv_staged(const int n, const int32_t* __
       const int c = ii + slot.off[k];
       double xv;
       if (on && c >= n) {
-        xv = fh(parts[__ldg(hpart + (c - n))], int64_t(__ldg(hidx + (c - n))));
+        // halo operand: from this part's mirror (pushed by the owner) or
+        // straight from the owning part (peer memory)
+        xv = mp ? fh(mirror_of(*mp), int64_t(c - n))
+                : fh(parts[__ldg(hpart + (c - n))], int64_t(__ldg(hidx + (c - n))));
       } else {
         xv = xs(on ? ii + slot.del[k] : 0);
         xv = on ? xv : 0.0;
@@ -679,21 +697,24 @@ __device__ __forceinline__ StagedTile staged_tile(const char* st, const StageHdr
   t.vbytes = H.vbytes;
   return t;
 }
-// Dispatch on whether the part has halo columns.
-template <class XS, class FH>
+// Dispatch on whether the part has halo columns.  MIRROR: the kernel keeps
+// the halo mirrors current (hpush on every write of a mirrored vector), so
+// halo operands come from the part's own mirror when the team has them on.
+template <bool MIRROR = false, class XS, class FH>
 __device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
                                              const StageHdr& H, const StagedTile& t, const Slots& slot, int lr,
                                              const XS& xs, FH&& fh, double& xd) {
   const int n = int(P.n);
-  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd)
-                  : row_spmv_staged<false>(n, P.hpart, P.hidx, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd);
+  const PartDev* mp = (MIRROR && P.mir) ? &P : nullptr;
+  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd)
+                  : row_spmv_staged<false>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd);
 }
-template <class XS, class FH>
+template <bool MIRROR = false, class XS, class FH>
 __device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
                                              const StageHdr& H, const StagedTile& t, const Slots& slot, int lr,
                                              const XS& xs, FH&& fh) {
   double xd;
-  return staged_row(P, parts, H, t, slot, lr, xs, fh, xd);
+  return staged_row<MIRROR>(P, parts, H, t, slot, lr, xs, fh, xd);
 }
 
 // Vectors of one packed elementwise tile: vector v at base + v * stride.
@@ -897,10 +918,13 @@ __global__ void LRB_STREAM_BOUNDS
         const double b = V[0][lr];
         P.x[i] = 0.0;
         P.r[i] = b;
+        hpush(P, parts, kMx, i, 0.0);
+        if (!JAC) hpush(P, parts, kMr, i, b);
         acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
         if (JAC) {
           const double z = __dmul_rn(V[1][lr], b);
           P.s[i] = z;
+          hpush(P, parts, kMs, i, z);
           acc[1] = __dadd_rn(acc[1], __dmul_rn(b, z));
         }
       });
@@ -953,16 +977,19 @@ __global__ void LRB_STREAM_BOUNDS
             const PnewCG pn{t.w(0), t.w(1), beta};
             const Win1 z1{t.w(0)};
             double pi;   // p_new of the row itself: the diagonal slot's operand
-            const double qi = first ? staged_row(P, parts, H, t, slot, lr, z1, pnew_g, pi)
-                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g, pi);
+            const double qi = first ? staged_row<true>(P, parts, H, t, slot, lr, z1, pnew_g, pi)
+                                    : staged_row<true>(P, parts, H, t, slot, lr, pn, pnew_g, pi);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
               pout[i] = pi;
+              hpush(P, parts, pa ? kMp0 : kMp1, i, pi);
               P.q[i] = qi;
               acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
               if (pend) {   // the pending x update: p_old of the row itself
                 const double po = t.w(1)[diag_pos(H, slot, sl, i)];
-                P.x[i] = __dadd_rn(t.tail(0)[lr], __dmul_rn(step_x, po));
+                const double xn = __dadd_rn(t.tail(0)[lr], __dmul_rn(step_x, po));
+                P.x[i] = xn;
+                hpush(P, parts, kMx, i, xn);
               }
             }
           } else if (lr < H.rows) {
@@ -970,9 +997,14 @@ __global__ void LRB_STREAM_BOUNDS
             const double pi = pnew_g(P, i);
             const double qi = row_spmv(P, parts, i, pnew_g);
             pout[i] = pi;
+            hpush(P, parts, pa ? kMp0 : kMp1, i, pi);
             P.q[i] = qi;
             acc[0] = __dadd_rn(acc[0], __dmul_rn(pi, qi));
-            if (pend) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(step_x, (pa ? P.p1 : P.p0)[i]));
+            if (pend) {
+              const double xn = __dadd_rn(P.x[i], __dmul_rn(step_x, (pa ? P.p1 : P.p0)[i]));
+              P.x[i] = xn;
+              hpush(P, parts, kMx, i, xn);
+            }
           }
         });
     pend = false;
@@ -1004,10 +1036,12 @@ __global__ void LRB_STREAM_BOUNDS
           const int64_t i = H.row0 + lr;
           const double r = __dsub_rn(V[0][lr], __dmul_rn(step, V[1][lr]));
           P.r[i] = r;
+          if (!JAC) hpush(P, parts, kMr, i, r);
           acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
           if (JAC) {
             const double z = __dmul_rn(V[2][lr], r);
             P.s[i] = z;
+            hpush(P, parts, kMs, i, z);
             acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
           }
         });
@@ -1028,10 +1062,13 @@ __global__ void LRB_STREAM_BOUNDS
           const double r = __dsub_rn(V[2][lr], __dmul_rn(step, V[3][lr]));
           P.x[i] = x;
           P.r[i] = r;
+          hpush(P, parts, kMx, i, x);
+          if (!JAC) hpush(P, parts, kMr, i, r);
           acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
           if (JAC) {
             const double z = __dmul_rn(V[4][lr], r);
             P.s[i] = z;
+            hpush(P, parts, kMs, i, z);
             acc[1] = __dadd_rn(acc[1], __dmul_rn(r, z));
           }
         });
@@ -1057,8 +1094,8 @@ __global__ void LRB_STREAM_BOUNDS
             if (H.tma) {
               const StagedTile t = staged_tile(st, H, pend ? 2 : 1);
               const Slots slot = slice_slots(st, H, lr >> 5);
-              const double ax = pend ? staged_row(P, parts, H, t, slot, lr, PnewCG{t.w(0), t.w(1), step_x}, xg)
-                                     : staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+              const double ax = pend ? staged_row<true>(P, parts, H, t, slot, lr, PnewCG{t.w(0), t.w(1), step_x}, xg)
+                                     : staged_row<true>(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
@@ -1126,6 +1163,8 @@ __global__ void LRB_STREAM_BOUNDS
         P.x[i] = 0.0;
         P.r[i] = b;
         P.rhat[i] = b;
+        hpush(P, parts, kMx, i, 0.0);
+        hpush(P, parts, kMr, i, b);
         acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
       });
   const double bb = red[0];
@@ -1173,12 +1212,14 @@ __global__ void LRB_STREAM_BOUNDS
             const Win1 r1{t.w(0)};
             const PnewCG pn{t.w(0), t.w(1), beta};   // r + beta u
             double pi;
-            const double vi = first ? staged_row(P, parts, H, t, slot, lr, r1, pnew_g, pi)
-                                    : staged_row(P, parts, H, t, slot, lr, pn, pnew_g, pi);
+            const double vi = first ? staged_row<true>(P, parts, H, t, slot, lr, r1, pnew_g, pi)
+                                    : staged_row<true>(P, parts, H, t, slot, lr, pn, pnew_g, pi);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
               pout[i] = pi;
               vout[i] = vi;
+              hpush(P, parts, pa ? kMp0 : kMp1, i, pi);
+              hpush(P, parts, pa ? kMv0 : kMv1, i, vi);
               acc[0] = __dadd_rn(acc[0], __dmul_rn(t.tail(0)[lr], vi));
             }
           } else if (lr < H.rows) {
@@ -1187,6 +1228,8 @@ __global__ void LRB_STREAM_BOUNDS
             const double vi = row_spmv(P, parts, i, pnew_g);
             pout[i] = pi;
             vout[i] = vi;
+            hpush(P, parts, pa ? kMp0 : kMp1, i, pi);
+            hpush(P, parts, pa ? kMv0 : kMv1, i, vi);
             acc[0] = __dadd_rn(acc[0], __dmul_rn(P.rhat[i], vi));
           }
         });
@@ -1212,7 +1255,7 @@ __global__ void LRB_STREAM_BOUNDS
             const Slots slot = slice_slots(st, H, sl);
             const SBiCG sv{t.w(0), t.w(1), alpha};
             double si;
-            const double ti = staged_row(P, parts, H, t, slot, lr, sv, sval_g, si);
+            const double ti = staged_row<true>(P, parts, H, t, slot, lr, sv, sval_g, si);
             if (lr < H.rows) {
               const int64_t i = H.row0 + lr;
               P.s[i] = si;
@@ -1246,9 +1289,13 @@ __global__ void LRB_STREAM_BOUNDS
           const double s = V[1][lr];
           const double x = __dadd_rn(__dadd_rn(V[2][lr], __dmul_rn(alpha, V[0][lr])), __dmul_rn(omega, s));
           const double r = __dsub_rn(s, __dmul_rn(omega, V[3][lr]));
-          (pa ? P.p1 : P.p0)[i] = __dsub_rn(V[0][lr], __dmul_rn(omega, V[5][lr]));
+          const double u = __dsub_rn(V[0][lr], __dmul_rn(omega, V[5][lr]));
+          (pa ? P.p1 : P.p0)[i] = u;
           P.x[i] = x;
           P.r[i] = r;
+          hpush(P, parts, pa ? kMp1 : kMp0, i, u);
+          hpush(P, parts, kMx, i, x);
+          hpush(P, parts, kMr, i, r);
           acc[0] = __dadd_rn(acc[0], __dmul_rn(r, r));
           acc[1] = __dadd_rn(acc[1], __dmul_rn(V[4][lr], r));
         });
@@ -1267,7 +1314,7 @@ __global__ void LRB_STREAM_BOUNDS
             if (H.tma) {
               const StagedTile t = staged_tile(st, H, 1);
               const Slots slot = slice_slots(st, H, lr >> 5);
-              const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+              const double ax = staged_row<true>(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
               if (lr < H.rows) {
                 const double d = __dsub_rn(t.tail(0)[lr], ax);
                 acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));

@@ -184,6 +184,19 @@ class DevicePart:
             lv, nv = self._values_cache
         return {"local": lv.copy(), "non_local": nv.copy()}
 
+    def write_values(self, which, values):
+        """Write one block ("local" / "non_local") in the reference's row-major
+        order into the device part (lrb_part_write_values); dinv follows."""
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        want = self.plan.nnz_local if which == "local" else self.plan.nnz_nonlocal
+        if len(values) != want:
+            raise ValueError(f"{which} values: expected {want}, got {len(values)}")
+        lp, np_ = (N.ptr(values), None) if which == "local" else (None, N.ptr(values))
+        N.check(N.lrb_part_write_values(self.h, lp, np_))
+        with self._lock:
+            self._version += 1
+            self._values_cache = None
+
     def join(self):
         N.check(N.lrb_part_join(self.h))
 
@@ -277,9 +290,10 @@ class Team:
 
     def kernel_info(self, method):
         """Solve-kernel geometry on device rank 0 (lrb_team_kernel_info)."""
-        out = np.zeros(6, np.int64)
+        out = np.zeros(8, np.int64)
         N.check(N.lrb_team_kernel_info(self.h, N.METHODS[method], N.ptr(out)))
-        keys = ("streaming", "grid", "block", "stages", "stage_bytes", "smem")
+        keys = ("streaming", "grid", "block", "stages", "stage_bytes", "smem", "halo_mirrors",
+                "push_runs")
         return dict(zip(keys, (int(v) for v in out)))
 
     def profile(self, cap):

@@ -309,3 +309,35 @@ def test_cross_device_protocol_on_one_gpu():
     assert pcg[1].iterations == split4[1].iterations
     for a, b in zip(pcg[0], split4[0]):
         assert np.array_equal(a, b)
+
+
+def test_vals_write_through():
+    """matrix.local/non_local.vals stay writable (reference tests/test_core.py:121):
+    scaling both blocks by 2 in place rewrites the device values and the Jacobi
+    diagonal, so Jacobi-PCG on 2A returns exactly x/2 in the same iterations."""
+    _, asm, pm = cavity_case((12, 12, 12), 4, 2)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 3), "direct")
+        out = None
+        if s.is_owner:
+            b = np.ones(s.matrix.n_owned)
+            x1, r1 = lrb.cg_solve(s.matrix, s.halo, b, 1e-8, 500, s.comm, method="pcg")
+            lv0, nv0 = s.matrix.local.vals.copy(), s.matrix.non_local.vals.copy()
+            v = s.matrix.local.vals
+            v *= 2.0
+            w = s.matrix.non_local.vals
+            w *= 2.0
+            ok = np.array_equal(s.matrix.local.vals, 2 * lv0) and \
+                np.array_equal(s.matrix.non_local.vals, 2 * nv0)
+            x2, r2 = lrb.cg_solve(s.matrix, s.halo, b, 1e-8, 500, s.comm, method="pcg")
+            one = s.matrix.local.vals
+            one[0] = 123.0
+            ok &= s.matrix.local.vals[0] == 123.0
+            out = ok, np.array_equal(x2, x1 / 2), r1.iterations == r2.iterations
+        return out
+
+    for r in lrb.run_world(4, program):
+        if r is not None:
+            assert all(r), r
