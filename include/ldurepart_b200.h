@@ -138,6 +138,18 @@ int lrb_part_read_values(lrb_part* part, double* local_vals, double* nonlocal_va
  * diagonal.  Backs the drop-in's writable DistributedCooMatrix .vals (the
  * reference keeps CooMatrix values writable by design, tests/test_core.py:121). */
 int lrb_part_write_values(lrb_part* part, const double* local_vals, const double* nonlocal_vals);
+/* GPU-side producer (the paper's "refactoring approach",
+ * PAPER.md:23-27).  lrb_part_capture_base copies the receive buffer as it is
+ * now (the pristine base coefficients, e.g. right after repartition) into a
+ * caller-owned device buffer of 8 * n_buf bytes; lrb_update_perturb then
+ * produces a timestep's values on the device — the base with every diagonal
+ * scaled by diag_scale, which is perturb_coefficients (assembly.py:225-243)
+ * for diag_scale = 1 + step/100 — fused with the scatter, ordered on the
+ * part's solve stream.  Values equal the host path bit for bit; no
+ * coefficients cross PCIe.  The receive buffer keeps the last transferred
+ * values. */
+int lrb_part_capture_base(lrb_part* part, void* dev_buf, int64_t bytes);
+int lrb_update_perturb(lrb_part* part, double diag_scale);
 /* Make the part's solve stream wait for all pending segment scatters. */
 int lrb_part_join(lrb_part* part);
 int lrb_part_sync(lrb_part* part);

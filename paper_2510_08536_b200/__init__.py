@@ -24,7 +24,8 @@ from .repart import (RepartitionedSystem, ScatterMap, SparsityPattern, UpdatePat
                      extract_sparsity, fuse_patterns, pack_order_pairs, repartition,
                      sparsity_fingerprint)
 from .update import (PackedCoefficients, PatternDriftError, TRANSFER_MODES, apply_scatter,
-                     pack_coefficients, transfer_coefficients, update)
+                     capture_device_base, pack_coefficients, transfer_coefficients, update,
+                     update_on_device)
 
 __version__ = "0.1.0"
 from .verify import gather_global, read_curves_csv, write_curves_csv  # noqa: E402

@@ -81,6 +81,8 @@ lrb_part_fill = _sig("lrb_part_fill", C.c_int, P, I64, P, I64)
 lrb_part_read_buffer = _sig("lrb_part_read_buffer", C.c_int, P, P)
 lrb_part_read_values = _sig("lrb_part_read_values", C.c_int, P, P, P)
 lrb_part_write_values = _sig("lrb_part_write_values", C.c_int, P, P, P)
+lrb_part_capture_base = _sig("lrb_part_capture_base", C.c_int, P, P, I64)
+lrb_update_perturb = _sig("lrb_update_perturb", C.c_int, P, D)
 lrb_part_join = _sig("lrb_part_join", C.c_int, P)
 lrb_part_sync = _sig("lrb_part_sync", C.c_int, P)
 lrb_part_stats = _sig("lrb_part_stats", C.c_int, P, P)
@@ -118,7 +120,7 @@ EXPORTED = [
     "lrb_team_connect_ipc", "lrb_team_read_vector", "lrb_team_debug", "lrb_team_kernel_info",
     "lrb_team_profile", "lrb_team_profile_read", "lrb_team_profile_counters",
     "lrb_update_segment_async", "lrb_team_solve_async", "lrb_team_spmv_async",
-    "lrb_part_write_values",
+    "lrb_part_write_values", "lrb_part_capture_base", "lrb_update_perturb",
 ]
 
 

@@ -114,6 +114,7 @@ struct lrb_part {
   // [2] H2D bytes, [3] scatter launches
   std::atomic<int64_t> stats[4] = {0, 0, 0, 0};
   std::mutex mu;
+  double* base = nullptr;           // device copy of the base receive buffer (lrb_part_capture_base)
 };
 
 namespace lrb {
@@ -345,12 +346,25 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
     // previous copy out of this stage slice must have landed
     LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
     LRB_CUDA(cudaEventSynchronize(part->stage_free));
-    int64_t o = 0;
+    // pipelined: host-copy chunk c into the pinned stage while the copy engine
+    // moves chunk c-1 (the host memcpy and the DMA overlap instead of adding)
+    constexpr int64_t kChunkDoubles = int64_t(1) << 19;   // 4 MB
+    int64_t o = 0, sent = 0;
     for (int i = 0; i < n_pieces; ++i) {
-      if (piece_len[i]) std::memcpy(part->stage + off + o, pieces[i], 8 * piece_len[i]);
-      o += piece_len[i];
+      for (int64_t a = 0; a < piece_len[i];) {
+        const int64_t take = std::min(piece_len[i] - a, kChunkDoubles - (o - sent));
+        std::memcpy(part->stage + off + o, pieces[i] + a, 8 * take);
+        a += take;
+        o += take;
+        if (o - sent == kChunkDoubles) {
+          LRB_CUDA(cudaMemcpyAsync(dst + sent, part->stage + off + sent, 8 * (o - sent),
+                                   cudaMemcpyHostToDevice, st));
+          sent = o;
+        }
+      }
     }
-    if (len) LRB_CUDA(cudaMemcpyAsync(dst, part->stage + off, 8 * len, cudaMemcpyHostToDevice, st));
+    if (o > sent)
+      LRB_CUDA(cudaMemcpyAsync(dst + sent, part->stage + off + sent, 8 * (o - sent), cudaMemcpyHostToDevice, st));
   }
   LRB_CUDA(cudaEventRecord(part->seg_h2d[seg], st));
   if (!part->seg_rows.empty()) {
@@ -523,6 +537,36 @@ int lrb_part_write_values(lrb_part* part, const double* local_vals, const double
   g_launches.fetch_add(1, std::memory_order_relaxed);
   LRB_CUDA(cudaStreamSynchronize(part->main));
   LRB_CUDA(cudaEventRecord(part->main_done, part->main));
+  return LRB_OK;
+}
+
+int lrb_part_capture_base(lrb_part* part, void* dev_buf, int64_t bytes) {
+  if (!part || !dev_buf || bytes < 8 * part->d.n_buf) {
+    set_error("lrb_part_capture_base: need a device buffer of 8 * n_buf bytes");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  part->base = static_cast<double*>(dev_buf);
+  if (part->d.n_buf)
+    LRB_CUDA(cudaMemcpyAsync(part->base, part->d.recv, 8 * part->d.n_buf, cudaMemcpyDeviceToDevice,
+                             part->main));
+  LRB_CUDA(cudaStreamSynchronize(part->main));
+  return LRB_OK;
+}
+
+int lrb_update_perturb(lrb_part* part, double diag_scale) {
+  if (!part || !part->base) {
+    set_error("lrb_update_perturb: no captured base coefficients (lrb_part_capture_base)");
+    return LRB_EVALUE;
+  }
+  int rc = lrb_part_join(part);
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  LRB_CUDA(perturb_launch(part->d, part->base, diag_scale, part->main));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  part->stats[3] += 1;
   return LRB_OK;
 }
 

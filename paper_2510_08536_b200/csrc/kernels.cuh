@@ -332,6 +332,62 @@ __device__ __forceinline__ void part_value(const TeamDev& T, int p, int K, doubl
   __syncthreads();
 }
 
+// All local parts' values in one pass (several parts per device, e.g. C2 /
+// C5 on one GPU): warp tasks (part q, lane group g) over the CTA's warps, the
+// canonical lane values and group butterflies exactly as part_value, group
+// sums parked in `scratch` (shared memory the caller owns and does not need
+// across the barrier), then thread q sums part q's groups in group order.
+// Two block barriers in total instead of two per part.  Out of line: it runs
+// only in the barrier's last CTA and must not perturb the register
+// allocation of the phase bodies.  scratch: [nloc * NR] part values followed
+// by [nloc * kLaneGroups * NR] group sums.
+template <int NR>
+__device__ __noinline__ void parts_values(const TeamDev& T, int K, double* scratch) {
+  const int nloc = T.part_end - T.part_begin;
+  double* grp = scratch + nloc * NR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = int(blockDim.x >> 5);
+  for (int task = warp; task < nloc * kLaneGroups; task += nw) {
+    const int q = task / kLaneGroups, g = task - q * kLaneGroups;
+    const int p = T.part_begin + q;
+    const PartDev& P = T.parts[p];
+    double acc[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+    const int v = g * 32 + lane;
+    if (v < kLanes) {
+      if (lanes_by_cta(T, P.ntiles, K)) {
+        const double* lv = T.lane_vals + (size_t(q) * kLanes + v) * kMaxRed;
+        if (v < int(gridDim.x))
+#pragma unroll
+          for (int j = 0; j < NR; ++j) acc[j] = __ldcg(lv + j);
+      } else {
+        lane_from_partials<NR>(T, P, K, v, acc);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) grp[(q * kLaneGroups + g) * NR + j] = acc[j];
+  }
+  __syncthreads();
+  if (int(threadIdx.x) < nloc) {
+    const int q = threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double s = grp[(q * kLaneGroups) * NR + j];
+      for (int g = 1; g < kLaneGroups; ++g) s = __dadd_rn(s, grp[(q * kLaneGroups + g) * NR + j]);
+      scratch[q * NR + j] = s;
+    }
+  }
+  // the scratch is the bulk-copy ring of the streaming kernels: order these
+  // generic writes before the next phase's async-proxy copies into it
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+}
+
 __device__ __forceinline__ int64_t tile_first(const TeamDev& T) {
   return LRB_CONTIG ? int64_t(blockIdx.x) * T.n_tiles / gridDim.x : int64_t(blockIdx.x);
 }
@@ -374,7 +430,7 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // the CTA's writes through the preceding __syncthreads).
 constexpr int kSmemParts = 16;
 template <int NR>
-__device__ void team_sync(const TeamDev& T, double* red, int K) {
+__device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch = nullptr) {
   __shared__ unsigned s_last, s_gen;
   __shared__ double gs[kLaneGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
@@ -396,8 +452,17 @@ __device__ void team_sync(const TeamDev& T, double* red, int K) {
     // e+2 before our flag for e+1, i.e. before we finished reading e.
     const unsigned long long e_next = (T.n_dev > 1) ? *(volatile unsigned long long*)T.epoch + 1 : 0;
     const int64_t pbuf = int64_t(e_next & 1) * T.n_parts * kMaxRed;
+    // several local parts: all their values in one pass (parts_values)
+    const bool batched = scratch != nullptr && T.part_end - T.part_begin > 1;
+    if (batched) parts_values<NR>(T, K, scratch);
     for (int p = T.part_begin; p < T.part_end; ++p) {
-      part_value<NR>(T, p, K, gs, pv);
+      if (batched) {
+        if (threadIdx.x == 0)
+#pragma unroll
+          for (int j = 0; j < NR; ++j) pv[j] = scratch[(p - T.part_begin) * NR + j];
+      } else {
+        part_value<NR>(T, p, K, gs, pv);
+      }
 #ifdef LRB_STAMP3
       if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
 #endif

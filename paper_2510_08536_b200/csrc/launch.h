@@ -12,6 +12,8 @@ namespace lrb {
 
 // Scatter of rows [r0, r1) of part P on stream st (scatter.cu).
 cudaError_t scatter_launch(const PartDev& P, int64_t r0, int64_t r1, cudaStream_t st);
+// Fused GPU-side perturb_coefficients + scatter from a device copy of the base buffer.
+cudaError_t perturb_launch(const PartDev& P, const double* base, double scale, cudaStream_t st);
 // dinv from the diagonal values (after lrb_part_write_values).
 cudaError_t dinv_refresh_launch(const PartDev& P, cudaStream_t st);
 

@@ -58,6 +58,45 @@ __global__ void __launch_bounds__(kScTPB) scatter_rows_kernel(PartDev P, int64_t
   scatter_row(P, i);
 }
 
+// GPU-side producer of the reference's pseudo-timestep (perturb_coefficients,
+// assembly.py:225-243: diag scaled by (1 + step/100), everything else the
+// pristine base) fused with the scatter: val[e] = base[src[e]], times `scale`
+// on the row's diagonal slot (correctly rounded, like numpy's m.diag * f),
+// dinv refreshed.  No host coefficients move (the paper's
+// "refactoring approach").  20 B per entry, like the scatter.
+__global__ void __launch_bounds__(kScTPB) perturb_rows_kernel(PartDev P, const double* __restrict__ base,
+                                                               double scale) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P.n) return;
+  const RowRef rr = row_ref(P, i);
+  const int dk = __ldg(P.dpos + i);
+  for (int k0 = 0; k0 < rr.w; k0 += kScChunk) {
+    int b[kScChunk];
+    double v[kScChunk];
+#pragma unroll
+    for (int u = 0; u < kScChunk; ++u)
+      b[u] = (k0 + u < rr.w) ? __ldg(P.src + rr.base + int64_t(k0 + u) * kSlice) : -1;
+#pragma unroll
+    for (int u = 0; u < kScChunk; ++u) v[u] = b[u] >= 0 ? __ldg(base + b[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kScChunk; ++u) {
+      if (b[u] < 0) continue;
+      double x = v[u];
+      if (k0 + u == dk) {
+        x = __dmul_rn(x, scale);
+        P.dinv[i] = 1.0 / x;
+      }
+      P.val[rr.base + int64_t(k0 + u) * kSlice] = x;
+    }
+  }
+}
+
+cudaError_t perturb_launch(const PartDev& P, const double* base, double scale, cudaStream_t st) {
+  if (P.n <= 0) return cudaSuccess;
+  perturb_rows_kernel<<<unsigned((P.n + kScTPB - 1) / kScTPB), kScTPB, 0, st>>>(P, base, scale);
+  return cudaGetLastError();
+}
+
 // Jacobi refresh after values were written directly (lrb_part_write_values):
 // dinv[i] = 1 / val[diagonal slot of row i].
 __global__ void __launch_bounds__(kScTPB) dinv_refresh_kernel(PartDev P) {

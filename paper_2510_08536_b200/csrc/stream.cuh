@@ -881,7 +881,9 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
   const int K = ELEM ? pack_factor(T, ntv) : 1;
-  team_sync<NR>(T, red, K);
+  // the ring is idle here (every stage of the phase was consumed): its shared
+  // memory is the scratch of the multi-part barrier reduction
+  team_sync<NR>(T, red, K, reinterpret_cast<double*>(S.stages));
   if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
   gseq += stage_count(ELEM ? (T.n_tiles + K - 1) / K : T.n_tiles);
 }

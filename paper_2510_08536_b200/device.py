@@ -184,6 +184,18 @@ class DevicePart:
             lv, nv = self._values_cache
         return {"local": lv.copy(), "non_local": nv.copy()}
 
+    def capture_base(self):
+        """Keep a device copy of the receive buffer as it is now (the base
+        coefficients) for update_perturb (lrb_part_capture_base)."""
+        torch = _torch()
+        self.base = torch.empty(max(self.n_buf, 1), dtype=torch.float64, device=f"cuda:{self.device}")
+        N.check(N.lrb_part_capture_base(self.h, self.base.data_ptr(), 8 * self.base.numel()))
+
+    def update_perturb(self, diag_scale):
+        """Device-side perturb_coefficients + scatter (lrb_update_perturb)."""
+        N.check(N.lrb_update_perturb(self.h, float(diag_scale)))
+        self._touch()
+
     def write_values(self, which, values):
         """Write one block ("local" / "non_local") in the reference's row-major
         order into the device part (lrb_part_write_values); dinv follows."""

@@ -341,3 +341,59 @@ def test_vals_write_through():
     for r in lrb.run_world(4, program):
         if r is not None:
             assert all(r), r
+
+
+def test_update_on_device_equals_host_update():
+    """GPU-side perturb_coefficients installs the host path's
+    values bit for bit, step after step, in either order with host updates."""
+    _, asm, pm = cavity_case((12, 12, 12), 8, 4)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.capture_device_base(s)
+        ok = True
+        for step in (2, 3, 7, 20):
+            lrb.update_on_device(s, step)
+            dev = (s.matrix.local.vals.copy(), s.matrix.non_local.vals.copy()) if s.is_owner else None
+            lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], step), "direct")
+            if s.is_owner:
+                ok &= np.array_equal(dev[0], s.matrix.local.vals)
+                ok &= np.array_equal(dev[1], s.matrix.non_local.vals)
+        if s.is_owner:   # the Jacobi diagonal follows: PCG equals the host-updated solve
+            lrb.update_on_device(s, 5)
+            xa, ra = lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), 1e-8, 500, s.comm,
+                                  method="pcg")
+        else:
+            lrb.update_on_device(s, 5)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 5), "direct")
+        if s.is_owner:
+            xb, rb = lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), 1e-8, 500, s.comm,
+                                  method="pcg")
+            ok &= np.array_equal(xa, xb) and ra.iterations == rb.iterations
+        return ok
+
+    assert all(lrb.run_world(8, program))
+    with pytest.raises(ValueError, match="step must be >= 1"):
+        lrb.update_on_device(None, 0)
+
+
+def test_pageable_update_chunked_pipeline_values():
+    """Pageable inputs larger than the 4 MB host-copy chunk (the pipelined
+    stage path) land bit-exactly."""
+    _, asm, pm = cavity_case((64, 64, 64), 2, 2)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        m, ifs = lrb.perturb_coefficients(*asm[ctx.rank], 9)    # fresh pageable arrays
+        lrb.update(s, m, ifs, "direct")
+        if s.is_owner:
+            st = s.part.stats()
+            return st["pageable_pieces"] > 0, s.matrix.local.vals, s.matrix.non_local.vals
+        return None
+
+    res = lrb.run_world(2, program)
+    probs = [ocav.perturb(p, 9) for p in ocav.cavity_problems((64, 64, 64), 2)]
+    pipe = OraclePipeline(probs, pm.offsets, 2)
+    staged, lv, nv = res[0]
+    assert staged
+    assert np.array_equal(lv, pipe.values[0][0]) and np.array_equal(nv, pipe.values[0][1])
