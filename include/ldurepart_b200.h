@@ -115,6 +115,17 @@ int lrb_part_pointers(const lrb_part* part, void** ptrs /* [16] */);
  * Returns once the host pieces may be reused (H2D complete). */
 int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces,
                        const double* const* pieces, const int64_t* piece_len);
+/* The direct update split at its two owners (update.py:72-83 + 105-112): a
+ * source rank uploads its segment into the receive buffer (returns when its
+ * pieces may be reused; never waits for the owner — the solve does not read
+ * the receive buffer), and the owner, once its previous solve is done,
+ * scatters every uploaded segment on that segment's stream.  The drop-in's
+ * update() orders the two by update epochs, so a source's upload of the next
+ * system overlaps the owner's solves of another (C4: pressure coefficients
+ * during the momentum solves). */
+int lrb_upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                       const int64_t* piece_len);
+int lrb_scatter_segment(lrb_part* part, int32_t seg);
 /* Staged update (update.py:85-102): the owner copies all sources' pieces
  * into the pinned stage, then one H2D of the whole buffer and the scatter. */
 int lrb_update_staged(lrb_part* part, int32_t n_pieces, const double* const* pieces,

@@ -110,6 +110,7 @@ struct lrb_part {
   double* stage = nullptr;          // pinned, n_buf doubles (caller-owned)
   int64_t stage_len = 0;
   cudaEvent_t stage_free = nullptr; // last H2D from the whole-buffer stage
+  cudaEvent_t staged_done = nullptr; // after the last whole-buffer (staged / fill) scatter on main
   // [0] pinned pieces copied zero-copy, [1] pageable pieces staged,
   // [2] H2D bytes, [3] scatter launches
   std::atomic<int64_t> stats[4] = {0, 0, 0, 0};
@@ -220,6 +221,8 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   }
   LRB_CUDA(cudaEventCreateWithFlags(&part->main_done, cudaEventDisableTiming));
   LRB_CUDA(cudaEventCreateWithFlags(&part->stage_free, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventCreateWithFlags(&part->staged_done, cudaEventDisableTiming));
+  LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
   LRB_CUDA(cudaEventCreate(&part->mark_a));
   LRB_CUDA(cudaEventCreate(&part->mark_b));
   part->seg_off = P.seg_off;
@@ -280,6 +283,7 @@ void lrb_part_destroy(lrb_part* part) {
     for (auto e : part->seg_done) cudaEventDestroy(e);
     cudaEventDestroy(part->main_done);
     cudaEventDestroy(part->stage_free);
+    cudaEventDestroy(part->staged_done);
     cudaEventDestroy(part->mark_a);
     cudaEventDestroy(part->mark_b);
     cudaStreamDestroy(part->main);
@@ -312,10 +316,14 @@ static int check_pieces(lrb_part* part, int64_t expect, int32_t n_pieces, const 
   return LRB_OK;
 }
 
-int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
-                       const int64_t* piece_len) {
+// H2D of one source segment into the receive buffer (pinned pieces straight,
+// pageable ones through the part's pinned stage in overlapped chunks), on
+// the segment's stream; returns once the host pieces may be reused.  No
+// ordering against the solve: the solve never reads the receive buffer.
+static int upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                          const int64_t* piece_len, const char* who) {
   if (!part || seg < 0 || seg >= int(part->seg_stream.size())) {
-    set_error("lrb_update_segment: bad segment");
+    set_error(std::string(who) + ": bad segment");
     return LRB_EVALUE;
   }
   const int64_t off = part->seg_off[seg], len = part->seg_off[seg + 1] - off;
@@ -323,8 +331,9 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
   if (rc) return rc;
   DeviceGuard g(part->device);
   cudaStream_t st = part->seg_stream[seg];
-  // the scatter below rewrites values the last solve may still read
-  LRB_CUDA(cudaStreamWaitEvent(st, part->main_done, 0));
+  // a whole-buffer scatter on the solve stream (staged update) may still read
+  // the receive buffer
+  LRB_CUDA(cudaStreamWaitEvent(st, part->staged_done, 0));
   bool all_pinned = true;
   for (int i = 0; i < n_pieces && all_pinned; ++i)
     if (piece_len[i]) all_pinned = is_pinned(pieces[i]);
@@ -340,7 +349,7 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
     }
   } else {
     if (!part->stage || part->stage_len < part->seg_off.back()) {
-      set_error("lrb_update_segment: pageable input needs a pinned stage");
+      set_error(std::string(who) + ": pageable input needs a pinned stage");
       return LRB_EVALUE;
     }
     // previous copy out of this stage slice must have landed
@@ -367,18 +376,52 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
       LRB_CUDA(cudaMemcpyAsync(dst + sent, part->stage + off + sent, 8 * (o - sent), cudaMemcpyHostToDevice, st));
   }
   LRB_CUDA(cudaEventRecord(part->seg_h2d[seg], st));
+  return LRB_OK;
+}
+
+// Scatter of one segment on its stream, after the last solve on the part.
+static int scatter_segment(lrb_part* part, int32_t seg) {
+  DeviceGuard g(part->device);
+  cudaStream_t st = part->seg_stream[seg];
+  // the scatter rewrites values the last solve may still read
+  LRB_CUDA(cudaStreamWaitEvent(st, part->main_done, 0));
   if (!part->seg_rows.empty()) {
-    rc = launch_scatter(part, part->seg_rows[seg], part->seg_rows[seg + 1], st);
+    int rc = launch_scatter(part, part->seg_rows[seg], part->seg_rows[seg + 1], st);
     if (rc) return rc;
   }
+  std::lock_guard<std::mutex> lk(part->mu);
   LRB_CUDA(cudaEventRecord(part->seg_done[seg], st));
-  {
-    std::lock_guard<std::mutex> lk(part->mu);
-    part->seg_pending[seg] = 1;
-  }
+  part->seg_pending[seg] = 1;
+  return LRB_OK;
+}
+
+int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                       const int64_t* piece_len) {
+  int rc = upload_segment(part, seg, n_pieces, pieces, piece_len, "lrb_update_segment");
+  if (rc) return rc;
+  rc = scatter_segment(part, seg);
+  if (rc) return rc;
   // host pieces are reusable once the copy has landed
+  DeviceGuard g(part->device);
   LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
   return LRB_OK;
+}
+
+int lrb_upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
+                       const int64_t* piece_len) {
+  int rc = upload_segment(part, seg, n_pieces, pieces, piece_len, "lrb_upload_segment");
+  if (rc) return rc;
+  DeviceGuard g(part->device);
+  LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
+  return LRB_OK;
+}
+
+int lrb_scatter_segment(lrb_part* part, int32_t seg) {
+  if (!part || seg < 0 || seg >= int(part->seg_stream.size())) {
+    set_error("lrb_scatter_segment: bad segment");
+    return LRB_EVALUE;
+  }
+  return scatter_segment(part, seg);
 }
 
 int lrb_part_join(lrb_part* part) {
@@ -398,6 +441,7 @@ int lrb_part_join(lrb_part* part) {
   if (any && part->seg_rows.empty()) {
     int rc = launch_scatter(part, 0, part->d.n, part->main);
     if (rc) return rc;
+    LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
   }
   return LRB_OK;
 }
@@ -431,6 +475,7 @@ int lrb_update_staged(lrb_part* part, int32_t n_pieces, const double* const* pie
   LRB_CUDA(cudaEventRecord(part->stage_free, part->main));
   rc = launch_scatter(part, 0, part->d.n, part->main);
   if (rc) return rc;
+  LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
   LRB_CUDA(cudaEventSynchronize(part->stage_free));
   return LRB_OK;
 }
@@ -467,7 +512,10 @@ int lrb_apply_scatter(lrb_part* part) {
   int rc = lrb_part_join(part);
   if (rc) return rc;
   DeviceGuard g(part->device);
-  return launch_scatter(part, 0, part->d.n, part->main);
+  rc = launch_scatter(part, 0, part->d.n, part->main);
+  if (rc) return rc;
+  LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
+  return LRB_OK;
 }
 
 int lrb_part_fill(lrb_part* part, int64_t offset, const double* values, int64_t n) {

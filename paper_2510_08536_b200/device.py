@@ -122,6 +122,11 @@ class DevicePart:
         self._values_cache = None
         self._version = 0
         self._lock = threading.Lock()
+        # update epochs per segment (drop-in update(), direct mode): the last
+        # epoch whose upload / scatter has been enqueued; repartition's
+        # initial transfer is epoch 0
+        self.seg_h2d_epoch = [0] * plan.n_seg
+        self.seg_scat_epoch = [0] * plan.n_seg
 
     # ---- update path -----------------------------------------------------
     @staticmethod
@@ -134,6 +139,16 @@ class DevicePart:
     def update_segment(self, seg, pieces):
         arrs, ptrs, lens = self._pieces(pieces)
         N.check(N.lrb_update_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
+        self._touch()
+
+    def upload_segment(self, seg, pieces):
+        """H2D of one source segment only (lrb_upload_segment)."""
+        arrs, ptrs, lens = self._pieces(pieces)
+        N.check(N.lrb_upload_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
+
+    def scatter_segment(self, seg):
+        """The owner's scatter of one uploaded segment (lrb_scatter_segment)."""
+        N.check(N.lrb_scatter_segment(self.h, seg))
         self._touch()
 
     def update_segment_async(self, seg, pieces, stream=0):

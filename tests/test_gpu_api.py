@@ -397,3 +397,41 @@ def test_pageable_update_chunked_pipeline_values():
     staged, lv, nv = res[0]
     assert staged
     assert np.array_equal(lv, pipe.values[0][0]) and np.array_equal(nv, pipe.values[0][1])
+
+
+def test_two_systems_interleaved_updates_and_solves():
+    """C4's flow (momentum + pressure systems on the same ranks): sources
+    upload the second system's coefficients while the owner is still solving
+    the first (update epochs, no owner-group barrier); every value and solve
+    equals a fresh repartition of the same step."""
+    _, asm, pm = cavity_case((16, 16, 16), 8, 4)
+
+    def program(ctx):
+        base = asm[ctx.rank]
+        sa = lrb.repartition(*base, pm, ctx)
+        sb = lrb.repartition(*base, pm, ctx)
+        ok = True
+        for step in range(2, 8):
+            ma = lrb.perturb_coefficients(*base, step)
+            mb = lrb.perturb_coefficients(*base, step + 30)
+            lrb.update(sa, *ma, "direct" if step != 5 else "staged")
+            if sa.is_owner:
+                xa, _ = lrb.cg_solve(sa.matrix, sa.halo, np.ones(sa.matrix.n_owned), 1e-8, 500,
+                                     sa.comm, method="pcg")
+            lrb.update(sb, *mb, "direct")
+            if sb.is_owner:
+                xb, _ = lrb.cg_solve(sb.matrix, sb.halo, np.ones(sb.matrix.n_owned), 1e-8, 500,
+                                     sb.comm)
+            fa = lrb.repartition(*ma, pm, ctx)
+            fb = lrb.repartition(*mb, pm, ctx)
+            if sa.is_owner:
+                ok &= np.array_equal(sa.matrix.local.vals, fa.matrix.local.vals)
+                ok &= np.array_equal(sb.matrix.non_local.vals, fb.matrix.non_local.vals)
+                ya, _ = lrb.cg_solve(fa.matrix, fa.halo, np.ones(fa.matrix.n_owned), 1e-8, 500,
+                                     fa.comm, method="pcg")
+                yb, _ = lrb.cg_solve(fb.matrix, fb.halo, np.ones(fb.matrix.n_owned), 1e-8, 500,
+                                     fb.comm)
+                ok &= np.array_equal(xa, ya) and np.array_equal(xb, yb)
+        return ok
+
+    assert all(lrb.run_world(8, program))

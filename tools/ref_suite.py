@@ -7,7 +7,9 @@
     python tools/ref_suite.py [pytest args] [--files test_repart.py ...]
 
 The alias maps ``ldurepart`` and its submodules (core, repart, update, solver,
-transport) to paper_2510_08536_b200.  The reference's verification helpers
+transport, assembly) to paper_2510_08536_b200; the reference's own cli.py and
+costmodel.py (out of scope) are loaded unmodified as submodules of the alias,
+so test_acceptance's case sweeps drive the B200 path.  The reference's verification helpers
 (``ldurepart.oracle``: reference_global_assemble, compare_matrices, to_csr,
 ...) are checkers, out of this repo's scope; they are taken
 from the unmodified reference installed in baseline/_ref.  Nothing in the
@@ -53,7 +55,12 @@ def _load_reference_package():
 def install_alias():
     sys.path.insert(0, ROOT)
     import paper_2510_08536_b200 as lrb
-    from paper_2510_08536_b200 import core, repart, solver, transport, update
+    import importlib
+    # submodules by import path (the package namespace re-exports functions of
+    # the same names, e.g. update)
+    core, repart, solver, transport, update = (
+        importlib.import_module(f"paper_2510_08536_b200.{m}")
+        for m in ("core", "repart", "solver", "transport", "update"))
     ref = _load_reference_package()
     alias = types.ModuleType("ldurepart")
     alias.__dict__.update({k: v for k, v in vars(lrb).items() if not k.startswith("__")})
@@ -65,10 +72,35 @@ def install_alias():
             setattr(alias, name, getattr(oracle, name))
     alias.oracle = oracle
     sys.modules["ldurepart"] = alias
+    cavity = importlib.import_module("paper_2510_08536_b200.cavity")
     for name, mod in (("core", core), ("repart", repart), ("solver", solver),
-                      ("transport", transport), ("update", update), ("oracle", oracle)):
+                      ("transport", transport), ("update", update), ("oracle", oracle),
+                      ("assembly", cavity)):
         sys.modules[f"ldurepart.{name}"] = mod
+        if not hasattr(alias, name):   # lr.update stays the function, as in the reference
+            setattr(alias, name, mod)
+    # the reference's driver and cost model (out of this repo's scope, SURVEY
+    # §2) are loaded from its unmodified sources AS submodules of the alias,
+    # so their relative imports (.repart, .update, .solver, ...) bind to the
+    # drop-in: test_acceptance's sweeps run the B200 path end to end
+    for name in ("costmodel", "cli"):
+        spec = importlib.util.spec_from_file_location(f"ldurepart.{name}",
+                                                      os.path.join(REF_PKG, f"{name}.py"))
+        mod = importlib.util.module_from_spec(spec)
+        mod.__package__ = "ldurepart"
+        sys.modules[f"ldurepart.{name}"] = mod
+        spec.loader.exec_module(mod)
         setattr(alias, name, mod)
+    # the names the reference's __init__ re-exports from them (__init__.py:25-33)
+    for name in ("CappedSpeedup", "CommCostParams", "CostCurves", "DegradingSpeedup",
+                 "IdealSpeedup", "Resources", "TabulatedSpeedup", "best_homogeneous",
+                 "load_curves_csv", "optimize_ranks", "recommend_alpha", "total_time",
+                 "total_time_hetero"):
+        if not hasattr(alias, name):
+            setattr(alias, name, getattr(sys.modules["ldurepart.costmodel"], name))
+    for name in ("BenchRecord", "CaseConfig", "run_case", "sweep"):
+        if not hasattr(alias, name):
+            setattr(alias, name, getattr(sys.modules["ldurepart.cli"], name))
     return ref
 
 
