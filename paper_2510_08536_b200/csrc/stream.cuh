@@ -109,15 +109,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
 // Spin on an mbarrier phase.  A ring that never completes is a bug, not a
 // slow peer: after timeout_ns the kernel traps (a clean launch error instead
 // of a hung device).
-template <bool HINT = true>
+// BACKOFF_NS > 0: sleep between polls (warps whose wake-up latency is not on
+// the critical path, so their polling does not take issue slots from the
+// consumers on the same SM sub-partition).
+template <bool HINT = true, int BACKOFF_NS = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity, long long timeout_ns) {
   if (mbar_try_wait<HINT>(b, parity)) return;
   const long long t0 = global_ns();
   for (unsigned k = 1;; ++k) {
+    if constexpr (BACKOFF_NS > 0) __nanosleep(BACKOFF_NS);
     if (mbar_try_wait<HINT>(b, parity)) return;
     if ((k & 15u) == 0 && global_ns() - t0 > timeout_ns) __trap();
   }
 }
+// Measured at C3 (profiles/r2_experiments.md): 64 ns for the issuers' slot
+// waits and the reducer's parked waits takes phase A 137.3 -> 135.3 us.
+#ifndef LRB_ISSUER_BACKOFF_NS
+#define LRB_ISSUER_BACKOFF_NS 64
+#endif
+#ifndef LRB_REDUCER_BACKOFF_NS
+#define LRB_REDUCER_BACKOFF_NS 64
+#endif
 // 1D bulk copy global -> shared (TMA engine), completes tx bytes on bar.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -275,7 +287,7 @@ __device__ __forceinline__ void wait_slot_free(const StreamSmem& S, int G, const
   const int Gp = G - R.ns;
   if (Gp < 0) return;
   const RingPos pp = ring_pos(Gp, R);
-  mbar_wait(S.empty + pp.bar, pp.parity, timeout_ns);
+  mbar_wait<true, LRB_ISSUER_BACKOFF_NS>(S.empty + pp.bar, pp.parity, timeout_ns);
 }
 
 // ---------------------------------------------------------------------------
@@ -825,7 +837,7 @@ __device__ __forceinline__ void reduce_phase(const TeamDev& T, const StreamSmem&
   for (int k = 0; k < count; ++k) {
     const int Gk = gseq + k;
     const WPos wp = wsum_pos(Gk);
-    mbar_wait<LRB_REDUCER_HINT>(S.parked + wp.slot, wp.parity, T.timeout_ns);
+    mbar_wait<LRB_REDUCER_HINT, LRB_REDUCER_BACKOFF_NS>(S.parked + wp.slot, wp.parity, T.timeout_ns);
     const int64_t t0 = (int64_t(blockIdx.x) + int64_t(k) * gridDim.x) * K;
     const int cnt = int(n_tiles - t0 < K ? n_tiles - t0 : K);
     if (lane < NR) {
