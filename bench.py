@@ -852,6 +852,8 @@ def run_c5(args):
     prob = Problem(N, n_cpu, layout.cpu_ranks)
     owner = DistributedOwner(layout, {r: prob.base[r] for r in layout.cpu_ranks}, solve=False)
     create_s = time.monotonic() - t0
+    for p in owner.parts:   # the pristine base, for the GPU-producer leg
+        p.capture_base()
     mx = (lambda v: max_over_ranks(v)) if world > 1 else (lambda v: v)
     sync = (lambda: torch.distributed.barrier()) if world > 1 else (lambda: None)
     log(f"[bench c5] create {create_s:.1f}s; parts {layout.parts} ranks "
@@ -894,6 +896,20 @@ def run_c5(args):
             if i >= 1:
                 rec["pg"].append((ev, wall))
             del live
+    # GPU-side producer: the timestep's coefficients made on the
+    # device from the base captured after create, fused with the scatter
+    for i, step in enumerate([2] + timed):
+        torch.cuda.synchronize()
+        sync()
+        for p in owner.parts:
+            p.mark()
+        for p in owner.parts:
+            p.update_perturb(1.0 + step / 100.0)
+        for p in owner.parts:
+            p.mark()
+        ms = mx(max(p.elapsed_ms() for p in owner.parts))
+        if i >= 1:
+            rec.setdefault("dev", []).append(ms)
     for i, step in enumerate(seq):   # value: receive buffers already in HBM
         owner.update({r: prob.produce(r, step) for r in layout.cpu_ranks}, "direct")
         for p in owner.parts:
@@ -945,6 +961,12 @@ def run_c5(args):
     }
     if n_buf_all is not None:
         line["breakdown"]["entries_all_parts"] = n_buf_all
+    if rec.get("dev"):
+        line["e2e_device_producer"] = {
+            "value": round(float(np.mean(rec["dev"])), 4), "unit": "ms/timestep",
+            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+            "what": "lrb_update_perturb per part (perturb_coefficients produced on the GPU from the "
+                    "base captured after create, fused with the scatter; SURVEY §8 f3)"}
     if rec["pg"]:
         pg = float(np.mean([e for e, _ in rec["pg"]]))
         line["e2e_pageable"] = {"value": round(pg, 4), "unit": "ms/timestep",
