@@ -442,6 +442,7 @@ int lrb_part_join(lrb_part* part) {
     int rc = launch_scatter(part, 0, part->d.n, part->main);
     if (rc) return rc;
     LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
+    LRB_CUDA(cudaEventRecord(part->main_done, part->main));
   }
   return LRB_OK;
 }
@@ -476,6 +477,7 @@ int lrb_update_staged(lrb_part* part, int32_t n_pieces, const double* const* pie
   rc = launch_scatter(part, 0, part->d.n, part->main);
   if (rc) return rc;
   LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
+  LRB_CUDA(cudaEventRecord(part->main_done, part->main));
   LRB_CUDA(cudaEventSynchronize(part->stage_free));
   return LRB_OK;
 }
@@ -515,6 +517,7 @@ int lrb_apply_scatter(lrb_part* part) {
   rc = launch_scatter(part, 0, part->d.n, part->main);
   if (rc) return rc;
   LRB_CUDA(cudaEventRecord(part->staged_done, part->main));
+  LRB_CUDA(cudaEventRecord(part->main_done, part->main));
   return LRB_OK;
 }
 
@@ -613,6 +616,8 @@ int lrb_update_perturb(lrb_part* part, double diag_scale) {
   if (rc) return rc;
   DeviceGuard g(part->device);
   LRB_CUDA(perturb_launch(part->d, part->base, diag_scale, part->main));
+  // a later segment scatter (host update) must land after these values
+  LRB_CUDA(cudaEventRecord(part->main_done, part->main));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   part->stats[3] += 1;
   return LRB_OK;
@@ -1940,6 +1945,7 @@ int lrb_update_segment_async(lrb_part* part, int32_t seg, int32_t n_pieces,
   DeviceGuard g(part->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   LRB_CUDA(cudaStreamWaitEvent(st, part->main_done, 0));
+  LRB_CUDA(cudaStreamWaitEvent(st, part->staged_done, 0));
   double* dst = part->d.recv + off;
   int64_t o = 0;
   for (int i = 0; i < n_pieces; ++i) {
