@@ -52,10 +52,42 @@ def allgather_obj(obj, group=None):
     return out
 
 
+def plumbing_backend(world: int) -> str:
+    """Process-group backend for the plumbing (blobs, barriers, timing): NCCL
+    when every process has a GPU of its own (one process per GPU over NVLink),
+    gloo when processes share a GPU (NCCL refuses duplicate devices) or there
+    is no GPU (CPU tests)."""
+    import torch
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    return "nccl" if n >= world > 1 else "gloo"
+
+
+def init_plumbing(world: int, local_rank: int) -> str:
+    """init_process_group for the multi-process path; returns the backend."""
+    import torch
+    import torch.distributed as dist
+    backend = plumbing_backend(world)
+    if backend == "nccl":
+        dev = torch.device("cuda", local_rank)
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    return backend
+
+
+def _dev():
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def max_over_ranks(value: float, group=None) -> float:
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(value)], dtype=torch.float64)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_dev())
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
 
