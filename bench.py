@@ -400,13 +400,9 @@ def run_ours(args):
             if r == 0:
                 part, team = system.part, system.team
                 part.sync()
-                part.mark()
-                part.apply_scatter()
-                part.mark()
+                t_sc = part.apply_scatter_timed()
                 _, rep, hist = team.solve(method, None, TOL, MAX_ITER, want_x=False,
                                           hist_cap=MAX_ITER)
-                t_sc = part.elapsed_ms()
-                part.mark()
                 part.sync()
                 if i >= W:
                     rec["scatter_ms"].append(t_sc)
@@ -514,13 +510,10 @@ def run_ours_multi(args):
         for p in owner.parts:
             p.sync()
         dist.barrier()
-        part.mark()
-        for p in owner.parts:
-            p.apply_scatter()
-        part.mark()
+        t_sc = owner.parts[0].apply_scatter_timed(owner.parts[1:])
         _, rep, hist = owner.team.solve(method, None, TOL, MAX_ITER, want_x=False,
                                         hist_cap=MAX_ITER)
-        t_sc = max_over_ranks(part.elapsed_ms())
+        t_sc = max_over_ranks(t_sc)
         kms = max_over_ranks(rep.device_ms)
         if i >= W:
             rec["scatter_ms"].append(t_sc)
@@ -748,10 +741,7 @@ def run_c4(args):
                 for part, team, method, rhs in ((sm.part, sm.team, "bicgstab", bs),
                                                 (sp.part, sp.team, "pcg", [bp])):
                     part.sync()
-                    part.mark()
-                    part.apply_scatter()
-                    part.mark()
-                    tot += part.elapsed_ms()
+                    tot += part.apply_scatter_timed()
                     alg += 20 * pln.n_buf
                     alg_k["scatter"] += 20 * pln.n_buf
                     for b in rhs:
@@ -919,13 +909,7 @@ def run_c5(args):
         for p in owner.parts:
             p.sync()
         sync()
-        for p in owner.parts:
-            p.mark()
-        for p in owner.parts:
-            p.apply_scatter()
-        for p in owner.parts:
-            p.mark()
-        ms = mx(max(p.elapsed_ms() for p in owner.parts))
+        ms = mx(owner.parts[0].apply_scatter_timed(owner.parts[1:]))
         if i >= W:
             rec["value"].append(ms)
     n_buf = sum(p.n_buf for p in owner.parts)

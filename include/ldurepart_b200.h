@@ -137,6 +137,10 @@ int lrb_stage_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doubl
                       const int64_t* piece_len);
 /* apply_scatter (update.py:105-112) of the whole device-resident buffer. */
 int lrb_apply_scatter(lrb_part* part);
+/* The same for n_parts parts of one device, synchronously, returning the
+ * device time from just before the first scatter launch to the end of the
+ * last (CUDA events around the launches, no host gap inside; bench `value`). */
+int lrb_apply_scatter_timed(int32_t n_parts, lrb_part* const* parts, float* device_ms);
 /* Write host values into the receive buffer (DeviceBuffer.fill, transport.py:115-123). */
 int lrb_part_fill(lrb_part* part, int64_t offset, const double* values, int64_t n);
 /* Read back the receive buffer (DeviceBuffer.values, transport.py:125-127). */

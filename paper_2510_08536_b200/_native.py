@@ -79,6 +79,7 @@ lrb_scatter_segment = _sig("lrb_scatter_segment", C.c_int, P, I32)
 lrb_update_staged = _sig("lrb_update_staged", C.c_int, P, I32, P, P)
 lrb_stage_segment = _sig("lrb_stage_segment", C.c_int, P, I32, I32, P, P)
 lrb_apply_scatter = _sig("lrb_apply_scatter", C.c_int, P)
+lrb_apply_scatter_timed = _sig("lrb_apply_scatter_timed", C.c_int, I32, P, C.POINTER(C.c_float))
 lrb_part_fill = _sig("lrb_part_fill", C.c_int, P, I64, P, I64)
 lrb_part_read_buffer = _sig("lrb_part_read_buffer", C.c_int, P, P)
 lrb_part_read_values = _sig("lrb_part_read_values", C.c_int, P, P, P)
@@ -123,7 +124,7 @@ EXPORTED = [
     "lrb_team_profile", "lrb_team_profile_read", "lrb_team_profile_counters",
     "lrb_update_segment_async", "lrb_team_solve_async", "lrb_team_spmv_async",
     "lrb_part_write_values", "lrb_part_capture_base", "lrb_update_perturb",
-    "lrb_upload_segment", "lrb_scatter_segment",
+    "lrb_upload_segment", "lrb_scatter_segment", "lrb_apply_scatter_timed",
 ]
 
 

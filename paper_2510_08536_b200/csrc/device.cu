@@ -521,6 +521,39 @@ int lrb_apply_scatter(lrb_part* part) {
   return LRB_OK;
 }
 
+int lrb_apply_scatter_timed(int32_t n_parts, lrb_part* const* parts, float* device_ms) {
+  if (n_parts < 1 || !parts || !device_ms) {
+    set_error("lrb_apply_scatter_timed: bad arguments");
+    return LRB_EVALUE;
+  }
+  for (int i = 0; i < n_parts; ++i) {
+    if (!parts[i] || parts[i]->device != parts[0]->device) {
+      set_error("lrb_apply_scatter_timed: parts must share one CUDA device");
+      return LRB_EVALUE;
+    }
+    int rc = lrb_part_join(parts[i]);
+    if (rc) return rc;
+  }
+  lrb_part* P0 = parts[0];
+  DeviceGuard g(P0->device);
+  // the start event is recorded right before the first launch and every
+  // part's stream starts behind it; the end event after all scatters
+  LRB_CUDA(cudaEventRecord(P0->mark_a, P0->main));
+  for (int i = 1; i < n_parts; ++i) LRB_CUDA(cudaStreamWaitEvent(parts[i]->main, P0->mark_a, 0));
+  for (int i = 0; i < n_parts; ++i) {
+    int rc = launch_scatter(parts[i], 0, parts[i]->d.n, parts[i]->main);
+    if (rc) return rc;
+    LRB_CUDA(cudaEventRecord(parts[i]->staged_done, parts[i]->main));
+    LRB_CUDA(cudaEventRecord(parts[i]->main_done, parts[i]->main));
+  }
+  for (int i = 1; i < n_parts; ++i) LRB_CUDA(cudaStreamWaitEvent(P0->main, parts[i]->main_done, 0));
+  LRB_CUDA(cudaEventRecord(P0->mark_b, P0->main));
+  LRB_CUDA(cudaEventSynchronize(P0->mark_b));
+  LRB_CUDA(cudaEventElapsedTime(device_ms, P0->mark_a, P0->mark_b));
+  P0->marks = 0;
+  return LRB_OK;
+}
+
 int lrb_part_fill(lrb_part* part, int64_t offset, const double* values, int64_t n) {
   if (!part || offset < 0 || n < 0 || offset + n > part->d.n_buf) {
     set_error("device buffer fill out of bounds");

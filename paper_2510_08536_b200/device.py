@@ -174,6 +174,17 @@ class DevicePart:
         N.check(N.lrb_apply_scatter(self.h))
         self._touch()
 
+    def apply_scatter_timed(self, others=()):
+        """apply_scatter of this part (and ``others`` on the same GPU) with the
+        scatter kernels' device time in ms (synchronous)."""
+        parts = [self, *others]
+        ms = C.c_float()
+        N.check(N.lrb_apply_scatter_timed(len(parts), N.ptr_array([p.h.value for p in parts]),
+                                          C.byref(ms)))
+        for p in parts:
+            p._touch()
+        return float(ms.value)
+
     def fill(self, offset, values):
         values = np.ascontiguousarray(values, dtype=np.float64)
         N.check(N.lrb_part_fill(self.h, int(offset), N.ptr(values), len(values)))

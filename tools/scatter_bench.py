@@ -43,10 +43,7 @@ def child(args):
         part.sync()
         ms = []
         for i in range(args.reps + 3):
-            part.mark()
-            part.apply_scatter()
-            part.mark()
-            t = part.elapsed_ms()
+            t = part.apply_scatter_timed()
             if i >= 3:
                 ms.append(t)
         part.sync()
