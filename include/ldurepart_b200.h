@@ -125,6 +125,13 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces,
  * during the momentum solves). */
 int lrb_upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
                        const int64_t* piece_len);
+/* Several sources' direct updates of one part from ONE host thread: segment
+ * segs[i] gets the next seg_pieces[i] pieces (all pinned; a pageable piece
+ * is rejected with LRB_EVALUE before anything moves); every H2D + scatter is
+ * enqueued on its segment's stream before the single wait.  For hosts that
+ * drive many sources per GPU (C5: 16 sources per part). */
+int lrb_update_segments(lrb_part* part, int32_t n_seg, const int32_t* segs, const int32_t* seg_pieces,
+                        const double* const* pieces, const int64_t* piece_len);
 int lrb_scatter_segment(lrb_part* part, int32_t seg);
 /* Staged update (update.py:85-102): the owner copies all sources' pieces
  * into the pinned stage, then one H2D of the whole buffer and the scatter. */

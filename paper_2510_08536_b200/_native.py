@@ -75,6 +75,7 @@ lrb_part_destroy = _sig("lrb_part_destroy", None, P)
 lrb_part_pointers = _sig("lrb_part_pointers", C.c_int, P, P)
 lrb_update_segment = _sig("lrb_update_segment", C.c_int, P, I32, I32, P, P)
 lrb_upload_segment = _sig("lrb_upload_segment", C.c_int, P, I32, I32, P, P)
+lrb_update_segments = _sig("lrb_update_segments", C.c_int, P, I32, P, P, P, P)
 lrb_scatter_segment = _sig("lrb_scatter_segment", C.c_int, P, I32)
 lrb_update_staged = _sig("lrb_update_staged", C.c_int, P, I32, P, P)
 lrb_stage_segment = _sig("lrb_stage_segment", C.c_int, P, I32, I32, P, P)
@@ -124,7 +125,7 @@ EXPORTED = [
     "lrb_team_profile", "lrb_team_profile_read", "lrb_team_profile_counters",
     "lrb_update_segment_async", "lrb_team_solve_async", "lrb_team_spmv_async",
     "lrb_part_write_values", "lrb_part_capture_base", "lrb_update_perturb",
-    "lrb_upload_segment", "lrb_scatter_segment", "lrb_apply_scatter_timed",
+    "lrb_upload_segment", "lrb_scatter_segment", "lrb_apply_scatter_timed", "lrb_update_segments",
 ]
 
 

@@ -407,6 +407,40 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const doub
   return LRB_OK;
 }
 
+int lrb_update_segments(lrb_part* part, int32_t n_seg, const int32_t* segs, const int32_t* seg_pieces,
+                        const double* const* pieces, const int64_t* piece_len) {
+  if (!part || n_seg < 0 || (n_seg && (!segs || !seg_pieces))) {
+    set_error("lrb_update_segments: bad arguments");
+    return LRB_EVALUE;
+  }
+  int64_t total = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    if (segs[i] < 0 || segs[i] >= int(part->seg_stream.size())) {
+      set_error("lrb_update_segments: bad segment");
+      return LRB_EVALUE;
+    }
+    total += seg_pieces[i];
+  }
+  for (int64_t i = 0; i < total; ++i)
+    if (piece_len[i] && !is_pinned(pieces[i])) {
+      set_error("lrb_update_segments: pageable piece (use one lrb_update_segment per source)");
+      return LRB_EVALUE;
+    }
+  // every segment's H2D + scatter enqueued on its stream, then one wait
+  int64_t at = 0;
+  for (int i = 0; i < n_seg; ++i) {
+    int rc = upload_segment(part, segs[i], seg_pieces[i], pieces + at, piece_len + at,
+                            "lrb_update_segments");
+    if (rc) return rc;
+    rc = scatter_segment(part, segs[i]);
+    if (rc) return rc;
+    at += seg_pieces[i];
+  }
+  DeviceGuard g(part->device);
+  for (int i = 0; i < n_seg; ++i) LRB_CUDA(cudaEventSynchronize(part->seg_h2d[segs[i]]));
+  return LRB_OK;
+}
+
 int lrb_upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
                        const int64_t* piece_len) {
   int rc = upload_segment(part, seg, n_pieces, pieces, piece_len, "lrb_upload_segment");
@@ -1254,9 +1288,19 @@ static void build_stage_headers(const TeamDevice& D, lrb_part* const* by_index, 
 }
 
 static int stream_grid(const void* kernel, int device, int64_t n_tiles, int n_share, size_t smem) {
-  int sms = 0;
+  int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
+    return -1;
+  // The attribute is per kernel FUNCTION, shared by every team: set it to the
+  // most any launch may ask for (opt-in limit minus the kernel's static
+  // shared memory), never to this team's need — a later team with smaller
+  // stages must not shrink it under an earlier team's launches.
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return -1;
+  const int cap_smem = optin - int(fa.sharedSizeBytes);
+  if (int64_t(smem) > cap_smem) return -3;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cap_smem) != cudaSuccess)
     return -1;
   int fit = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, kernel, kStreamThreads, smem) != cudaSuccess ||

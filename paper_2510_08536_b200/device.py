@@ -127,6 +127,7 @@ class DevicePart:
         # initial transfer is epoch 0
         self.seg_h2d_epoch = [0] * plan.n_seg
         self.seg_scat_epoch = [0] * plan.n_seg
+        self.epoch_cv = threading.Condition()
 
     # ---- update path -----------------------------------------------------
     @staticmethod
@@ -140,6 +141,21 @@ class DevicePart:
         arrs, ptrs, lens = self._pieces(pieces)
         N.check(N.lrb_update_segment(self.h, seg, len(arrs), ptrs, N.ptr(lens)))
         self._touch()
+
+    def update_segments(self, segs, pieces_per_seg):
+        """Direct updates of several segments from this thread
+        (lrb_update_segments); False if a piece is pageable (nothing moved)."""
+        arrs = [np.ascontiguousarray(p, dtype=np.float64) for ps in pieces_per_seg for p in ps]
+        ptrs = N.ptr_array([a.ctypes.data for a in arrs])
+        lens = np.array([len(a) for a in arrs], dtype=np.int64)
+        sg = np.asarray(segs, dtype=np.int32)
+        npc = np.array([len(ps) for ps in pieces_per_seg], dtype=np.int32)
+        rc = N.lrb_update_segments(self.h, len(sg), N.ptr(sg), N.ptr(npc), ptrs, N.ptr(lens))
+        if rc == N.LRB_EVALUE and "pageable" in N.last_error():
+            return False
+        N.check(rc)
+        self._touch()
+        return True
 
     def upload_segment(self, seg, pieces):
         """H2D of one source segment only (lrb_upload_segment)."""

@@ -104,3 +104,31 @@ def test_async_length_violation():
     t = torch.zeros(5, dtype=torch.float64, device="cuda:0")
     with pytest.raises(ValueError, match="update pattern violation"):
         s.part.update_segment_async(s.segment, [t], 0)
+
+
+def test_async_solve_split_device_ranks():
+    """Two device ranks on one GPU (the cross-device peer protocol): the
+    stream-ordered solve orders each device's inputs before every device's
+    kernel (join_devices) and equals the synchronous solve bit for bit."""
+    import torch
+
+    from paper_2510_08536_b200.device import Team
+    asm, pm, systems = _setup()
+    owners = [systems[ALPHA * k] for k in range(pm.n_gpu)]
+    parts = [o.part for o in owners]
+    team = Team(parts, dev_ranks=list(range(len(parts))))
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    rng = np.random.default_rng(3)
+    bh = [rng.standard_normal(p.n) for p in parts]
+    b = [torch.from_numpy(v).to("cuda:0") for v in bh]
+    x = [torch.zeros(p.n, dtype=torch.float64, device="cuda:0") for p in parts]
+    rep = torch.zeros(64, dtype=torch.uint8).pin_memory()
+    torch.cuda.synchronize()
+    team.solve_async("pcg", b, x, 1e-8, 500, streams=[s0.cuda_stream, s1.cuda_stream], report=rep)
+    s0.synchronize()
+    s1.synchronize()
+    ra = team.report_from(rep)
+    xs, rs, _ = team.solve("pcg", bh, 1e-8, 500)
+    assert ra.converged == 1 and ra.iterations == rs.iterations and ra.residual == rs.residual
+    for k in range(len(parts)):
+        assert np.array_equal(x[k].cpu().numpy(), xs[k])
