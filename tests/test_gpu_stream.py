@@ -229,3 +229,24 @@ def test_stream_ring_depth_variants(stages, monkeypatch):
 
     lrb.run_world(4, program)
     assert holder["r"]["pcg"].converged
+
+
+def test_teams_of_different_geometry_coexist():
+    """Kernel launch attributes are per function and shared by every team: a
+    team created later with smaller stages must not break an earlier team's
+    launches (interleaved solves, each equal to a fresh team's result)."""
+    from paper_2510_08536_b200.device import Team
+    teams = []
+    for dims, n_cpu, alpha in (((48, 44, 40), 2, 2), ((12, 12, 12), 4, 2), ((30, 30, 30), 3, 1)):
+        _, asm, pm = cavity_case(dims, n_cpu, alpha)
+        parts = _owner_parts(asm, pm)[0]
+        teams.append((parts, Team(parts), Team(parts, dev_ranks=list(range(len(parts))))))
+    ref = [t.solve("pcg", [np.ones(p.n) for p in parts], 1e-9, 500) for parts, t, _ in teams]
+    for k in (0, 2, 1, 0):
+        parts, team, split = teams[k]
+        bs = [np.ones(p.n) for p in parts]
+        for tm in (team, split):
+            xs, rep, _ = tm.solve("pcg", bs, 1e-9, 500)
+            assert rep.iterations == ref[k][1].iterations
+            for a, b in zip(xs, ref[k][0]):
+                assert np.array_equal(a, b)
