@@ -231,9 +231,17 @@ def traffic_ratio(workload):
 # problem
 # ---------------------------------------------------------------------------
 class Problem:
-    """Per-rank LDU inputs whose value arrays live in pinned host memory."""
+    """Per-rank LDU inputs whose value arrays live in pinned host memory.
 
-    def __init__(self, N, n_cpu, ranks, pinned=True):
+    Producer layout (the producer writes straight into pinned
+    buffers in pack order): the value arrays of the ``group`` consecutive
+    ranks that feed one GPU part are views into ONE pinned block, rank after
+    rank, each as [diag | upper | lower | interface blocks by neighbour] —
+    the reference's pack order (update.py:40-45) — so the update moves
+    host-contiguous runs in few large copies.  The LduMatrix / InterfaceBlock
+    objects handed to ``update`` are the reference's types as usual."""
+
+    def __init__(self, N, n_cpu, ranks, pinned=True, group=1):
         import paper_2510_08536_b200 as lrb
         self.lrb = lrb
         grid = lrb.StructuredGrid(N, N, N)
@@ -242,19 +250,41 @@ class Problem:
         self.base = {}
         self.live = {}
         for r in ranks:
-            m, ifs = lrb.assemble_poisson(parts[r])
-            self.base[r] = (m, ifs)
-            if pinned:
-                import torch
-                pin = lambda a: self._pin(torch, a)  # noqa: E731
-                diag = pin(m.diag)
-                mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, diag,
-                                   pin(m.lower_val), pin(m.upper_val))
-                ifp = [lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote, pin(b.values))
-                       for b in ifs]
-                self.live[r] = (mm, ifp, diag)
+            self.base[r] = lrb.assemble_poisson(parts[r])
             parts[r] = None   # drop the mesh (faces live on in the LDU matrix)
+        if pinned:
+            import torch
+            ranks = sorted(self.base)
+            blocks = {}
+            for r in ranks:
+                blocks.setdefault(r // group, []).append(r)
+            for members in blocks.values():
+                sizes = [self._pack_len(*self.base[r]) for r in members]
+                flat = self._pin(torch, np.zeros(sum(sizes)))
+                o = 0
+                for r, n in zip(members, sizes):
+                    self.live[r] = self._views(lrb, *self.base[r], flat[o:o + n])
+                    o += n
         self.n_cells = grid.total_cells
+
+    @staticmethod
+    def _pack_len(m, ifs):
+        return m.n_cells + 2 * m.n_faces + sum(len(b.values) for b in ifs)
+
+    @staticmethod
+    def _views(lrb, m, ifs, buf):
+        """LduMatrix / InterfaceBlocks of the base values over buf, pack order."""
+        n, f = m.n_cells, m.n_faces
+        diag, upper, lower = buf[:n], buf[n:n + f], buf[n + f:n + 2 * f]
+        diag[:], upper[:], lower[:] = m.diag, m.upper_val, m.lower_val
+        mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, diag, lower, upper)
+        o, ifp = n + 2 * f, []
+        for b in sorted(ifs, key=lambda b: b.neighbor_rank):
+            v = buf[o:o + len(b.values)]
+            v[:] = b.values
+            ifp.append(lrb.InterfaceBlock(b.neighbor_rank, b.rows, b.cols_remote, v))
+            o += len(b.values)
+        return mm, ifp, diag
 
     _pinned = []
 
@@ -304,7 +334,7 @@ def run_ours(args):
     alpha = args.rpg
     torch.cuda.set_device(0)
     t0 = time.monotonic()
-    prob = Problem(N, n_cpu, range(n_cpu))
+    prob = Problem(N, n_cpu, range(n_cpu), group=alpha)
     pm = lrb.make_partition_map(prob.cells, alpha)
     log(f"[bench] inputs {time.monotonic() - t0:.1f}s; n_cpu={n_cpu} alpha={alpha}")
     warm, timed = step_plan(args)
@@ -470,7 +500,7 @@ def run_ours_multi(args):
     parts_all = lrb.decompose_slab(lrb.StructuredGrid(N, N, N), n_cpu)
     layout = ProcessLayout([p.n_cells for p in parts_all], alpha, world, rank)
     del parts_all
-    prob = Problem(N, n_cpu, layout.cpu_ranks)
+    prob = Problem(N, n_cpu, layout.cpu_ranks, group=alpha)
     owner = DistributedOwner(layout, {r: prob.base[r] for r in layout.cpu_ranks})
     dist.barrier()
     create_s = max_over_ranks(time.monotonic() - t0)
@@ -843,7 +873,7 @@ def run_c5(args):
     t0 = time.monotonic()
     cells = [p.n_cells for p in lrb.decompose_slab(lrb.StructuredGrid(N, N, N), n_cpu)]
     layout = ProcessLayout(cells, alpha, world, rank)
-    prob = Problem(N, n_cpu, layout.cpu_ranks)
+    prob = Problem(N, n_cpu, layout.cpu_ranks, group=alpha)
     owner = DistributedOwner(layout, {r: prob.base[r] for r in layout.cpu_ranks}, solve=False)
     create_s = time.monotonic() - t0
     for p in owner.parts:   # the pristine base, for the GPU-producer leg

@@ -341,11 +341,17 @@ static int upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const d
   part->stats[all_pinned ? 0 : 1] += n_pieces;
   part->stats[2] += 8 * len;
   if (all_pinned) {
+    // pieces adjacent in host memory (a producer writing in pack order into
+    // one pinned block) travel as one copy
     int64_t o = 0;
-    for (int i = 0; i < n_pieces; ++i) {
-      if (piece_len[i])
-        LRB_CUDA(cudaMemcpyAsync(dst + o, pieces[i], 8 * piece_len[i], cudaMemcpyHostToDevice, st));
-      o += piece_len[i];
+    for (int i = 0; i < n_pieces;) {
+      const double* src = pieces[i];
+      int64_t run = piece_len[i];
+      int j = i + 1;
+      while (j < n_pieces && (piece_len[j] == 0 || pieces[j] == src + run)) run += piece_len[j++];
+      if (run) LRB_CUDA(cudaMemcpyAsync(dst + o, src, 8 * run, cudaMemcpyHostToDevice, st));
+      o += run;
+      i = j;
     }
   } else {
     if (!part->stage || part->stage_len < part->seg_off.back()) {
@@ -426,17 +432,57 @@ int lrb_update_segments(lrb_part* part, int32_t n_seg, const int32_t* segs, cons
       set_error("lrb_update_segments: pageable piece (use one lrb_update_segment per source)");
       return LRB_EVALUE;
     }
-  // every segment's H2D + scatter enqueued on its stream, then one wait
+  // Copies: runs that are contiguous both in host memory and in the receive
+  // buffer (consecutive segments whose sources were produced in pack order
+  // into one pinned block) merge across pieces and segments; each run goes
+  // on the stream of the segment it starts in, and every segment's scatter
+  // follows all the runs that fill it.
+  DeviceGuard g(part->device);
   int64_t at = 0;
+  std::vector<int64_t> seg_at(n_seg + 1, 0);
   for (int i = 0; i < n_seg; ++i) {
-    int rc = upload_segment(part, segs[i], seg_pieces[i], pieces + at, piece_len + at,
-                            "lrb_update_segments");
-    if (rc) return rc;
-    rc = scatter_segment(part, segs[i]);
+    const int64_t off = part->seg_off[segs[i]], len = part->seg_off[segs[i] + 1] - off;
+    int rc = check_pieces(part, len, seg_pieces[i], piece_len + at, "segment", segs[i]);
     if (rc) return rc;
     at += seg_pieces[i];
+    seg_at[i + 1] = at;
   }
-  DeviceGuard g(part->device);
+  struct Piece { double* dst; const double* src; int64_t n; int seg; };
+  std::vector<Piece> ps;
+  for (int i = 0; i < n_seg; ++i) {
+    int64_t o = part->seg_off[segs[i]];
+    for (int64_t k = seg_at[i]; k < seg_at[i + 1]; ++k) {
+      if (piece_len[k]) ps.push_back({part->d.recv + o, pieces[k], piece_len[k], i});
+      o += piece_len[k];
+    }
+    part->stats[0] += seg_pieces[i];
+    part->stats[2] += 8 * (part->seg_off[segs[i] + 1] - part->seg_off[segs[i]]);
+  }
+  for (int i = 0; i < n_seg; ++i) LRB_CUDA(cudaStreamWaitEvent(part->seg_stream[segs[i]], part->staged_done, 0));
+  // waits[i]: the other segments whose streams carry a run that fills part of segment i
+  std::vector<std::vector<int>> waits(n_seg);
+  for (size_t k = 0; k < ps.size();) {
+    size_t e = k + 1;
+    int64_t run = ps[k].n;
+    while (e < ps.size() && ps[e].src == ps[k].src + run && ps[e].dst == ps[k].dst + run) run += ps[e++].n;
+    const int home = ps[k].seg;
+    LRB_CUDA(cudaMemcpyAsync(ps[k].dst, ps[k].src, 8 * run, cudaMemcpyHostToDevice,
+                             part->seg_stream[segs[home]]));
+    for (size_t q = k; q < e; ++q) {
+      auto& w = waits[ps[q].seg];
+      if (ps[q].seg != home && (w.empty() || w.back() != home)) w.push_back(home);
+    }
+    k = e;
+  }
+  // each stream's copies are all issued: mark them, then the scatters wait
+  for (int i = 0; i < n_seg; ++i)
+    LRB_CUDA(cudaEventRecord(part->seg_h2d[segs[i]], part->seg_stream[segs[i]]));
+  for (int i = 0; i < n_seg; ++i)
+    for (int h : waits[i]) LRB_CUDA(cudaStreamWaitEvent(part->seg_stream[segs[i]], part->seg_h2d[segs[h]], 0));
+  for (int i = 0; i < n_seg; ++i) {
+    int rc = scatter_segment(part, segs[i]);
+    if (rc) return rc;
+  }
   for (int i = 0; i < n_seg; ++i) LRB_CUDA(cudaEventSynchronize(part->seg_h2d[segs[i]]));
   return LRB_OK;
 }

@@ -435,3 +435,45 @@ def test_two_systems_interleaved_updates_and_solves():
         return ok
 
     assert all(lrb.run_world(8, program))
+
+
+def test_update_segments_contiguous_runs():
+    """lrb_update_segments: a part's sources produced in pack order into one
+    pinned block move as merged host-contiguous runs (across pieces and
+    segments); values equal the per-source update bit for bit, also with a
+    gap that splits the runs."""
+    import torch
+
+    from paper_2510_08536_b200.repart import _pieces
+    _, asm, pm = cavity_case((16, 16, 16), 8, 4)
+    systems = lrb.run_world(8, lambda ctx: lrb.repartition(*asm[ctx.rank], pm, ctx))
+    step = 6
+    new = [lrb.perturb_coefficients(*asm[r], step) for r in range(8)]
+    for gap in (0, 3):
+        for k in range(pm.n_gpu):
+            ranks = range(pm.alpha * k, pm.alpha * (k + 1))
+            pcs = [_pieces(*new[r]) for r in ranks]
+            total = sum(len(p) for ps in pcs for p in ps) + gap * len(ranks)
+            block = torch.zeros(total, dtype=torch.float64).pin_memory().numpy()
+            views, o = [], 0
+            for ps in pcs:
+                vs = []
+                for p in ps:
+                    v = block[o:o + len(p)]
+                    v[:] = p
+                    vs.append(v)
+                    o += len(p)
+                o += gap
+                views.append(vs)
+            part = systems[pm.alpha * k].part
+            assert part.update_segments([r % pm.alpha for r in ranks], views)
+            part.join()
+        dev = [(systems[pm.alpha * k].matrix.local.vals.copy(),
+                systems[pm.alpha * k].matrix.non_local.vals.copy()) for k in range(pm.n_gpu)]
+        probs = [ocav.perturb(p, step) for p in ocav.cavity_problems((16, 16, 16), 8)]
+        pipe = OraclePipeline(probs, pm.offsets, pm.alpha)
+        for k in range(pm.n_gpu):
+            assert np.array_equal(dev[k][0], pipe.values[k][0])
+            assert np.array_equal(dev[k][1], pipe.values[k][1])
+        # pageable pieces are refused before anything moves
+        assert not systems[0].part.update_segments([0], [_pieces(*asm[0])])
