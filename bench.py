@@ -691,17 +691,21 @@ def run_c4(args):
     alpha = args.rpg
     torch.cuda.set_device(0)
     t0 = time.monotonic()
-    prob = Problem(N, n_cpu, range(n_cpu))
+    prob = Problem(N, n_cpu, range(n_cpu), group=alpha)
     pm = lrb.make_partition_map(prob.cells, alpha)
     mom = {}
-    for r in range(n_cpu):   # momentum LDU on the same addressing, pinned value arrays
+    # momentum LDU on the same addressing; its value arrays (interface blocks
+    # included) are pinned views in pack order, one block per GPU part
+    flat = Problem._pin(torch, np.zeros(sum(Problem._pack_len(*prob.base[r]) for r in range(n_cpu))))
+    o = 0
+    for r in range(n_cpu):
         m, ifs = prob.base[r]
+        n = Problem._pack_len(m, ifs)
+        mm, ifp, dg = Problem._views(lrb, m, ifs, flat[o:o + n])
+        o += n
+        dg[:] = 6.5
         eu, el = momentum_eps(m, r)
-        up = Problem._pin(torch, np.zeros(m.n_faces))
-        lo = Problem._pin(torch, np.zeros(m.n_faces))
-        dg = Problem._pin(torch, np.full(m.n_cells, 6.5))
-        mm = lrb.LduMatrix(m.n_cells, m.lower_addr, m.upper_addr, dg, lo, up)
-        mom[r] = (mm, ifs, eu, el, up, lo)
+        mom[r] = (mm, ifp, eu, el, mm.upper_val, mm.lower_val)
     log(f"[bench c4] inputs {time.monotonic() - t0:.1f}s; N={N} n_cpu={n_cpu} alpha={alpha}")
     warm, timed = step_plan(args)
     seq = warm + timed
