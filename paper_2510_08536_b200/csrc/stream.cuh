@@ -431,6 +431,34 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
   }
 }
 
+// Cross-phase L2 prefetch (issuers, before the elementwise phase's barrier):
+// the next phase is an SpMV phase over the same tiles (CG: A or the check C;
+// BiCGStab: phase 1 or the check), and a tile's record and values do not
+// depend on the barrier's results, so the CTA's first LRB_XPF tiles of it are
+// pulled toward L2 while the barrier completes; the phase's first bulk copies
+// then hit L2 instead of paying the DRAM latency at the phase start.
+#ifndef LRB_XPF
+#define LRB_XPF 3
+#endif
+template <bool INL>
+__device__ __forceinline__ void prefetch_next_spmv(const TeamDev& T) {
+  if (LRB_XPF <= 0 || !T.tile_hdr) return;
+  const int pw = (int(threadIdx.x) - kConsumers) >> 5;
+  if ((threadIdx.x & 31) != 0) return;
+  const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
+  const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
+  const int64_t G = gridDim.x;
+  for (int k = pw; k < LRB_XPF; k += kIssuers) {
+    const int64_t tile = blockIdx.x + int64_t(k) * G;
+    if (tile >= T.n_tiles) break;
+    PfAddr a;
+    load_pf_addr(hdrs + tile, a);
+    if (!a.tma) continue;
+    bulk_prefetch_l2(recs + tile, kRecBytes);
+    bulk_prefetch_l2(part_of(T, a.part, INL).val + a.e0, unsigned(a.vbytes));
+  }
+}
+
 // Elementwise phases: stage k holds chunk q = cta + k * grid = tiles
 // [q * K, q * K + K) ∩ [0, n_tiles): the headers, then each vector's tiles
 // (one copy per vector when the tiles belong to one part).
@@ -875,7 +903,7 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
 // Phase wrapper: issuers stream, consumer teams compute, then the team
 // barrier with the fused reduction (all threads); gseq advances by the
 // phase's stage count (identical in every thread).
-template <int NR, bool INL, bool ELEM, class SpecF, class Body>
+template <int NR, bool INL, bool ELEM, bool PF_NEXT = false, class SpecF, class Body>
 __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, int& gseq, double* red,
                                              int kind, SpecF&& spec_of, Body&& body) {
   const int ntv = ELEM ? spec_of(part_of(T, T.part_begin, INL)).ntv : 0;
@@ -887,6 +915,7 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
       produce_elementwise<INL>(T, S, gseq, kind, spec_of);
     else
       produce_spmv<INL>(T, S, gseq, kind, spec_of);
+    if constexpr (PF_NEXT) prefetch_next_spmv<INL>(T);
   } else {
     consume_phase<NR, INL, ELEM>(T, S, gseq, kind, ntv, body);
   }
@@ -921,7 +950,7 @@ __global__ void LRB_STREAM_BOUNDS
   int gseq = 0;
   double red[2];
   // ---- phase 0: x = 0, r = b, (z = dinv*b), b.b (, b.z)
-  stream_phase<2, INL, true>(
+  stream_phase<2, INL, true, true>(
       T, S, gseq, red, 0,
       [&](const PartDev& P) {
         return Spec{0, JAC ? 2 : 1, {nullptr, nullptr}, {P.b, JAC ? P.dinv : nullptr}};
@@ -1040,7 +1069,7 @@ __global__ void LRB_STREAM_BOUNDS
     pa ^= 1;
 #if LRB_LAZY_X
     // ---- phase B: r -= step q, r.r (, z = dinv r, r.z); x += step p pending
-    stream_phase<2, INL, true>(
+    stream_phase<2, INL, true, true>(
         T, S, gseq, red, 2,
         [&](const PartDev& P) {
           return Spec{0, kCgBVecs<JAC>, {nullptr, nullptr}, {P.r, P.q, JAC ? P.dinv : nullptr}};
@@ -1063,7 +1092,7 @@ __global__ void LRB_STREAM_BOUNDS
     step_x = step;
 #else
     // ---- phase B: x += step p, r -= step q, r.r (, r.z)
-    stream_phase<2, INL, true>(
+    stream_phase<2, INL, true, true>(
         T, S, gseq, red, 2,
         [&](const PartDev& P) {
           return Spec{0, kCgBVecs<JAC>, {nullptr, nullptr},
@@ -1168,7 +1197,7 @@ __global__ void LRB_STREAM_BOUNDS
   stream_init(T, S);
   int gseq = 0;
   double red[2];
-  stream_phase<1, INL, true>(
+  stream_phase<1, INL, true, true>(
       T, S, gseq, red, 0, [&](const PartDev& P) { return Spec{0, 1, {nullptr, nullptr}, {P.b}}; },
       [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[1]) {
         if (lr >= H.rows) return;
@@ -1291,7 +1320,7 @@ __global__ void LRB_STREAM_BOUNDS
     omega = red[1] != 0.0 ? red[0] / red[1] : 0.0;
     // ---- phase 3: x = (x + alpha p) + omega s, r = s - omega t, r.r, rhat.r;
     //      u = p - omega v over p (the next phase 1's operand)
-    stream_phase<2, INL, true>(
+    stream_phase<2, INL, true, true>(
         T, S, gseq, red, 2,
         [&](const PartDev& P) {
           return Spec{0, 6, {nullptr, nullptr},
