@@ -477,3 +477,41 @@ def test_update_segments_contiguous_runs():
             assert np.array_equal(dev[k][1], pipe.values[k][1])
         # pageable pieces are refused before anything moves
         assert not systems[0].part.update_segments([0], [_pieces(*asm[0])])
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_interleaving_of_update_paths(seed):
+    """A seeded random sequence of direct / staged / device-producer updates
+    and solves on two systems sharing the ranks: after every operation the
+    owners' values equal a fresh repartition of the same coefficients, and
+    every solve equals the solve of that fresh system."""
+    _, asm, pm = cavity_case((14, 14, 14), 8, 4)
+    rng = np.random.default_rng(seed)
+    ops = [(int(rng.integers(2)), ["direct", "staged", "device"][int(rng.integers(3))],
+            int(rng.integers(2, 40)), bool(rng.integers(2))) for _ in range(10)]
+
+    def program(ctx):
+        base = asm[ctx.rank]
+        sys_ = [lrb.repartition(*base, pm, ctx), lrb.repartition(*base, pm, ctx)]
+        for s in sys_:
+            lrb.capture_device_base(s)
+        ok = True
+        for which, how, step, solve in ops:
+            s = sys_[which]
+            if how == "device":
+                lrb.update_on_device(s, step)
+            else:
+                lrb.update(s, *lrb.perturb_coefficients(*base, step), how)
+            fresh = lrb.repartition(*lrb.perturb_coefficients(*base, step), pm, ctx)
+            if s.is_owner:
+                ok &= np.array_equal(s.matrix.local.vals, fresh.matrix.local.vals)
+                ok &= np.array_equal(s.matrix.non_local.vals, fresh.matrix.non_local.vals)
+                if solve:
+                    b = np.ones(s.matrix.n_owned)
+                    xa, ra = lrb.cg_solve(s.matrix, s.halo, b, 1e-8, 500, s.comm, method="pcg")
+                    xb, rb = lrb.cg_solve(fresh.matrix, fresh.halo, b, 1e-8, 500, fresh.comm,
+                                          method="pcg")
+                    ok &= np.array_equal(xa, xb) and ra.iterations == rb.iterations
+        return ok
+
+    assert all(lrb.run_world(8, program))
