@@ -97,3 +97,33 @@ def test_pcg1_matches_reference_cg(name):
         ref = ref_history(get(name, 0, f"cg_{s}_log"), it_ref, TOL)
         assert abs(rep.iterations - it_ref) <= 1
         assert history_ok(rep.history, ref)[0], (rep.history, ref)
+
+
+@pytest.mark.parametrize("dims,n_cpu,alpha", [((12, 12, 12), 4, 2), ((20, 18, 16), 6, 3)])
+def test_bicgstab_solution_against_direct_solve(dims, n_cpu, alpha):
+    """An independent check of BiCGStab (the reference has none): the GPU
+    solution of the non-symmetric momentum system at tol 1e-12 equals SciPy's
+    direct sparse solve of the gathered global matrix to 1e-9."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    mom = momentum_ldu(asm, seed=4)
+
+    def program(ctx):
+        s = lrb.repartition(*mom[ctx.rank], pm, ctx)
+        if not s.is_owner:
+            return None
+        rng = np.random.default_rng(100 + s.gpu_rank)
+        b = rng.standard_normal(s.matrix.n_owned)
+        x, rep = lrb.bicgstab_solve(s.matrix, s.halo, b, 1e-12, 2000, s.comm)
+        g = lrb.gather_global(s.matrix, pm, s.comm)
+        xs = s.comm.gather(x, 0)
+        bs = s.comm.gather(b, 0)
+        return (g, np.concatenate(xs), np.concatenate(bs), rep) if g is not None else None
+
+    g, x, b, rep = lrb.run_world(n_cpu, program)[0]
+    assert rep.converged
+    A = sp.coo_matrix((g.vals, (g.rows, g.cols)), shape=(g.n_rows, g.n_cols)).tocsc()
+    xd = spla.spsolve(A, b)
+    assert np.linalg.norm(x - xd) <= 1e-9 * np.linalg.norm(xd)
+    assert np.linalg.norm(A @ x - b) <= 1e-11 * np.linalg.norm(b)
