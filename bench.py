@@ -467,8 +467,10 @@ def run_ours(args):
             "update_wall_ms": round(float(np.mean(rec["pg_update_ms"])), 4),
             "timer": "host wall clock around update + cg_solve of rank 0 (synchronous API)",
             "inputs": "perturb_coefficients output (pageable numpy, as the reference's own "
-                      "generator returns it); each rank thread copies into the part's pinned "
-                      "stage, counted inside the update"}
+                      "generator returns it: a fresh diagonal, the same off-diagonal arrays "
+                      "every step); the fresh pieces are host-copied into the part's pinned "
+                      "stage inside the update, reused >= 4 MB arrays are page-locked in place "
+                      "from their second update on (first update, untimed warm-up)"}
     return line
 
 

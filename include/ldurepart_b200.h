@@ -123,6 +123,13 @@ int lrb_update_segment(lrb_part* part, int32_t seg, int32_t n_pieces,
  * update() orders the two by update epochs, so a source's upload of the next
  * system overlaps the owner's solves of another (C4: pressure coefficients
  * during the momentum solves). */
+/* Page-lock an existing host range in place (cudaHostRegister) / release it:
+ * the drop-in registers a producer's coefficient arrays that come back in a
+ * second update (the reference's perturb_coefficients returns the same
+ * off-diagonal arrays every timestep), so their bytes go straight to the
+ * device instead of through the stage; unregistered when the array dies. */
+int lrb_host_register(void* ptr, int64_t bytes);
+int lrb_host_unregister(void* ptr);
 int lrb_upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const double* const* pieces,
                        const int64_t* piece_len);
 /* Several sources' direct updates of one part from ONE host thread: segment

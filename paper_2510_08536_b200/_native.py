@@ -76,6 +76,8 @@ lrb_part_pointers = _sig("lrb_part_pointers", C.c_int, P, P)
 lrb_update_segment = _sig("lrb_update_segment", C.c_int, P, I32, I32, P, P)
 lrb_upload_segment = _sig("lrb_upload_segment", C.c_int, P, I32, I32, P, P)
 lrb_update_segments = _sig("lrb_update_segments", C.c_int, P, I32, P, P, P, P)
+lrb_host_register = _sig("lrb_host_register", C.c_int, P, I64)
+lrb_host_unregister = _sig("lrb_host_unregister", C.c_int, P)
 lrb_scatter_segment = _sig("lrb_scatter_segment", C.c_int, P, I32)
 lrb_update_staged = _sig("lrb_update_staged", C.c_int, P, I32, P, P)
 lrb_stage_segment = _sig("lrb_stage_segment", C.c_int, P, I32, I32, P, P)
@@ -126,6 +128,7 @@ EXPORTED = [
     "lrb_update_segment_async", "lrb_team_solve_async", "lrb_team_spmv_async",
     "lrb_part_write_values", "lrb_part_capture_base", "lrb_update_perturb",
     "lrb_upload_segment", "lrb_scatter_segment", "lrb_apply_scatter_timed", "lrb_update_segments",
+    "lrb_host_register", "lrb_host_unregister",
 ]
 
 

@@ -334,52 +334,53 @@ static int upload_segment(lrb_part* part, int32_t seg, int32_t n_pieces, const d
   // a whole-buffer scatter on the solve stream (staged update) may still read
   // the receive buffer
   LRB_CUDA(cudaStreamWaitEvent(st, part->staged_done, 0));
-  bool all_pinned = true;
-  for (int i = 0; i < n_pieces && all_pinned; ++i)
-    if (piece_len[i]) all_pinned = is_pinned(pieces[i]);
+  // Per piece: pinned (or registered) host memory goes straight to the
+  // device, runs of pieces adjacent in host memory as one copy (a producer
+  // writing in pack order into one pinned block); pageable
+  // pieces go through the part's pinned stage, host-copying chunk c while the
+  // copy engine moves chunk c-1.
+  std::vector<char> pinned(size_t(std::max(n_pieces, 0)), 0);
+  int n_pinned = 0;
+  for (int i = 0; i < n_pieces; ++i) {
+    pinned[i] = piece_len[i] == 0 || is_pinned(pieces[i]);
+    n_pinned += pinned[i] && piece_len[i] ? 1 : 0;
+  }
   double* dst = part->d.recv + off;
-  part->stats[all_pinned ? 0 : 1] += n_pieces;
+  part->stats[0] += n_pinned;
+  part->stats[1] += n_pieces - n_pinned;
   part->stats[2] += 8 * len;
-  if (all_pinned) {
-    // pieces adjacent in host memory (a producer writing in pack order into
-    // one pinned block) travel as one copy
-    int64_t o = 0;
-    for (int i = 0; i < n_pieces;) {
+  bool staged = false;
+  constexpr int64_t kChunkDoubles = int64_t(1) << 19;   // 4 MB
+  int64_t o = 0;
+  for (int i = 0; i < n_pieces;) {
+    if (pinned[i]) {
       const double* src = pieces[i];
       int64_t run = piece_len[i];
       int j = i + 1;
-      while (j < n_pieces && (piece_len[j] == 0 || pieces[j] == src + run)) run += piece_len[j++];
+      while (j < n_pieces && pinned[j] && (piece_len[j] == 0 || pieces[j] == src + run)) run += piece_len[j++];
       if (run) LRB_CUDA(cudaMemcpyAsync(dst + o, src, 8 * run, cudaMemcpyHostToDevice, st));
       o += run;
       i = j;
+      continue;
     }
-  } else {
-    if (!part->stage || part->stage_len < part->seg_off.back()) {
-      set_error(std::string(who) + ": pageable input needs a pinned stage");
-      return LRB_EVALUE;
-    }
-    // previous copy out of this stage slice must have landed
-    LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
-    LRB_CUDA(cudaEventSynchronize(part->stage_free));
-    // pipelined: host-copy chunk c into the pinned stage while the copy engine
-    // moves chunk c-1 (the host memcpy and the DMA overlap instead of adding)
-    constexpr int64_t kChunkDoubles = int64_t(1) << 19;   // 4 MB
-    int64_t o = 0, sent = 0;
-    for (int i = 0; i < n_pieces; ++i) {
-      for (int64_t a = 0; a < piece_len[i];) {
-        const int64_t take = std::min(piece_len[i] - a, kChunkDoubles - (o - sent));
-        std::memcpy(part->stage + off + o, pieces[i] + a, 8 * take);
-        a += take;
-        o += take;
-        if (o - sent == kChunkDoubles) {
-          LRB_CUDA(cudaMemcpyAsync(dst + sent, part->stage + off + sent, 8 * (o - sent),
-                                   cudaMemcpyHostToDevice, st));
-          sent = o;
-        }
+    if (!staged) {
+      if (!part->stage || part->stage_len < part->seg_off.back()) {
+        set_error(std::string(who) + ": pageable input needs a pinned stage");
+        return LRB_EVALUE;
       }
+      // the previous copy out of this stage slice must have landed
+      LRB_CUDA(cudaEventSynchronize(part->seg_h2d[seg]));
+      LRB_CUDA(cudaEventSynchronize(part->stage_free));
+      staged = true;
     }
-    if (o > sent)
-      LRB_CUDA(cudaMemcpyAsync(dst + sent, part->stage + off + sent, 8 * (o - sent), cudaMemcpyHostToDevice, st));
+    for (int64_t a = 0; a < piece_len[i];) {
+      const int64_t take = std::min(piece_len[i] - a, kChunkDoubles);
+      std::memcpy(part->stage + off + o, pieces[i] + a, 8 * take);
+      LRB_CUDA(cudaMemcpyAsync(dst + o, part->stage + off + o, 8 * take, cudaMemcpyHostToDevice, st));
+      a += take;
+      o += take;
+    }
+    ++i;
   }
   LRB_CUDA(cudaEventRecord(part->seg_h2d[seg], st));
   return LRB_OK;
@@ -484,6 +485,21 @@ int lrb_update_segments(lrb_part* part, int32_t n_seg, const int32_t* segs, cons
     if (rc) return rc;
   }
   for (int i = 0; i < n_seg; ++i) LRB_CUDA(cudaEventSynchronize(part->seg_h2d[segs[i]]));
+  return LRB_OK;
+}
+
+int lrb_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) {
+    set_error("lrb_host_register: bad range");
+    return LRB_EVALUE;
+  }
+  LRB_CUDA(cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterDefault));
+  return LRB_OK;
+}
+
+int lrb_host_unregister(void* ptr) {
+  if (!ptr) return LRB_OK;
+  LRB_CUDA(cudaHostUnregister(ptr));
   return LRB_OK;
 }
 

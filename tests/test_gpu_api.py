@@ -515,3 +515,37 @@ def test_random_interleaving_of_update_paths(seed):
         return ok
 
     assert all(lrb.run_world(8, program))
+
+
+def test_pageable_arrays_pinned_in_place_on_reuse():
+    """The reference generator's arrays (fresh diagonal, the same off-diagonal
+    arrays every step): from the second update on, the reused >= 4 MB arrays
+    are page-locked in place and go straight to the device (pinned pieces
+    counted), the fresh diagonal keeps going through the stage; values stay
+    bit-exact and the registration dies with the arrays."""
+    import gc
+
+    from paper_2510_08536_b200.device import _host_pins
+    _, asm, pm = cavity_case((96, 96, 96), 2, 2)
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        before = s.part.stats() if s.is_owner else None
+        for step in (2, 3, 4):
+            lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], step), "direct")
+        if s.is_owner:
+            after = s.part.stats()
+            return after["pinned_pieces"] - before["pinned_pieces"], s.matrix.local.vals.copy()
+        return None
+
+    res = lrb.run_world(2, program)
+    pinned_pieces, lv = res[0]
+    assert pinned_pieces >= 2      # upper / lower of both sources at steps 3 and 4
+    probs = [ocav.perturb(p, 4) for p in ocav.cavity_problems((96, 96, 96), 2)]
+    pipe = OraclePipeline(probs, pm.offsets, 2)
+    assert np.array_equal(lv, pipe.values[0][0])
+    registered = [k for k, v in _host_pins._seen.items() if v == 2]
+    assert registered
+    asm.clear()
+    gc.collect()
+    assert not [k for k in registered if k in _host_pins._seen]
