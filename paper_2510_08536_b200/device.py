@@ -117,8 +117,11 @@ class _HostPins:
     MIN_BYTES = 4 << 20
 
     def __init__(self):
+        import os
         self._lock = threading.Lock()
         self._seen = {}      # id(owner) -> sightings (owner alive: finalize removes it)
+        # LRB_PIN_REUSED=0: never page-lock caller arrays (always stage them)
+        self.enabled = os.environ.get("LRB_PIN_REUSED", "1") != "0"
 
     @staticmethod
     def _owner(a):
@@ -128,6 +131,8 @@ class _HostPins:
         return o if o.base is None and o.flags.owndata else None
 
     def note(self, arrays):
+        if not self.enabled:
+            return
         for a in arrays:
             if a.nbytes < self.MIN_BYTES:
                 continue
