@@ -100,6 +100,7 @@ struct lrb_part {
   std::vector<int32_t> slice_pat_host, pat_off_host;
   std::vector<uint16_t> rmask_host;
   std::vector<int32_t> loc_sell, nl_sell;  // SELL slot of each CSR entry (value mirror)
+  std::vector<char> tile_halo;             // per tile: some row has halo (non-local) columns
   int64_t nnz_l = 0, nnz_n = 0;
   cudaStream_t main = nullptr;
   std::vector<cudaStream_t> seg_stream;
@@ -234,6 +235,9 @@ int lrb_part_create(const lrb_plan* plan, int32_t device, void* dev_arena, int64
   part->slice_pat_host = P.slice_pat;
   part->pat_off_host = P.pat_off;
   part->rmask_host = P.rmask;
+  part->tile_halo.assign(size_t((P.n + kTile - 1) / kTile), 0);
+  for (int64_t r = 0; r < P.n; ++r)
+    if (P.nl_ptr[r + 1] > P.nl_ptr[r]) part->tile_halo[r / kTile] = 1;
   part->nnz_l = int64_t(P.loc_col.size());
   part->nnz_n = int64_t(P.nl_col.size());
   part->stage = host_stage;
@@ -1244,6 +1248,7 @@ static int64_t tile_geometry(const lrb_part* P, int64_t lt, int part_index, int6
   h.tile = int32_t(dev_tile);
   h.e0 = P->slice_ptr[s0];
   h.vbytes = int32_t(8 * (P->slice_ptr[s1] - P->slice_ptr[s0]));
+  h.halo = (lt < int64_t(P->tile_halo.size()) && P->tile_halo[lt]) ? 1 : 0;
   for (int64_t s = s0; s <= s1; ++s) h.sp[s - s0] = int32_t(P->slice_ptr[s] - P->slice_ptr[s0]);
   const bool have_win = int64_t(P->tile_win.size()) >= (lt + 1) * kWinStride;
   const int32_t* tw = have_win ? &P->tile_win[lt * kWinStride] : nullptr;

@@ -120,6 +120,7 @@ struct StageHdrFields {
   int32_t woff[kMaxWin]; // window offsets inside a vector's staged run
   int32_t vbytes;        // staged value bytes
   int32_t npat;          // distinct patterns of the tile (slot tables in StageTab)
+  int32_t halo;          // 1: some row of the tile has non-local (halo) columns
   int32_t sp[kTile / kSlice + 1];   // slice entry offsets relative to e0
   int32_t pat[kTile / kSlice];      // slice pattern ids (dictionary)
   int8_t spat[kTile / kSlice];      // slice -> slot table of the tile's StageTab

@@ -746,8 +746,11 @@ __device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __
                                              const XS& xs, FH&& fh, double& xd) {
   const int n = int(P.n);
   const PartDev* mp = (MIRROR && P.mir) ? &P : nullptr;
-  return P.n_halo ? row_spmv_staged<true>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd)
-                  : row_spmv_staged<false>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd);
+  // only tiles holding rows with halo columns take the per-entry halo test;
+  // every other tile of a multi-part / multi-GPU part keeps the fixed-width path
+  return (P.n_halo && H.halo)
+             ? row_spmv_staged<true>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd)
+             : row_spmv_staged<false>(n, P.hpart, P.hidx, mp, parts, H, slot, t.sval, t.smask, lr, xs, fh, xd);
 }
 template <bool MIRROR = false, class XS, class FH>
 __device__ __forceinline__ double staged_row(const PartDev& P, const PartDev* __restrict__ parts,
