@@ -437,8 +437,10 @@ def run_ours(args):
             ctx.barrier()
             if r == 0:
                 part, team = system.part, system.team
-                part.sync()
-                t_sc = part.apply_scatter_timed()
+                others = [q for q in team.parts if q is not part]   # parts on the same GPU
+                for q in team.parts:
+                    q.sync()
+                t_sc = part.apply_scatter_timed(others)
                 _, rep, hist = team.solve(method, None, TOL, MAX_ITER, want_x=False,
                                           hist_cap=MAX_ITER)
                 part.sync()
@@ -450,8 +452,10 @@ def run_ours(args):
                     rec.setdefault("value_iters", []).append(rep.iterations)
             ctx.barrier()
         if r == 0:
-            p = system.part.plan
-            rec["plan"] = (p.n, p.nnz_local + p.nnz_nonlocal, p.n_halo, p.n_buf)
+            # every part of the team is on this GPU: the work of all of them
+            ps = [q.plan for q in system.team.parts]
+            rec["plan"] = (sum(p.n for p in ps), sum(p.nnz_local + p.nnz_nonlocal for p in ps),
+                           sum(p.n_halo for p in ps), sum(p.n_buf for p in ps))
             rec["kernel_info"] = system.team.kernel_info(method)
         return None
 
