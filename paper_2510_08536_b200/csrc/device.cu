@@ -976,7 +976,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_parts = take(sizeof(PartDev) * n_parts);
   const size_t o_tp = take(sizeof(int32_t) * n_tiles);
   const size_t o_partials = take(sizeof(double) * kMaxRed * n_tiles);
-  const size_t o_lanes = take(sizeof(double) * kMaxRed * kLanes * D.parts.size());
+  const size_t o_lanes = take(sizeof(double) * kMaxRed * kLanes * 2);   // lane_fast: one part
   const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts * 2);  // epoch parity
   const size_t o_red = take(sizeof(double) * kMaxRed);
   const size_t o_bar = take(sizeof(unsigned) * 2);

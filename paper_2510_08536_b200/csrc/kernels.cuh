@@ -256,6 +256,16 @@ __device__ __forceinline__ bool lanes_by_cta(const TeamDev& T, int64_t ntiles, i
   return T.lane_fast && (int(gridDim.x) == kLanes || units <= int64_t(gridDim.x));
 }
 
+// Flat barriers passed by this CTA in the current launch (streaming kernels
+// zero it in stream_init).  Its parity selects the lane-value buffer: a CTA
+// can write barrier b+1's lane value only after every CTA arrived at b+1, i.e.
+// after every CTA finished reading barrier b's lane values.  Teams that never
+// take the flat barrier keep parity 0 for writer and reader.
+static __shared__ unsigned s_flat_bar;
+__device__ __forceinline__ double* lane_slots(const TeamDev& T, unsigned bar) {
+  return T.lane_vals + size_t(bar & 1u) * kLanes * kMaxRed;
+}
+
 // Lane v's value from the tile partials (the slow path): its tiles in
 // ascending order, loads batched so the chain costs ceil(tiles / 16) trips.
 template <int NR>
@@ -302,7 +312,7 @@ __device__ __forceinline__ void part_value(const TeamDev& T, int p, int K, doubl
   if (v < kLanes) {
     if (lanes_by_cta(T, P.ntiles, K)) {
       // lanes >= grid have no units (lanes_by_cta) and were not written
-      const double* lv = T.lane_vals + (size_t(p - T.part_begin) * kLanes + v) * kMaxRed;
+      const double* lv = lane_slots(T, s_flat_bar) + (size_t(p - T.part_begin) * kLanes + v) * kMaxRed;
       if (v < int(gridDim.x))
 #pragma unroll
         for (int j = 0; j < NR; ++j) acc[j] = __ldcg(lv + j);
@@ -420,6 +430,90 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu64(unsigned long long* p) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_gpu64(unsigned long long* p) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef LRB_FLAT_BAR   // 0: single-part lane_fast teams take the last-CTA barrier too
+#define LRB_FLAT_BAR 1
+#endif
+#ifndef LRB_FLAT_POLL_NS
+#define LRB_FLAT_POLL_NS 32
+#endif
+// Flat barrier (one device, one part, CTA c = reduction lane c): every CTA
+// publishes its lane value, arrives with a release add on a launch-monotonic
+// counter and waits for the count of this barrier; then EVERY CTA sums the
+// lane values itself in the canonical order (part_value's tree), so nobody
+// waits for a last CTA to reduce, publish and release.  Bit-identical to the
+// last-CTA barrier.  Critical path: the last arrival's add, one poll, one
+// batch of lane loads.
+template <int NR>
+__device__ __forceinline__ void flat_sync(const TeamDev& T, double* red, double (*gs)[kMaxRed], double* pv,
+                                          unsigned& s_last) {
+  const unsigned b = s_flat_bar;   // every thread, before thread 0 advances it
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = &T.out->flat_count;
+    const unsigned long long target = (unsigned long long)(b + 1) * gridDim.x;
+    if (T.prof) {   // diagnostics: the last arrival stamps the phase end
+      s_last = atom_add_acq_rel_gpu64(cnt) + 1 == target;
+      if (s_last && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
+    } else {
+      red_add_release_gpu64(cnt);
+    }
+    const long long t0 = global_ns();
+    while (ld_acquire_gpu64(cnt) < target) {
+      if (LRB_FLAT_POLL_NS) __nanosleep(LRB_FLAT_POLL_NS);
+      if (global_ns() - t0 > T.timeout_ns) {
+        team_fail(T, LRB_ETIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  double acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+  const int v = threadIdx.x;
+  if (v < int(gridDim.x)) {   // lanes >= grid have no units (lanes_by_cta)
+    const double* lv = lane_slots(T, b) + size_t(v) * kMaxRed;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) acc[j] = __ldcg(lv + j);
+  }
+  const int warp = threadIdx.x >> 5;
+  if (warp < kLaneGroups) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] = __dadd_rn(acc[j], __shfl_xor_sync(0xffffffffu, acc[j], o));
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) gs[warp][j] = acc[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double s = gs[0][j];
+      for (int g = 1; g < kLaneGroups; ++g) s = __dadd_rn(s, gs[g][j]);
+      pv[j] = s;
+    }
+    s_flat_bar = b + 1;
+    if (T.prof && s_last && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NR; ++j) red[j] = pv[j];
+}
 
 // All blocks of this device arrive; the last one reduces the tile partials of
 // every local part in fixed order, exchanges part values with the peer devices
@@ -436,6 +530,10 @@ __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch 
   __shared__ double pv[kMaxRed];
   __shared__ double pvals[kSmemParts][kMaxRed];
   __syncthreads();
+  if (LRB_FLAT_BAR && T.n_dev == 1 && T.n_parts == 1 && lanes_by_cta(T, T.n_tiles, K)) {
+    flat_sync<NR>(T, red, gs, pv, s_last);
+    return;
+  }
   if (threadIdx.x == 0) {
     s_gen = ld_acquire_gpu(T.bar_gen);
     if (T.n_dev > 1) __threadfence_system();

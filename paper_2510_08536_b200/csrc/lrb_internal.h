@@ -164,6 +164,9 @@ struct SolveOut {
   int32_t breakdown;
   double residual;
   double bnorm;
+  // arrivals at the flat team barrier (kernels.cuh: team_sync); zeroed with
+  // the rest of the record before every launch
+  unsigned long long flat_count;
 };
 
 // Descriptors of up to kInlineParts local parts ride in the kernel parameter
@@ -205,7 +208,7 @@ struct TeamDev {
   int32_t lane_fast;        // CTA c computes reduction lane c itself (kernels.cuh: canonical tree)
   int32_t stage_bytes;      // streaming solvers: bytes of one shared-memory stage (classic: the
   int32_t n_stages;         //   streaming geometry, for the tree's units) and ring depth (stream.cuh)
-  double* lane_vals;        // [local parts][kLanes][kMaxRed] lane values (lane_fast)
+  double* lane_vals;        // [2][kLanes][kMaxRed] lane values by flat-barrier parity (lane_fast)
   double tol;
   long long timeout_ns;
   PartDev lp[kInlineParts];  // local parts [part_begin, part_end) when they fit

@@ -160,8 +160,11 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+#ifndef LRB_NO_PROXY_FENCE   // diagnostics only (timing; unsafe ordering)
+#define LRB_NO_PROXY_FENCE 0
+#endif
 __device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (!LRB_NO_PROXY_FENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Diagnostic counters per CTA (build with -DLRB_PROF=1; lrb_team_profile_counters):
@@ -175,7 +178,11 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 #endif
 constexpr bool kProf = LRB_PROF != 0;
 constexpr int kCntPer = 8;
-constexpr int kCnt = 4 * kCntPer;
+// + a timeline of the last phase A per CTA (globaltimer ns): entry, issuer's
+// first copy, consumers' first data, consumers done, reducer done, issuer
+// done, barrier entry, barrier exit
+constexpr int kStamps = 8;
+constexpr int kCnt = 4 * kCntPer + kStamps;
 
 struct StreamSmem {
   char* stages;        // n_stages * stage_bytes
@@ -392,6 +399,8 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
       if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
     const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
+    if (kProf && T.prof_cta && kind == 1 && k == k0 && pw == 0)
+      S.cnt[4 * kCntPer + 1] = (unsigned long long)global_ns();
     const PartDev& P = part_of(T, cur.part, INL);
     const Spec sp = spec_of(P);
     const unsigned vec_bytes = unsigned((cur.rows * 8 + 15) & ~15);
@@ -798,6 +807,8 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       mbar_wait(S.full + rp.bar, rp.parity, T.timeout_ns);
       if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
+      if (kProf && T.prof_cta && threadIdx.x == 0 && !ELEM && kind == 1 && k == first_stage(gseq, tm, kTeams))
+        S.cnt[4 * kCntPer + 2] = (unsigned long long)global_ns();
     }
     const WPos wp = wsum_pos(Gk);
     if (Gk >= kSlotRing) {   // the slot's previous stage must be summed
@@ -884,7 +895,7 @@ __device__ __forceinline__ void reduce_phase(const TeamDev& T, const StreamSmem&
     __syncwarp();
     if (lane == 0) mbar_arrive(S.reduced + wp.slot);
   }
-  if (fast && lane < NR) T.lane_vals[size_t(blockIdx.x) * kMaxRed + lane] = lacc;
+  if (fast && lane < NR) lane_slots(T, s_flat_bar)[size_t(blockIdx.x) * kMaxRed + lane] = lacc;
 }
 
 __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& S) {
@@ -900,6 +911,7 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < kCnt) S.cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_flat_bar = 0;
   __syncthreads();
 }
 
@@ -910,8 +922,12 @@ template <int NR, bool INL, bool ELEM, bool PF_NEXT = false, class SpecF, class 
 __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem& S, int& gseq, double* red,
                                              int kind, SpecF&& spec_of, Body&& body) {
   const int ntv = ELEM ? spec_of(part_of(T, T.part_begin, INL)).ntv : 0;
+  const bool stamp = kProf && T.prof_cta && !ELEM && kind == 1;   // timeline of phase A
+  unsigned long long* const ts = S.cnt + 4 * kCntPer;
+  if (stamp && threadIdx.x == 0) ts[0] = (unsigned long long)global_ns();
   if (threadIdx.x >= kReducer) {
     reduce_phase<NR, ELEM>(T, S, gseq, ntv);
+    if (stamp && threadIdx.x == kReducer) ts[4] = (unsigned long long)global_ns();
   } else if (threadIdx.x >= kConsumers) {
     fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
     if constexpr (ELEM)
@@ -919,15 +935,19 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
     else
       produce_spmv<INL>(T, S, gseq, kind, spec_of);
     if constexpr (PF_NEXT) prefetch_next_spmv<INL>(T);
+    if (stamp && threadIdx.x == kConsumers) ts[5] = (unsigned long long)global_ns();
   } else {
     consume_phase<NR, INL, ELEM>(T, S, gseq, kind, ntv, body);
+    if (stamp && threadIdx.x == 0) ts[3] = (unsigned long long)global_ns();
   }
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
+  if (stamp && threadIdx.x == 0) ts[6] = (unsigned long long)global_ns();
   const int K = ELEM ? pack_factor(T, ntv) : 1;
   // the ring is idle here (every stage of the phase was consumed): its shared
   // memory is the scratch of the multi-part barrier reduction
   team_sync<NR>(T, red, K, reinterpret_cast<double*>(S.stages));
+  if (stamp && threadIdx.x == 0) ts[7] = (unsigned long long)global_ns();
   if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 3] += clock64() - c0;
   gseq += stage_count(ELEM ? (T.n_tiles + K - 1) / K : T.n_tiles);
 }

@@ -434,11 +434,13 @@ class Team:
         """Per-CTA SM-cycle counters of the last streaming solve, shape
         (grid, 4 phase kinds, 8) — see stream.cuh kCnt."""
         grid = self.kernel_info(method)["grid"]
-        out = np.zeros(grid * 32, np.int64)
+        out = np.zeros(grid * 40, np.int64)
         n = N.lrb_team_profile_counters(self.h, N.METHODS[method], N.ptr(out), len(out))
         if n < 0:
             N.check(n)
-        return out[:n].reshape(-1, 4, 8)
+        per = out[:n].reshape(-1, 40)
+        self.last_timeline_ns = per[:, 32:40]   # last phase A: see stream.cuh kStamps
+        return per[:, :32].reshape(-1, 4, 8)
 
     def debug(self, n_dev):
         out = np.zeros(1 + n_dev, np.int64)

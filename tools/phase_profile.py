@@ -96,6 +96,20 @@ def main():
             out["waits_us"] = {kind: {nm: round(float(cnt[:, ki, wi].mean()) / mhz, 1)
                                       for wi, nm in enumerate(names)}
                                for ki, kind in enumerate(("init", "A", "B", "C"))}
+            tl = team.last_timeline_ns.astype(np.float64)
+            t0 = tl[:, 0].min()
+            rel = (tl - t0) / 1e3
+            names_tl = ("entry", "first_issue", "first_data", "consumers_done", "reducer_done",
+                        "issuer_done", "barrier_in", "barrier_out")
+            out["last_A_timeline_us"] = {nm: {"min": round(float(rel[:, j].min()), 2),
+                                              "mean": round(float(rel[:, j].mean()), 2),
+                                              "max": round(float(rel[:, j].max()), 2),
+                                              "argmax_cta": int(rel[:, j].argmax())}
+                                         for j, nm in enumerate(names_tl)}
+            # the slowest CTA per counter (stragglers set the phase time)
+            out["waits_us_max"] = {kind: {nm: round(float(cnt[:, ki, wi].max()) / mhz, 1)
+                                          for wi, nm in enumerate(names)}
+                                   for ki, kind in enumerate(("init", "A", "B", "C"))}
         for k, v in sorted(per.items()):
             us = float(np.mean(v))
             out[k] = {"count": len(v) // args.repeat, "us": round(us, 2)}
