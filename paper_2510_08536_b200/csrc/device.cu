@@ -979,7 +979,6 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   const size_t o_lanes = take(sizeof(double) * kMaxRed * kLanes * 2);   // lane_fast: one part
   const size_t o_pred = take(sizeof(double) * kMaxRed * n_parts * 2);  // epoch parity
   const size_t o_red = take(sizeof(double) * kMaxRed);
-  const size_t o_bar = take(sizeof(unsigned) * 2);
   const size_t o_epoch = take(sizeof(unsigned long long));
   const size_t o_flags = take(sizeof(unsigned long long) * n_dev);
   const size_t o_peer_flags = take(sizeof(void*) * n_dev);
@@ -1017,8 +1016,6 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
   H.lane_fast = 0;
   H.part_red = reinterpret_cast<double*>(w + o_pred);
   H.red = reinterpret_cast<double*>(w + o_red);
-  H.bar_count = reinterpret_cast<unsigned*>(w + o_bar);
-  H.bar_gen = H.bar_count + 1;
   H.epoch = reinterpret_cast<unsigned long long*>(w + o_epoch);
   H.flags = reinterpret_cast<unsigned long long*>(w + o_flags);
   H.peer_flags = reinterpret_cast<unsigned long long**>(w + o_peer_flags);

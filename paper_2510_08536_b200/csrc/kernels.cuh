@@ -256,11 +256,12 @@ __device__ __forceinline__ bool lanes_by_cta(const TeamDev& T, int64_t ntiles, i
   return T.lane_fast && (int(gridDim.x) == kLanes || units <= int64_t(gridDim.x));
 }
 
-// Flat barriers passed by this CTA in the current launch (streaming kernels
-// zero it in stream_init).  Its parity selects the lane-value buffer: a CTA
+// Team barriers passed by this CTA in the current launch (every solver kernel
+// zeroes it first).  Barrier b completes when the launch's arrival counter
+// (SolveOut::flat_count, zeroed before the launch) reaches (b + 1) * grid, so
+// no counter is reset in flight.  Its parity selects the lane-value buffer: a CTA
 // can write barrier b+1's lane value only after every CTA arrived at b+1, i.e.
-// after every CTA finished reading barrier b's lane values.  Teams that never
-// take the flat barrier keep parity 0 for writer and reader.
+// after every CTA finished reading barrier b's lane values.
 static __shared__ unsigned s_flat_bar;
 __device__ __forceinline__ double* lane_slots(const TeamDev& T, unsigned bar) {
   return T.lane_vals + size_t(bar & 1u) * kLanes * kMaxRed;
@@ -303,7 +304,7 @@ __device__ __forceinline__ void lane_from_partials(const TeamDev& T, const PartD
 // Part value (last CTA of the barrier, all threads): lanes, then the group tree.
 template <int NR>
 __device__ __forceinline__ void part_value(const TeamDev& T, int p, int K, double (*gs)[kMaxRed],
-                                           double* out) {
+                                           double* out, unsigned bar) {
   const PartDev& P = T.parts[p];
   double acc[NR];
 #pragma unroll
@@ -312,7 +313,7 @@ __device__ __forceinline__ void part_value(const TeamDev& T, int p, int K, doubl
   if (v < kLanes) {
     if (lanes_by_cta(T, P.ntiles, K)) {
       // lanes >= grid have no units (lanes_by_cta) and were not written
-      const double* lv = lane_slots(T, s_flat_bar) + (size_t(p - T.part_begin) * kLanes + v) * kMaxRed;
+      const double* lv = lane_slots(T, bar) + (size_t(p - T.part_begin) * kLanes + v) * kMaxRed;
       if (v < int(gridDim.x))
 #pragma unroll
         for (int j = 0; j < NR; ++j) acc[j] = __ldcg(lv + j);
@@ -438,6 +439,9 @@ __device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu64(unsigned lo
 __device__ __forceinline__ void red_add_release_gpu64(unsigned long long* p) {
   asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
 }
+__device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -525,7 +529,7 @@ __device__ __forceinline__ void flat_sync(const TeamDev& T, double* red, double 
 constexpr int kSmemParts = 16;
 template <int NR>
 __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch = nullptr) {
-  __shared__ unsigned s_last, s_gen;
+  __shared__ unsigned s_last;
   __shared__ double gs[kLaneGroups][kMaxRed];
   __shared__ double pv[kMaxRed];
   __shared__ double pvals[kSmemParts][kMaxRed];
@@ -534,11 +538,11 @@ __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch 
     flat_sync<NR>(T, red, gs, pv, s_last);
     return;
   }
+  const unsigned bar = s_flat_bar;   // every thread, before thread 0 advances it
   if (threadIdx.x == 0) {
-    s_gen = ld_acquire_gpu(T.bar_gen);
     if (T.n_dev > 1) __threadfence_system();
-    const unsigned t = atom_add_acq_rel_gpu(T.bar_count, 1u);
-    s_last = (t == gridDim.x - 1);
+    const unsigned long long t = atom_add_acq_rel_gpu64(&T.out->flat_count);
+    s_last = (t + 1 == (unsigned long long)(bar + 1) * gridDim.x);
   }
   __syncthreads();
   if (s_last) {
@@ -559,7 +563,7 @@ __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch 
 #pragma unroll
           for (int j = 0; j < NR; ++j) pv[j] = scratch[(p - T.part_begin) * NR + j];
       } else {
-        part_value<NR>(T, p, K, gs, pv);
+        part_value<NR>(T, p, K, gs, pv, bar);
       }
 #ifdef LRB_STAMP3
       if (threadIdx.x == 0 && T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
@@ -606,8 +610,8 @@ __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch 
         pv[j] = s;
       }
       if (T.prof && *T.prof_n < T.prof_cap) T.prof[(*T.prof_n)++] = global_ns();
-      *T.bar_count = 0;
-      red_add_release_gpu(T.bar_gen, 1u);
+      s_flat_bar = bar + 1;
+      st_release_gpu64(&T.out->flat_gen, bar + 1);
     }
     __syncthreads();
 #pragma unroll
@@ -616,7 +620,8 @@ __device__ void team_sync(const TeamDev& T, double* red, int K, double* scratch 
   }
   if (threadIdx.x == 0) {
     const long long t0 = global_ns();
-    while (ld_acquire_gpu(T.bar_gen) == s_gen) {
+    s_flat_bar = bar + 1;
+    while (ld_acquire_gpu64(&T.out->flat_gen) < bar + 1) {
       __nanosleep(32);
       if (global_ns() - t0 > T.timeout_ns) {
         team_fail(T, LRB_ETIMEOUT);
@@ -765,6 +770,7 @@ __device__ __forceinline__ bool team_failed(const TeamDev& T) {
 template <bool JAC, bool INL>
 __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
+  if (threadIdx.x == 0) s_flat_bar = 0;   // ordered by team_sync's entry barrier
   double red[2];
   // phase 0: x = 0, r = b, partial b.b (and r.z)
   team_phase<2, INL>(T, red, JAC ? 2 : 1, [&](const PartDev& P, int64_t i, double (&acc)[2]) {
@@ -892,6 +898,7 @@ __global__ void __launch_bounds__(kTPB, LRB_MINB) team_cg_kernel(const __grid_co
 template <bool INL>
 __global__ void __launch_bounds__(kTPB, LRB_MINB) team_bicgstab_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
+  if (threadIdx.x == 0) s_flat_bar = 0;   // ordered by team_sync's entry barrier
   double red[2];
   team_phase<1, INL>(T, red, 1, [&](const PartDev& P, int64_t i, double (&acc)[1]) {
     const double b = P.b[i];

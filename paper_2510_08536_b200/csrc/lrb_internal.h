@@ -167,6 +167,8 @@ struct SolveOut {
   // arrivals at the flat team barrier (kernels.cuh: team_sync); zeroed with
   // the rest of the record before every launch
   unsigned long long flat_count;
+  // barriers released by the last CTA (kernels.cuh: team_sync), same lifetime
+  unsigned long long flat_gen;
 };
 
 // Descriptors of up to kInlineParts local parts ride in the kernel parameter
@@ -188,8 +190,6 @@ struct TeamDev {
   double* partials;         // [kMaxRed][n_tiles] (one reduction's tiles contiguous)
   double* part_red;         // [2][n_parts][kMaxRed] all parts' values, by epoch parity
   double* red;              // [kMaxRed] team-reduced values (this device)
-  unsigned int* bar_count;
-  unsigned int* bar_gen;
   unsigned long long* epoch;    // barrier epoch (this device)
   unsigned long long* flags;    // [n_dev] arrival epochs written by peers
   // peers' arrays (index = device rank), valid when n_dev > 1
