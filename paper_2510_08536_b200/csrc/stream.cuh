@@ -178,9 +178,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 #endif
 constexpr bool kProf = LRB_PROF != 0;
 constexpr int kCntPer = 8;
-// + a timeline of the last phase A per CTA (globaltimer ns): entry, issuer's
-// first copy, consumers' first data, consumers done, reducer done, issuer
-// done, barrier entry, barrier exit
+// + a timeline of the last phase A per CTA (globaltimer ns): entry, issuer
+// past the proxy fence, issuer before / after its first stage's copies,
+// consumers' first data, consumers done, reducer done, barrier exit
 constexpr int kStamps = 8;
 constexpr int kCnt = 4 * kCntPer + kStamps;
 
@@ -337,6 +337,14 @@ __device__ __forceinline__ void load_pf_addr(const StageHdr* h, PfAddr& a) {
   a.tma = __ldg(&h->tma);
 }
 
+// Header of each issuer's first stage of the coming SpMV phase, loaded by
+// the issuer before the preceding barrier (prefetch_next_spmv) so the phase's
+// first copies are issued without a global-memory round trip.  Tag: the
+// global stage index it belongs to (-1: none).  Only the issuer lane touches
+// its entry.
+static __shared__ HdrAddr s_hdr[kIssuers];
+static __shared__ int s_hdr_g[kIssuers];
+
 // SpMV phases: issuer pw issues stages k = pw, pw + kIssuers, ... (tile
 // cta + k * grid), reading each tile's header one of its stages ahead.
 template <bool INL, class SpecF>
@@ -353,7 +361,12 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
   const Ring R = make_ring(T.n_stages);
   HdrAddr cur{}, nxt{};
   const int k0 = first_stage(gseq, pw, kIssuers);
-  if (k0 < count) load_hdr_addr(hdrs + blockIdx.x + k0 * G, cur);
+  if (k0 < count) {
+    if (s_hdr_g[pw] == gseq + k0)
+      cur = s_hdr[pw];
+    else
+      load_hdr_addr(hdrs + blockIdx.x + k0 * G, cur);
+  }
   // Deep L2 prefetch of the values LRB_PF_DIST of this issuer's tiles ahead
   // (the TMA ring holds ~1 stage in flight per SM; L2 prefetches need no
   // shared memory).  pf = the header fields of the tile prefetched next.
@@ -373,34 +386,17 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
   }
   for (int k = k0; k < count; k += kIssuers) {
     const int64_t tile = blockIdx.x + k * G;
-    if (k + kIssuers < count) load_hdr_addr(hdrs + tile + kIssuers * G, nxt);
-    if (kPf > 1 && k + kPf * kIssuers < count) {
-      if (pf.tma) bulk_prefetch_l2(part_of(T, pf.part, INL).val + pf.e0, unsigned(pf.vbytes));
-      if (k + (kPf + 1) * kIssuers < count) load_pf_addr(hdrs + tile + int64_t(kPf + 1) * kIssuers * G, pf);
-    }
-    if (LRB_ISSUER_PREFETCH && k + kIssuers < count && nxt.tma) {
-      // this issuer's next tile: bring its values and operand windows toward
-      // L2 while it waits for a free slot (its copies then hit L2)
-      const PartDev& Pn = part_of(T, nxt.part, INL);
-      const Spec spn = spec_of(Pn);
-      bulk_prefetch_l2(Pn.val + nxt.e0, unsigned(nxt.vbytes));
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int w = 0; w < kMaxWin; ++w)
-          if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
-    }
     const RingPos rp = ring_pos(gseq + k, R);
     char* st = S.stages + size_t(rp.slot) * T.stage_bytes;
     uint64_t* full = S.full + rp.bar;
+    const bool tl = kProf && T.prof_cta && kind == 1 && k == k0 && pw == 0;   // timeline stamps
+    if (tl) S.cnt[4 * kCntPer + 2] = (unsigned long long)global_ns();
     {
       const long long c0 = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
       wait_slot_free(S, gseq + k, R, T.timeout_ns);
       if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 2] += clock64() - c0;
     }
     const long long ci = (kProf && T.prof_cta && pw == 0) ? clock64() : 0;
-    if (kProf && T.prof_cta && kind == 1 && k == k0 && pw == 0)
-      S.cnt[4 * kCntPer + 1] = (unsigned long long)global_ns();
     const PartDev& P = part_of(T, cur.part, INL);
     const Spec sp = spec_of(P);
     const unsigned vec_bytes = unsigned((cur.rows * 8 + 15) & ~15);
@@ -436,6 +432,25 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + cur.row0, vec_bytes, full, pol_vec);
     }
     if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 7] += clock64() - ci;
+    if (tl) S.cnt[4 * kCntPer + 3] = (unsigned long long)global_ns();
+    // this issuer's next tile: its header, and its values and operand windows
+    // toward L2 while this issuer waits for its next slot (the copies then
+    // hit L2).  After the issue, so a phase's first copies never wait on it.
+    if (k + kIssuers < count) load_hdr_addr(hdrs + tile + kIssuers * G, nxt);
+    if (kPf > 1 && k + kPf * kIssuers < count) {
+      if (pf.tma) bulk_prefetch_l2(part_of(T, pf.part, INL).val + pf.e0, unsigned(pf.vbytes));
+      if (k + (kPf + 1) * kIssuers < count) load_pf_addr(hdrs + tile + int64_t(kPf + 1) * kIssuers * G, pf);
+    }
+    if (LRB_ISSUER_PREFETCH && k + kIssuers < count && nxt.tma) {
+      const PartDev& Pn = part_of(T, nxt.part, INL);
+      const Spec spn = spec_of(Pn);
+      bulk_prefetch_l2(Pn.val + nxt.e0, unsigned(nxt.vbytes));
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int w = 0; w < kMaxWin; ++w)
+          if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
+    }
     cur = nxt;
   }
 }
@@ -450,13 +465,20 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
 #define LRB_XPF 3
 #endif
 template <bool INL>
-__device__ __forceinline__ void prefetch_next_spmv(const TeamDev& T) {
+__device__ __forceinline__ void prefetch_next_spmv(const TeamDev& T, int gnext) {
   if (LRB_XPF <= 0 || !T.tile_hdr) return;
   const int pw = (int(threadIdx.x) - kConsumers) >> 5;
   if ((threadIdx.x & 31) != 0) return;
   const StageHdr* hdrs = reinterpret_cast<const StageHdr*>(T.tile_hdr);
   const TileRec* recs = reinterpret_cast<const TileRec*>(T.tile_rec);
   const int64_t G = gridDim.x;
+  {   // this issuer's first header of the next phase (produce_spmv's cur)
+    const int k0 = first_stage(gnext, pw, kIssuers);
+    if (k0 < stage_count(T.n_tiles)) {
+      load_hdr_addr(hdrs + blockIdx.x + int64_t(k0) * G, s_hdr[pw]);
+      s_hdr_g[pw] = gnext + k0;
+    }
+  }
   for (int k = pw; k < LRB_XPF; k += kIssuers) {
     const int64_t tile = blockIdx.x + int64_t(k) * G;
     if (tile >= T.n_tiles) break;
@@ -808,7 +830,7 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
       mbar_wait(S.full + rp.bar, rp.parity, T.timeout_ns);
       if (kProf && T.prof_cta && threadIdx.x == 0) S.cnt[kind * kCntPer + 0] += clock64() - c0;
       if (kProf && T.prof_cta && threadIdx.x == 0 && !ELEM && kind == 1 && k == first_stage(gseq, tm, kTeams))
-        S.cnt[4 * kCntPer + 2] = (unsigned long long)global_ns();
+        S.cnt[4 * kCntPer + 4] = (unsigned long long)global_ns();
     }
     const WPos wp = wsum_pos(Gk);
     if (Gk >= kSlotRing) {   // the slot's previous stage must be summed
@@ -912,6 +934,7 @@ __device__ __forceinline__ void stream_init(const TeamDev& T, const StreamSmem& 
   }
   if (threadIdx.x < kCnt) S.cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_flat_bar = 0;
+  if (threadIdx.x < kIssuers) s_hdr_g[threadIdx.x] = -1;
   __syncthreads();
 }
 
@@ -927,22 +950,24 @@ __device__ __forceinline__ void stream_phase(const TeamDev& T, const StreamSmem&
   if (stamp && threadIdx.x == 0) ts[0] = (unsigned long long)global_ns();
   if (threadIdx.x >= kReducer) {
     reduce_phase<NR, ELEM>(T, S, gseq, ntv);
-    if (stamp && threadIdx.x == kReducer) ts[4] = (unsigned long long)global_ns();
+    if (stamp && threadIdx.x == kReducer) ts[6] = (unsigned long long)global_ns();
   } else if (threadIdx.x >= kConsumers) {
     fence_proxy_async_global();   // peers' generic writes of the last phase -> our bulk reads
+    if (stamp && threadIdx.x == kConsumers) ts[1] = (unsigned long long)global_ns();
     if constexpr (ELEM)
       produce_elementwise<INL>(T, S, gseq, kind, spec_of);
     else
       produce_spmv<INL>(T, S, gseq, kind, spec_of);
-    if constexpr (PF_NEXT) prefetch_next_spmv<INL>(T);
-    if (stamp && threadIdx.x == kConsumers) ts[5] = (unsigned long long)global_ns();
+    if constexpr (PF_NEXT) {
+      const int K = ELEM ? pack_factor(T, ntv) : 1;
+      prefetch_next_spmv<INL>(T, gseq + stage_count(ELEM ? (T.n_tiles + K - 1) / K : T.n_tiles));
+    }
   } else {
     consume_phase<NR, INL, ELEM>(T, S, gseq, kind, ntv, body);
-    if (stamp && threadIdx.x == 0) ts[3] = (unsigned long long)global_ns();
+    if (stamp && threadIdx.x == 0) ts[5] = (unsigned long long)global_ns();
   }
   fence_proxy_async_global();
   const long long c0 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
-  if (stamp && threadIdx.x == 0) ts[6] = (unsigned long long)global_ns();
   const int K = ELEM ? pack_factor(T, ntv) : 1;
   // the ring is idle here (every stage of the phase was consumed): its shared
   // memory is the scratch of the multi-part barrier reduction

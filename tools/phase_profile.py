@@ -99,13 +99,18 @@ def main():
             tl = team.last_timeline_ns.astype(np.float64)
             t0 = tl[:, 0].min()
             rel = (tl - t0) / 1e3
-            names_tl = ("entry", "first_issue", "first_data", "consumers_done", "reducer_done",
-                        "issuer_done", "barrier_in", "barrier_out")
-            out["last_A_timeline_us"] = {nm: {"min": round(float(rel[:, j].min()), 2),
-                                              "mean": round(float(rel[:, j].mean()), 2),
-                                              "max": round(float(rel[:, j].max()), 2),
-                                              "argmax_cta": int(rel[:, j].argmax())}
-                                         for j, nm in enumerate(names_tl)}
+            names_tl = ("entry", "issuer_fenced", "issuer_hdr", "issuer_issued", "first_data",
+                        "consumers_done", "reducer_done", "barrier_out")
+            out["last_A_timeline_us"] = {}
+            for j, nm in enumerate(names_tl):
+                ok = tl[:, j] >= tl[:, 0]   # stamps left over from an earlier phase A are stale
+                if not ok.any():
+                    continue
+                col = np.where(ok, rel[:, j], np.nan)
+                out["last_A_timeline_us"][nm] = {
+                    "min": round(float(np.nanmin(col)), 2), "mean": round(float(np.nanmean(col)), 2),
+                    "max": round(float(np.nanmax(col)), 2), "argmax_cta": int(np.nanargmax(col)),
+                    "ctas": int(ok.sum())}
             # the slowest CTA per counter (stragglers set the phase time)
             out["waits_us_max"] = {kind: {nm: round(float(cnt[:, ki, wi].max()) / mhz, 1)
                                           for wi, nm in enumerate(names)}
