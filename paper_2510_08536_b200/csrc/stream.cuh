@@ -40,18 +40,27 @@
 
 namespace lrb {
 
-constexpr int kTeams = 2;                         // 16 consumer warps in two teams
-constexpr int kTeamThreads = kTPB;
-constexpr int kConsumers = kTeams * kTeamThreads;
+#ifndef LRB_TEAMS
+#define LRB_TEAMS 2
+#endif
+constexpr int kTeams = LRB_TEAMS;                 // 16 consumer warps in one or two teams
+constexpr int kConsumers = 16 * 32;
+constexpr int kTeamThreads = kConsumers / kTeams;
 constexpr int kTeamWarps = kTeamThreads / 32;
-static_assert(kTile == kTPB * kRPT,
-              "a team thread computes rows t + m * kTPB (m < kRPT), like the classic kernels");
-// issuer p fills exactly the stages team p consumes (G % kTeams == p)
+constexpr int kSRPT = kTile / kTeamThreads;       // rows per team thread and tile
+static_assert((kTeams == 1 || kTeams == 2) && kSRPT * kTeamThreads == kTile,
+              "a team thread computes rows t + m * kTeamThreads (m < kSRPT); warp w of a team "
+              "produces groups w + m * kTeamWarps of the canonical tile tree");
 #ifndef LRB_ISSUERS
 #define LRB_ISSUERS 2
 #endif
 constexpr int kIssuers = LRB_ISSUERS;             // producer warps (alternate stages)
-static_assert(kIssuers == 1 || kIssuers == kTeams, "one issuer, or one per consumer team");
+// Two teams: issuer p fills exactly the stages team p consumes (G % kTeams ==
+// p).  One team: the issuers alternate; the issuer of stage G waits for the
+// slot's use G - ns, and its own previous stage (G - 2) needed G - 2 - ns
+// consumed, so G - 2 ns was consumed before (one team consumes in order): the
+// parity wait is never a stale phase.
+static_assert(kIssuers == 1 || kIssuers == 2, "one or two issuer warps");
 // One CTA per SM; 19 warps put 5 on some SM sub-partitions, so a thread
 // gets at most 96 registers (16384 per sub-partition).
 #define LRB_STREAM_BOUNDS __launch_bounds__(kStreamThreads, 1)
@@ -848,18 +857,18 @@ __device__ __forceinline__ void consume_phase(const TeamDev& T, const StreamSmem
                       size_t(cnt) * kVecTileBytes};
       const StageHdr& H = *reinterpret_cast<const StageHdr*>(st);
       const PartDev& P = part_of(T, H.part, INL);
-      double acc[kRPT][NR];
+      double acc[kSRPT][NR];
       const long long c3 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
 #pragma unroll
-      for (int m = 0; m < kRPT; ++m) {
+      for (int m = 0; m < kSRPT; ++m) {
 #pragma unroll
         for (int q = 0; q < NR; ++q) acc[m][q] = 0.0;
-        if (!(LRB_NOCOMPUTE && !ELEM)) body(P, H, st, V, tt + m * kTPB, acc[m]);
+        if (!(LRB_NOCOMPUTE && !ELEM)) body(P, H, st, V, tt + m * kTeamThreads, acc[m]);
       }
       const long long c4 = (kProf && T.prof_cta && threadIdx.x == 0) ? clock64() : 0;
       double* ws = S.wsum + size_t(wp.slot * kMaxPack + j) * kGroups * kSlotNR;
 #pragma unroll
-      for (int m = 0; m < kRPT; ++m) {
+      for (int m = 0; m < kSRPT; ++m) {
         group_reduce<NR>(acc[m]);
         if (lane == 0)
 #pragma unroll
