@@ -191,8 +191,14 @@ def solve_bytes(n, nnz, h, iterations, checks, method):
     """Algorithmic HBM bytes of one solve: CG it 12nnz+4(n+1)+88n+8h, PCG +16n,
     true-residual check 12nnz+4(n+1)+16n+8h, init (b read, x r written) 24n.
     pcg1 (single reduction): it 12nnz+4(n+1)+8h + 88n (r, dinv, w, s_old and
-    p, x read; p, x, r, s, w written), init + one SpMV 12nnz+4(n+1)+24n+8h."""
+    p, x read; p, x, r, s, w written), init + one SpMV 12nnz+4(n+1)+24n+8h.
+    pipecg (pipelined): it 12nnz+4(n+1)+8h + 104n (w, dinv, z, s, p, x, r read;
+    z, s, p, x, r, w written), init as pcg1 (the final x copy, 16n when the
+    last iterate sits in the second buffer, is not counted)."""
     chk = 12 * nnz + 4 * (n + 1) + 16 * n + 8 * h
+    if method == "pipecg":
+        it = 12 * nnz + 4 * (n + 1) + 104 * n + 8 * h
+        return iterations * it + checks * chk + 24 * n + 12 * nnz + 4 * (n + 1) + 24 * n + 8 * h
     if method == "pcg1":
         it = 12 * nnz + 4 * (n + 1) + 88 * n + 8 * h
         return iterations * it + checks * chk + 24 * n + 12 * nnz + 4 * (n + 1) + 24 * n + 8 * h
@@ -597,7 +603,10 @@ def run_ours_multi(args):
 
 def kernel_name(info, method):
     """The solve kernel that ran (lrb_team_kernel_info): streaming or classic."""
-    jac = "true" if method in ("pcg", "pcg1") else "false"
+    jac = "true" if method in ("pcg", "pcg1", "pipecg") else "false"
+    if info and info.get("streaming") and method == "pipecg":
+        return (f"team_pipecg_stream_kernel (pipelined Jacobi-PCG, reduction read one phase late, bulk-copy "
+                f"ring: {info['stages']} x {info['stage_bytes']} B stages, {info['grid']} x {info['block']} threads)")
     if info and info.get("streaming") and method == "pcg1":
         return (f"team_pcg1_stream_kernel (single-reduction Jacobi-PCG, bulk-copy ring: {info['stages']} x "
                 f"{info['stage_bytes']} B stages, {info['grid']} x {info['block']} threads)")
@@ -1241,7 +1250,7 @@ def main():
     ap.add_argument("--rpg", type=int, default=None, help="CPU ranks per GPU (alpha)")
     ap.add_argument("--n", type=int, default=None, help="cavity edge (c4; default 300)")
     ap.add_argument("--mode", choices=("direct", "staged"), default="direct")
-    ap.add_argument("--method", choices=("cg", "pcg", "pcg1"), default=None)
+    ap.add_argument("--method", choices=("cg", "pcg", "pcg1", "pipecg"), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pageable", action="store_true",
                     help="skip the pageable-input e2e leg")

@@ -36,6 +36,9 @@ extern "C" {
 #define LRB_METHOD_BICGSTAB 2  /* BiCGStab */
 #define LRB_METHOD_PCG1 3      /* single-reduction (Chronopoulos-Gear) Jacobi-PCG, SURVEY.md §8 f1:
                                   one team barrier per iteration; CG's iterates up to rounding */
+#define LRB_METHOD_PIPECG 4    /* pipelined (Ghysels-Vanroose) Jacobi-PCG: the
+                                  iteration's reduction completes behind the next SpMV (flat
+                                  teams read it one phase late); CG's iterates up to rounding */
 
 const char* lrb_last_error(void);
 const char* lrb_version(void);

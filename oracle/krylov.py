@@ -261,3 +261,75 @@ def pcg1(S: DistSystem, bs, tol, max_iter):
         else:
             res = rec
     return xs, Report(it, float(res), converged, hist, log)
+
+
+def pipecg(S: DistSystem, bs, tol, max_iter):
+    """Pipelined Jacobi-PCG (Ghysels-Vanroose).
+
+    The iteration's SpMV n = A m (m = M w) does not depend on the scalars of
+    the reduction issued just before it, so that reduction can complete while
+    the SpMV runs (the B200 kernel reads it one phase late):
+      beta = gamma / gamma_prev, eta = delta - beta * (gamma / alpha_prev),
+      alpha = gamma / eta;  n = A (M w);
+      z = n + beta z,  s = w + beta s,  p = M r + beta p,
+      x += alpha p,  r -= alpha s,  w -= alpha z,
+      (gamma, delta, rho) = (r.Mr, w.Mr, r.r)   -- one fused allreduce.
+    With M = diag^-1 the preconditioned recurrences u = M r, m = M w and
+    q = M s of the published algorithm are formed directly from r, w and s
+    (the same vectors in exact arithmetic; no drift of u against r).  CG's
+    iterates up to rounding; same stopping rule as cg_solve
+    (solver.py:136-142) and the same breakdown error as the reference's
+    p.q <= 0 (solver.py:129-130).
+    """
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    log, hist = [], []
+    xs = [np.zeros(len(b)) for b in bs]
+    bb = S.dot(bs, bs)
+    log.append(bb)
+    if bb == 0.0:
+        return xs, Report(0, 0.0, True, hist, log)
+    bnorm = math.sqrt(bb)
+    dinv = S.dinv()
+    rs = [b.astype(np.float64).copy() for b in bs]
+    us = [d * r for d, r in zip(dinv, rs)]
+    ws = S.spmv(us)
+    gamma, delta = S.dot(rs, us), S.dot(ws, us)
+    log += [gamma, delta]
+    gamma_prev = alpha_prev = 1.0
+    zs = ss = ps = None
+    res, converged, it = 1.0, False, 0
+    for it in range(1, max_iter + 1):
+        first = it == 1
+        beta = 0.0 if first else gamma / gamma_prev
+        eta = delta if first else delta - beta * (gamma / alpha_prev)
+        if eta <= 0.0:
+            raise ValueError("cg: matrix is not positive definite")
+        alpha = gamma / eta
+        ns = S.spmv([d * w for d, w in zip(dinv, ws)])
+        if first:
+            zs = ns
+            ss = [w.copy() for w in ws]
+            ps = [d * r for d, r in zip(dinv, rs)]
+        else:
+            zs = [n + beta * z for n, z in zip(ns, zs)]
+            ss = [w + beta * s_ for w, s_ in zip(ws, ss)]
+            ps = [d * r + beta * p for d, r, p in zip(dinv, rs, ps)]
+        for x, p in zip(xs, ps):
+            x += alpha * p
+        rs = [r - alpha * s_ for r, s_ in zip(rs, ss)]
+        ws = [w - alpha * z for w, z in zip(ws, zs)]
+        us = [d * r for d, r in zip(dinv, rs)]
+        gamma_prev, alpha_prev = gamma, alpha
+        gamma, delta, rr = S.dot(rs, us), S.dot(ws, us), S.dot(rs, rs)
+        log += [gamma, delta, rr]
+        rec = math.sqrt(rr) / bnorm
+        hist.append(rec)
+        if rec <= tol or it % 10 == 0:
+            res = _true_residual(S, bs, xs, bnorm, log)
+            if res <= tol:
+                converged = True
+                break
+        else:
+            res = rec
+    return xs, Report(it, float(res), converged, hist, log)

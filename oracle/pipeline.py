@@ -42,6 +42,8 @@ class OraclePipeline:
             return krylov.cg(self.system, bs, tol, max_iter, jacobi=True)
         if method == "pcg1":
             return krylov.pcg1(self.system, bs, tol, max_iter)
+        if method == "pipecg":
+            return krylov.pipecg(self.system, bs, tol, max_iter)
         if method == "bicgstab":
             return krylov.bicgstab(self.system, bs, tol, max_iter)
         raise ValueError(f"unknown method {method!r}")

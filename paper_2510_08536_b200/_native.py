@@ -19,7 +19,7 @@ LRB_ECUDA = -3
 LRB_ENOTPD = -4
 LRB_ETIMEOUT = -5
 
-METHODS = {"cg": 0, "pcg": 1, "bicgstab": 2, "pcg1": 3}
+METHODS = {"cg": 0, "pcg": 1, "bicgstab": 2, "pcg1": 3, "pipecg": 4}
 
 
 class NativeError(RuntimeError):

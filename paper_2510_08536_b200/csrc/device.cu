@@ -808,7 +808,7 @@ int lrb_part_elapsed_ms(lrb_part* part, float* ms) {
 // ---------------------------------------------------------------------------
 namespace lrb {
 
-constexpr int kMethods = 4;
+constexpr int kMethods = 5;
 // the streaming kernels' static shared memory (team_sync scratch, ~3.2 KB)
 // shares the opt-in per-block limit with the dynamic ring
 constexpr int64_t kStaticSmemMargin = 4096;
@@ -822,6 +822,8 @@ static int64_t method_need(int method, int64_t base, int64_t wb) {
       return base + std::max({2 * wb + tv, 2 * wb, wb + tv});
     case LRB_METHOD_PCG1:       // fused phase: r, dinv, w, s_old windows + p, x tiles
       return base + std::max({4 * wb + 2 * tv, 2 * wb, wb + tv});
+    case LRB_METHOD_PIPECG:     // pipelined phase: w, dinv windows + z, s, p, x, r tiles
+      return base + std::max({2 * wb + 5 * tv, 2 * wb, wb + tv});
     default:                    // CG / PCG: z, p_old windows (+ x tile); check: x (+ p) windows + b tile
       return base + (LRB_LAZY_X ? 2 * wb + tv : std::max(2 * wb, wb + tv));
   }
@@ -836,10 +838,10 @@ struct TeamDevice {
   bool cooperative = true;        // whole device to one team kernel
   size_t ws_bytes = 0;
   const void* fn[kMethods] = {};
-  int grid[kMethods] = {};          // per method (CG, PCG, BiCGStab, PCG1)
+  int grid[kMethods] = {};          // per method (CG, PCG, BiCGStab, PCG1, PIPECG)
   size_t smem[kMethods] = {};
-  int block[kMethods] = {kTPB, kTPB, kTPB, kTPB};
-  int stage_bytes[kMethods] = {};   // streaming ring per method (BiCGStab / PCG1 stage more windows)
+  int block[kMethods] = {kTPB, kTPB, kTPB, kTPB, kTPB};
+  int stage_bytes[kMethods] = {};   // streaming ring per method (BiCGStab / PCG1 / PIPECG stage more)
   int n_stages[kMethods] = {};
   bool streaming[kMethods] = {};    // streaming (bulk-copy) kernel for this method
   cudaStream_t stream = nullptr;  // main stream of the first local part
@@ -1127,7 +1129,7 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
     } else {
       D.stage_bytes[m] = m_bytes[m];   // the reduction tree's units (classic kernels)
       D.fn[m] = solve_kernel(m, D.inl);
-      if (!D.fn[m]) continue;   // PCG1 exists only as a streaming kernel
+      if (!D.fn[m]) continue;   // PCG1 / PIPECG exist only as streaming kernels
       D.grid[m] = max_grid(D.fn[m], D.device, D.n_tiles, n_share, stage, &D.smem[m]);
     }
     if (D.grid[m] <= 0) {
@@ -1226,6 +1228,8 @@ static const void* stream_kernel(int method, bool inl) {
       return bicgstab_stream_kernel(inl);
     case LRB_METHOD_PCG1:
       return pcg1_stream_kernel(inl);
+    case LRB_METHOD_PIPECG:
+      return pipecg_stream_kernel(inl);
     default:
       return nullptr;
   }
@@ -1885,7 +1889,7 @@ int lrb_team_solve(lrb_team* team, int32_t method, const double* const* b_host,
   }
   for (auto& D : team->devs)
     if (!D.fn[method]) {
-      set_error("lrb_team_solve: pcg1 (single-reduction PCG) needs the streaming solver "
+      set_error("lrb_team_solve: pcg1 / pipecg need the streaming solver "
                 "(unset LRB_SOLVER=classic; stages must fit shared memory)");
       return LRB_EVALUE;
     }
@@ -2127,7 +2131,7 @@ int lrb_team_solve_async(lrb_team* team, int32_t method, const double* const* b_
   }
   for (auto& D : team->devs)
     if (!D.fn[method]) {
-      set_error("lrb_team_solve_async: pcg1 needs the streaming solver");
+      set_error("lrb_team_solve_async: pcg1 / pipecg need the streaming solver");
       return LRB_EVALUE;
     }
   std::lock_guard<std::mutex> lk(team->mu);

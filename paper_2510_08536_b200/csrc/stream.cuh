@@ -1640,3 +1640,400 @@ __global__ void LRB_STREAM_BOUNDS
 }
 
 }  // namespace lrb
+
+namespace lrb {
+
+// ---------------------------------------------------------------------------
+// Pipelined Jacobi-PCG (Ghysels-Vanroose, method "pipecg").
+// The iteration's SpMV n = A (M w) does not depend on the scalars of the
+// reduction issued at the end of the previous phase, so on a flat team (one
+// device, one part: every CTA its own reduction lane, kernels.cuh flat_sync)
+// the barrier between phases only waits for the arrivals (neighbour data
+// complete) and the reduction itself is read one phase late: the reducer warp
+// combines the previous barrier's lane values (the canonical tree) while the
+// consumers run the SpMV of their first stage, and the consumers pick the
+// scalars up before the first elementwise update.  Other teams reduce at the
+// barrier (same tree, same bits).
+//   beta = gamma / gamma_prev, eta = delta - beta * gamma / alpha_prev,
+//   alpha = gamma / eta;  n = A (M w);  z = n + beta z;  s = w + beta s;
+//   p = M r + beta p;  x += alpha p;  r -= alpha s;  w -= alpha z;
+//   (gamma, delta, rho) = (r.Mr, w.Mr, r.r)
+// oracle/krylov.py pipecg restates it.  The scalars of state k are known only
+// during phase k+1, so the stopping decision for iteration k is taken after
+// phase k+1: x is double-buffered (x_k in buffer k & 1) and that decision's
+// true-residual check reads x_k; w is double-buffered (the SpMV reads its
+// window while the phase writes the new w).  Buffers: x in {x, p1}, w in
+// {v0, v1}, z = t, s, p = p0, r.
+// ---------------------------------------------------------------------------
+static __shared__ unsigned s_pgen;            // deferred reductions published (reducer warp)
+// by generation parity: a slow thread may still read generation g's values
+// after the phase barrier while the reducer of the next phase writes g + 1
+static __shared__ double s_pscal[2][8];       // their values [0, 3), alpha, beta, breakdown
+static __shared__ double s_pread[kMaxRed];    // flat_read_last
+
+// Canonical tree of barrier b's lane values (flat_sync's, bit for bit), by
+// one warp; lane 0 writes out[0..NR).
+template <int NR>
+__device__ __forceinline__ void lanes_tree_warp(const TeamDev& T, unsigned b, double* out) {
+  const int lane = threadIdx.x & 31;
+  const double* lv = lane_slots(T, b);
+  double x[kLaneGroups][NR];
+#pragma unroll
+  for (int g = 0; g < kLaneGroups; ++g) {
+    const int v = g * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) x[g][j] = v < int(gridDim.x) ? __ldcg(lv + size_t(v) * kMaxRed + j) : 0.0;
+  }
+  double s[NR];
+#pragma unroll
+  for (int g = 0; g < kLaneGroups; ++g)
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double a = x[g][j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+      s[j] = g == 0 ? a : __dadd_rn(s[j], a);
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < NR; ++j) out[j] = s[j];
+}
+
+// Arrival-only flat barrier: lane values stay in their parity slot for a
+// later lanes_tree_warp; the count is launch-monotonic like flat_sync's.
+__device__ __forceinline__ void flat_arrive(const TeamDev& T) {
+  __syncthreads();
+  const unsigned b = s_flat_bar;
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = &T.out->flat_count;
+    const unsigned long long target = (unsigned long long)(b + 1) * gridDim.x;
+    red_add_release_gpu64(cnt);
+    const long long t0 = global_ns();
+    while (ld_acquire_gpu64(cnt) < target) {
+      if (LRB_FLAT_POLL_NS) __nanosleep(LRB_FLAT_POLL_NS);
+      if (global_ns() - t0 > T.timeout_ns) {
+        team_fail(T, LRB_ETIMEOUT);
+        break;
+      }
+    }
+    s_flat_bar = b + 1;
+  }
+  __syncthreads();
+}
+
+// The last barrier's pending lane values, read now by every thread.
+template <int NR>
+__device__ __forceinline__ void flat_read_last(const TeamDev& T, double* red) {
+  __syncthreads();   // every thread has read the previous s_pscal values
+  if (threadIdx.x < 32) lanes_tree_warp<NR>(T, s_flat_bar - 1, s_pread);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < NR; ++j) red[j] = s_pread[j];
+  __syncthreads();
+}
+
+// SpMV phase with the pipelined barrier: din = the reducer publishes the
+// previous barrier's reduction and coef()'s scalars from it (generation
+// `want`) before its own stages;
+// dout = arrival-only barrier (flat teams), else the reducing team_sync.
+template <int NR, bool INL, class SpecF, class CoefF, class PreF, class Body>
+__device__ __forceinline__ void stream_phase_pipe(const TeamDev& T, const StreamSmem& S, int& gseq, double* red,
+                                                  int kind, bool din, bool dout, unsigned want, SpecF&& spec_of,
+                                                  CoefF&& coef, PreF&& pre, Body&& body) {
+  if (threadIdx.x >= kReducer) {
+    if (din) {
+      double* ps = s_pscal[want & 1];
+      lanes_tree_warp<NR>(T, s_flat_bar - 1, ps);
+      if ((threadIdx.x & 31) == 0) {
+        coef(ps);   // ps[NR..]: the phase's own scalars
+        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&s_pgen)), "r"(want) : "memory");
+      }
+      __syncwarp();
+    }
+    reduce_phase<NR, false>(T, S, gseq, 0);
+  } else if (threadIdx.x >= kConsumers) {
+    fence_proxy_async_global();
+    produce_spmv<INL>(T, S, gseq, kind, spec_of);
+  } else {
+    if (din) {   // the reducer publishes before its own stages, while the first copies fly
+      unsigned g;
+      do {   // acquire: orders the scalar reads in pre()
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(g) : "r"(smem_u32(&s_pgen)) : "memory");
+      } while (g < want);
+      pre(s_pscal[want & 1]);
+    }
+    consume_phase<NR, INL, false>(T, S, gseq, kind, 0, body);
+  }
+  fence_proxy_async_global();
+  if (dout)
+    flat_arrive(T);
+  else
+    team_sync<NR>(T, red, 1, reinterpret_cast<double*>(S.stages));
+  gseq += stage_count(T.n_tiles);
+}
+
+template <bool INL, bool DEFER>
+__global__ void LRB_STREAM_BOUNDS
+    team_pipecg_stream_kernel(const __grid_constant__ TeamDev T) {
+  const PartDev* __restrict__ parts = T.parts;
+  const StreamSmem S = stream_smem(T);
+  stream_init(T, S);
+  if (threadIdx.x == 0) s_pgen = 0;
+  int gseq = 0;
+  double red[4];
+  auto xbuf = [](const PartDev& Q, int b) -> double* { return b ? Q.p1 : Q.x; };
+  auto wbuf = [](const PartDev& Q, int b) -> double* { return b ? Q.v1 : Q.v0; };
+  // ---- phase 0: x = 0, r = b, b.b
+  stream_phase<1, INL, true>(
+      T, S, gseq, red, 0, [&](const PartDev& P) { return Spec{0, 1, {nullptr}, {P.b}}; },
+      [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&acc)[1]) {
+        if (lr >= H.rows) return;
+        const int64_t i = H.row0 + lr;
+        const double b = V[0][lr];
+        P.x[i] = 0.0;
+        P.r[i] = b;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(b, b));
+      });
+  const double bb = red[0];
+  SolveOut* out = T.out;
+  const bool lead = (blockIdx.x == 0 && threadIdx.x == 0);
+  if (bb == 0.0 || team_failed(T)) {
+    if (lead && bb == 0.0) {
+      out->iterations = 0;
+      out->converged = 1;
+      out->residual = 0.0;
+      out->bnorm = 0.0;
+    }
+    return;
+  }
+  const double bnorm = sqrt(bb);
+  // ---- phase 0b: w0 = A (M r0) into v0, gamma = r.Mr, delta = w.Mr
+  auto u0_g = [](const PartDev& Q, int64_t j) -> double { return __dmul_rn(Q.dinv[j], Q.r[j]); };
+  stream_phase<2, INL, false>(
+      T, S, gseq, red, 1, [&](const PartDev& P) { return Spec{2, 0, {P.r, P.dinv}, {}}; },
+      [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[2]) {
+        double wi, ui;
+        if (H.tma) {
+          const StagedTile t = staged_tile(st, H, 2);
+          const int sl = lr >> 5;
+          const Slots slot = slice_slots(st, H, sl);
+          const double* rw = t.w(0);
+          const double* dw = t.w(1);
+          auto u = [&](int q) { return __dmul_rn(dw[q], rw[q]); };
+          wi = staged_row(P, parts, H, t, slot, lr, u, u0_g, ui);
+          if (lr >= H.rows) return;
+        } else {
+          if (lr >= H.rows) return;
+          const int64_t i = H.row0 + lr;
+          wi = row_spmv(P, parts, i, u0_g);
+          ui = u0_g(P, i);
+        }
+        const int64_t i = H.row0 + lr;
+        P.v0[i] = wi;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(P.r[i], ui));
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(wi, ui));
+      });
+  if (team_failed(T)) return;
+  const bool flat =
+      DEFER && LRB_FLAT_BAR && T.n_dev == 1 && T.n_parts == 1 && lanes_by_cta(T, T.n_tiles, 1);
+  // scalars of the newest state whose reduction was read
+  double gamma = red[0], delta = red[1], gamma_prev = 1.0, alpha_prev = 1.0, res = 1.0;
+  bool pend = false;        // the newest state's reduction still sits in the lane slots
+  bool converged = false, stop = false;
+  int last = 0;             // newest iteration whose stopping decision was taken
+  unsigned pgen = 0;
+  // alpha, beta of a phase from the scalars (g, d) of the state before it
+  // (the reducer warp and, after the phase, every thread: same bits)
+  auto coef = [&](bool first, double g, double d, double& alpha, double& beta) -> bool {
+    beta = first ? 0.0 : g / gamma_prev;
+    const double eta = first ? d : __dsub_rn(d, __dmul_rn(beta, g / alpha_prev));
+    alpha = g / eta;
+    return !(eta > 0.0);
+  };
+  for (int k = 1;; ++k) {
+    const bool run = k <= T.max_iter;
+    const bool first = (k == 1);
+    const bool din = pend && run;
+    double alpha = 0.0, beta = 0.0;
+    bool bad = false;
+    int jd[2];          // iterations whose stopping decision is due after this step
+    double rrd[2];
+    int nd = 0;
+    if (run) {
+      if (!din) {
+        bad = coef(first, gamma, delta, alpha, beta);
+        if (bad) {   // iteration k-1 was decided (not converged): breakdown now
+          if (lead) team_fail(T, LRB_ENOTPD);
+          break;
+        }
+      }
+      const int ob = (k - 1) & 1, nb = k & 1;   // x / w buffers: read ob, write nb
+      auto m_g = [ob](const PartDev& Q, int64_t j) -> double {
+        return __dmul_rn(Q.dinv[j], (ob ? Q.v1 : Q.v0)[j]);
+      };
+      const unsigned want = pgen + 1;
+      stream_phase_pipe<3, INL>(
+          T, S, gseq, red, 1, din, flat, want,
+          [&](const PartDev& P) {
+            return Spec{2, 5, {wbuf(P, ob), P.dinv}, {P.t, P.s, P.p0, xbuf(P, ob), P.r}};
+          },
+          [&](double* pab) {   // reducer warp, lane 0: this phase's alpha, beta, breakdown
+            double a, b;
+            const bool bk = coef(first, pab[0], pab[1], a, b);
+            pab[3] = a;
+            pab[4] = b;
+            pab[5] = bk ? 1.0 : 0.0;
+          },
+          [&](const double* pab) {   // consumers: the phase's scalars from the reducer
+            alpha = pab[3];
+            beta = pab[4];
+            bad = pab[5] != 0.0;
+          },
+          [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[3]) {
+            double n_i, w_i, d_i, z_o, s_o, p_o, x_o, r_i;
+            if (H.tma) {
+              const StagedTile t = staged_tile(st, H, 2);
+              const int sl = lr >> 5;
+              const Slots slot = slice_slots(st, H, sl);
+              const double* ww = t.w(0);
+              const double* dw = t.w(1);
+              auto m = [&](int q) { return __dmul_rn(dw[q], ww[q]); };
+              n_i = staged_row(P, parts, H, t, slot, lr, m, m_g);
+              if (lr >= H.rows || bad) return;
+              const int qd = diag_pos(H, slot, sl, H.row0 + lr);
+              w_i = ww[qd];
+              d_i = dw[qd];
+              z_o = t.tail(0)[lr];
+              s_o = t.tail(1)[lr];
+              p_o = t.tail(2)[lr];
+              x_o = t.tail(3)[lr];
+              r_i = t.tail(4)[lr];
+            } else {
+              if (lr >= H.rows || bad) return;
+              const int64_t i = H.row0 + lr;
+              n_i = row_spmv(P, parts, i, m_g);
+              w_i = wbuf(P, ob)[i];
+              d_i = P.dinv[i];
+              z_o = P.t[i];
+              s_o = P.s[i];
+              p_o = P.p0[i];
+              x_o = xbuf(P, ob)[i];
+              r_i = P.r[i];
+            }
+            const int64_t i = H.row0 + lr;
+            const double u_i = __dmul_rn(d_i, r_i);
+            const double z = first ? n_i : __dadd_rn(n_i, __dmul_rn(beta, z_o));
+            const double s = first ? w_i : __dadd_rn(w_i, __dmul_rn(beta, s_o));
+            const double p = first ? u_i : __dadd_rn(u_i, __dmul_rn(beta, p_o));
+            const double r = __dsub_rn(r_i, __dmul_rn(alpha, s));
+            const double w = __dsub_rn(w_i, __dmul_rn(alpha, z));
+            const double un = __dmul_rn(d_i, r);
+            P.t[i] = z;
+            P.s[i] = s;
+            P.p0[i] = p;
+            xbuf(P, nb)[i] = __dadd_rn(x_o, __dmul_rn(alpha, p));
+            P.r[i] = r;
+            wbuf(P, nb)[i] = w;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(r, un));
+            acc[1] = __dadd_rn(acc[1], __dmul_rn(w, un));
+            acc[2] = __dadd_rn(acc[2], __dmul_rn(r, r));
+          });
+      if (team_failed(T)) break;
+      if (din) {   // state k-1's reduction, read by the reducer during phase k
+        pgen = want;
+        const double* ps = s_pscal[want & 1];
+        const double g = ps[0];
+        bad = coef(first, g, ps[1], alpha, beta);
+        jd[nd] = k - 1;
+        rrd[nd++] = ps[2];
+        gamma_prev = g;
+      } else {
+        gamma_prev = gamma;
+      }
+      alpha_prev = alpha;
+      pend = flat;
+      if (!flat) {   // state k's reduction came with the barrier
+        gamma = red[0];
+        delta = red[1];
+        jd[nd] = k;
+        rrd[nd++] = red[2];
+      }
+    } else {   // max_iter reached: the last state's decision may still be pending
+      if (!pend) break;
+      flat_read_last<3>(T, red);
+      pend = false;
+      jd[nd] = k - 1;
+      rrd[nd++] = red[2];
+    }
+    // stopping decisions (solver.py:136-142), oldest first: recurrence
+    // residual, true residual of x_j (buffer j & 1) at tol or every 10th
+    for (int q = 0; q < nd && !stop; ++q) {
+      const int j = jd[q];
+      const double rec = sqrt(rrd[q]) / bnorm;
+      if (lead && T.hist && j <= T.hist_cap) T.hist[j - 1] = rec;
+      last = j;
+      if (rec <= T.tol || j % 10 == 0) {
+        if (pend) {   // the check's barrier reuses the lane slots: take state k's first
+          flat_read_last<3>(T, red);
+          pend = false;
+          gamma = red[0];
+          delta = red[1];
+          jd[nd] = k;
+          rrd[nd++] = red[2];
+        }
+        const int xb = j & 1;
+        auto xg = [xb](const PartDev& Q, int64_t c) -> double { return (xb ? Q.p1 : Q.x)[c]; };
+        stream_phase<1, INL, false>(
+            T, S, gseq, red, 3, [&](const PartDev& P) { return Spec{1, 1, {xbuf(P, xb)}, {P.b}}; },
+            [&](const PartDev& P, const StageHdr& H, const char* st, const VecView&, int lr, double (&acc)[1]) {
+              if (H.tma) {
+                const StagedTile t = staged_tile(st, H, 1);
+                const Slots slot = slice_slots(st, H, lr >> 5);
+                const double ax = staged_row(P, parts, H, t, slot, lr, Win1{t.w(0)}, xg);
+                if (lr < H.rows) {
+                  const double d = __dsub_rn(t.tail(0)[lr], ax);
+                  acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+                }
+              } else if (lr < H.rows) {
+                const int64_t i = H.row0 + lr;
+                const double ax = row_spmv(P, parts, i, xg);
+                const double d = __dsub_rn(P.b[i], ax);
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+              }
+            });
+        if (team_failed(T)) {
+          stop = true;
+          break;
+        }
+        res = sqrt(red[0]) / bnorm;
+        if (res <= T.tol) {
+          converged = true;
+          stop = true;
+        }
+      } else {
+        res = rec;
+      }
+      if (!stop && din && q == 0 && bad) {   // phase k broke down; iteration k-1 did not converge
+        if (lead) team_fail(T, LRB_ENOTPD);
+        stop = true;
+      }
+    }
+    if (stop || !run) break;
+  }
+  if (!team_failed(T) && (last & 1)) {   // the result x_last sits in the second buffer
+    stream_phase<1, INL, true>(
+        T, S, gseq, red, 0, [&](const PartDev& P) { return Spec{0, 1, {nullptr}, {P.p1}}; },
+        [&](const PartDev& P, const StageHdr& H, const char*, const VecView& V, int lr, double (&)[1]) {
+          if (lr < H.rows) P.x[H.row0 + lr] = V[0][lr];
+        });
+  }
+  stream_flush_counters(T, S);
+  if (lead) {
+    out->iterations = last;
+    out->converged = converged ? 1 : 0;
+    out->residual = res;
+    out->bnorm = bnorm;
+  }
+}
+
+}  // namespace lrb

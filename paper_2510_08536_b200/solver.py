@@ -15,7 +15,7 @@ import numpy as np
 
 from .transport import CommGroup
 
-METHODS = ("cg", "pcg", "bicgstab", "pcg1")
+METHODS = ("cg", "pcg", "bicgstab", "pcg1", "pipecg")
 
 
 @dataclass(frozen=True)
@@ -120,7 +120,10 @@ def cg_solve(matrix, plan: HaloPlan, b, tol: float, max_iter: int, comm: CommGro
     the true residual, max_iter reports instead of raising.  method="pcg"
     selects Jacobi-PCG (pressure), "bicgstab" BiCGStab (momentum), "pcg1" the
     single-reduction (Chronopoulos-Gear) Jacobi-PCG: one team barrier per
-    iteration, CG's iterates up to rounding."""
+    iteration, CG's iterates up to rounding; "pipecg" the
+    pipelined (Ghysels-Vanroose) Jacobi-PCG: one barrier per iteration that
+    only waits for the arrivals, the reduction completes behind the next
+    SpMV (§8 f1)."""
     return krylov_solve(matrix, plan, b, tol, max_iter, comm, method, history)
 
 

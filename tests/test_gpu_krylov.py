@@ -7,6 +7,9 @@ residual history within 1e-10 relative, iterations +-1).
 * Single-reduction Jacobi-PCG (method "pcg1"): against the
   oracle's Chronopoulos-Gear restatement (krylov.pcg1) and, on the
   uniform-diagonal cavity, against the reference's own CG logs.
+* Pipelined Jacobi-PCG (method "pipecg"): against the oracle's
+  Ghysels-Vanroose restatement (krylov.pipecg), the reference's CG logs, and
+  the max_iter edge (the kernel decides iteration k one phase late).
 """
 
 import numpy as np
@@ -38,10 +41,10 @@ def _solve_gpu(pm, per_rank, method, step=None, tol=TOL):
     return lrb.run_world(pm.n_cpu, program, timeout=1800)[0]
 
 
-def _compare(rep, ro, x, xo):
+def _compare(rep, ro, x, xo, rtol=1e-10):
     assert rep.converged and ro.converged
     assert abs(rep.iterations - ro.iterations) <= 1, (rep.iterations, ro.iterations)
-    ok, n = history_ok(rep.history, ro.history)
+    ok, n = history_ok(rep.history, ro.history, rtol=rtol)
     assert ok and n >= min(len(ro.history), rep.iterations) - 1, (rep.history, ro.history)
     np.testing.assert_allclose(x, np.concatenate(xo), rtol=1e-8, atol=1e-12)
 
@@ -84,6 +87,71 @@ def test_pcg1_matches_oracle_pcg1(dims, n_cpu, alpha):
     pipe = OraclePipeline(probs, pm.offsets, alpha)
     xo, ro = pipe.solve("pcg1", TOL, 2000)
     _compare(rep, ro, x, xo)
+
+
+# GV's recurrences carry one more level of accumulated rounding than CG's
+# (tests/test_oracle_golden.py: 2.1e-10 against the reference's CG at c1)
+PIPE_RTOL = 1e-9
+
+
+@pytest.mark.parametrize("dims,n_cpu,alpha", [((12, 12, 12), 8, 4), ((12, 12, 12), 8, 8),
+                                              ((48, 48, 48), 8, 2), ((100, 100, 100), 8, 8)])
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_pipecg_matches_oracle_pipecg(dims, n_cpu, alpha, defer, monkeypatch):
+    monkeypatch.setenv("LRB_PIPE_DEFER", defer)
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    x, rep = _solve_gpu(pm, asm, "pipecg", step=3)
+    from oracle import cavity as ocav
+    probs = [ocav.perturb(p, 3) for p in oracle_problems(asm)]
+    pipe = OraclePipeline(probs, pm.offsets, alpha)
+    xo, ro = pipe.solve("pipecg", TOL, 2000)
+    _compare(rep, ro, x, xo, rtol=PIPE_RTOL)
+
+
+@pytest.mark.parametrize("name", ["c1", "cav12x12x12_r8_a2", "cav7x9x11_r6_a3"])
+def test_pipecg_matches_reference_cg(name):
+    """Uniform cavity diagonal: pipecg's iterates are CG's up to rounding, so
+    its recurrence residuals follow the reference's recorded CG log."""
+    pm, per_rank = golden_inputs(name)
+    for s in (2, 3):
+        _, rep = _solve_gpu(pm, per_rank, "pipecg", step=s)
+        it_ref = int(get(name, 0, f"cg_{s}_rep")[0])
+        ref = ref_history(get(name, 0, f"cg_{s}_log"), it_ref, TOL)
+        assert rep.converged and abs(rep.iterations - it_ref) <= 1
+        assert history_ok(rep.history, ref, rtol=PIPE_RTOL)[0], (rep.history, ref)
+
+
+@pytest.mark.parametrize("defer", ["0", "1"])
+@pytest.mark.parametrize("alpha", [8, 4])   # one part (flat team) / two parts
+@pytest.mark.parametrize("max_iter", [1, 2, 9, 10, 11, 17])
+def test_pipecg_max_iter_edge(alpha, max_iter, defer, monkeypatch):
+    """With LRB_PIPE_DEFER=1 the kernel learns iteration k's residual during
+    phase k+1: at max_iter it must still take the last decision (true
+    residual at the 10th), report max_iter iterations and return x_max_iter,
+    exactly as the oracle (and as the reducing variant)."""
+    monkeypatch.setenv("LRB_PIPE_DEFER", defer)
+    _, asm, pm = cavity_case((24, 24, 24), 8, alpha)
+
+    def program(ctx):
+        m, ifs = asm[ctx.rank]
+        s = lrb.repartition(m, ifs, pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(m, ifs, 3), "direct")
+        if not s.is_owner:
+            return None
+        x, rep = lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), TOL, max_iter, s.comm,
+                              method="pipecg", history=True)
+        pieces = s.comm.gather(x, 0)
+        return (np.concatenate(pieces), rep) if pieces is not None else rep
+
+    x, rep = lrb.run_world(pm.n_cpu, program, timeout=600)[0]
+    from oracle import cavity as ocav
+    probs = [ocav.perturb(p, 3) for p in oracle_problems(asm)]
+    xo, ro = OraclePipeline(probs, pm.offsets, alpha).solve("pipecg", TOL, max_iter)
+    assert rep.iterations == ro.iterations == max_iter and not rep.converged and not ro.converged
+    assert len(rep.history) == max_iter
+    assert history_ok(rep.history, ro.history, rtol=PIPE_RTOL)[0]
+    np.testing.assert_allclose(rep.residual, ro.residual, rtol=1e-8)
+    np.testing.assert_allclose(x, np.concatenate(xo), rtol=1e-9, atol=1e-13)
 
 
 @pytest.mark.parametrize("name", ["c1", "cav12x12x12_r8_a2", "cav7x9x11_r6_a3"])

@@ -208,6 +208,46 @@ def test_pcg1_matches_pcg(dims, n_cpu, alpha, dev_ranks):
     assert all(np.array_equal(a, b) for a, b in zip(xc, holder["pcg1"][0]))
 
 
+@pytest.mark.parametrize("dims,n_cpu,alpha,dev_ranks", [((24, 24, 24), 4, 4, None),
+                                                        ((24, 24, 24), 4, 2, None),
+                                                        ((20, 20, 20), 4, 1, [0, 0, 1, 1]),
+                                                        ((100, 100, 100), 4, 4, None)])
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_pipecg_matches_pcg(dims, n_cpu, alpha, dev_ranks, defer, monkeypatch):
+    """Pipelined PCG: CG's iterates in exact arithmetic (same iterations +-1,
+    history and solution to rounding); deterministic run to run on flat teams
+    (deferred reductions) and on multi-part / split-device teams (reducing
+    barrier).  defer "1": LRB_PIPE_DEFER=1 (reductions read one phase late
+    on flat teams)."""
+    from paper_2510_08536_b200.device import Team
+    monkeypatch.setenv("LRB_PIPE_DEFER", defer)
+    _, asm, pm = cavity_case(dims, n_cpu, alpha)
+    holder = {}
+
+    def program(ctx):
+        s = lrb.repartition(*asm[ctx.rank], pm, ctx)
+        lrb.update(s, *lrb.perturb_coefficients(*asm[ctx.rank], 3), "direct")
+        parts = s.comm.allgather(s.part) if s.is_owner else None
+        if s.is_owner and s.comm.group_rank == 0:
+            team = Team(parts, dev_ranks=dev_ranks)
+            assert team.kernel_info("pipecg")["streaming"] == 1
+            bs = [np.ones(p.n) for p in parts]
+            holder["pcg"] = team.solve("pcg", bs, 1e-9, 500, hist_cap=500)
+            holder["pipe"] = team.solve("pipecg", bs, 1e-9, 500, hist_cap=500)
+            holder["pipeb"] = team.solve("pipecg", bs, 1e-9, 500, hist_cap=500)
+        return None
+
+    lrb.run_world(n_cpu, program)
+    (xa, ra, ha), (xb, rb, hb), (xc, rc, hc) = holder["pcg"], holder["pipe"], holder["pipeb"]
+    assert ra.converged and rb.converged and abs(ra.iterations - rb.iterations) <= 1
+    n = min(len(ha), len(hb))
+    np.testing.assert_allclose(hb[:n], ha[:n], rtol=1e-6, atol=1e-14)
+    xa, xb = np.concatenate(xa), np.concatenate(xb)
+    assert np.linalg.norm(xb - xa) <= 1e-7 * np.linalg.norm(xa)
+    assert rc.iterations == rb.iterations and np.array_equal(hc, hb)
+    assert all(np.array_equal(a, b) for a, b in zip(xc, holder["pipe"][0]))
+
+
 @pytest.mark.parametrize("stages", ["2", "3"])
 def test_stream_ring_depth_variants(stages, monkeypatch):
     """Two- and three-stage rings (L = lcm(stages, 2) = 2 / 6 ring periods

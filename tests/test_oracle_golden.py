@@ -119,20 +119,27 @@ def test_oracle_pcg_matches_reference_cg_on_cavity():
 
 
 @pytest.mark.parametrize("name", ["c1", "cav12x12x12_r8_a2", "cav7x9x11_r6_a3"])
-def test_oracle_pcg1_matches_reference_cg_on_cavity(name):
-    """The single-reduction restatement (krylov.pcg1) is pinned to
-    the reference's CG: on the uniform-diagonal cavity its recurrence residuals
-    follow the reference's CG history within 1e-10, iterations +-1."""
+@pytest.mark.parametrize("method", ["pcg1", "pipecg"])
+def test_oracle_pcg1_matches_reference_cg_on_cavity(name, method):
+    """The single-reduction and pipelined restatements (krylov.pcg1 /
+    krylov.pipecg) are pinned to the reference's CG: on the
+    uniform-diagonal cavity their recurrence residuals follow the reference's
+    CG history within 1e-10 (pcg1) / 1e-9 (pipecg), iterations +-1.  The
+    pipelined recurrences (w -= alpha z on top of z = n + beta z) carry one
+    more level of accumulated rounding: measured 2.1e-10 at the last
+    iterations of c1, where the residual is ~1e-6 of |b| (parity
+    by tolerance)."""
     probs, offsets, alpha = problems_of(name)
     pipe = OraclePipeline(probs, offsets, alpha)
     for s in (2, 3):
         pipe.update([cavity.perturb(p, s) for p in probs])
-        _, rep = pipe.solve("pcg1", 1e-6, 2000)
+        _, rep = pipe.solve(method, 1e-6, 2000)
         it = int(get(name, 0, f"cg_{s}_rep")[0])
         assert abs(rep.iterations - it) <= 1 and rep.converged
         ref_hist = _recurrence_history(get(name, 0, f"cg_{s}_log"), it)
         n = min(len(ref_hist), len(rep.history))
-        np.testing.assert_allclose(rep.history[:n], ref_hist[:n], rtol=1e-10)
+        rtol = 1e-10 if method == "pcg1" else 1e-9
+        np.testing.assert_allclose(rep.history[:n], ref_hist[:n], rtol=rtol)
 
 
 def _recurrence_history(log, iterations, tol=1e-6):
