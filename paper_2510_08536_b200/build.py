@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libldurepart_b200.so")
 # separately compiled translation units (built in parallel, then linked)
-SOURCES = ["plan.cpp", "device.cu", "scatter.cu", "solve_cg.cu", "solve_bicgstab.cu", "solve_pcg1.cu", "solve_pipecg.cu"]
+SOURCES = ["plan.cpp", "device.cu", "scatter.cu", "solve_cg.cu", "solve_bicgstab.cu", "solve_pcg1.cu", "solve_pipecg.cu", "solve_pipecg_t.cu"]
 HEADERS = ["lrb_internal.h", "kernels.cuh", "stream.cuh", "launch.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

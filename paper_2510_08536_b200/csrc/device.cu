@@ -815,15 +815,19 @@ constexpr int64_t kStaticSmemMargin = 4096;
 
 // Largest shared-memory need of any SpMV phase of a method for a staged tile
 // with `base` bytes of record + values and `wb` bytes per window vector.
-static int64_t method_need(int method, int64_t base, int64_t wb) {
+// PIPECG stages its five own-row vectors only on teams whose devices have at
+// most one tile per CTA and phase (latency-bound; stream.cuh TAILS)
+static bool pipe_staged_tails(int64_t n_tiles) { return n_tiles <= kLanes; }
+
+static int64_t method_need(int method, int64_t base, int64_t wb, bool staged_tails) {
   const int64_t tv = kVecTileBytes;
   switch (method) {
     case LRB_METHOD_BICGSTAB:   // phase 1: r, u = p_old - omega v_old windows + rhat tile
       return base + std::max({2 * wb + tv, 2 * wb, wb + tv});
     case LRB_METHOD_PCG1:       // fused phase: r, dinv, w, s_old windows + p, x tiles
       return base + std::max({4 * wb + 2 * tv, 2 * wb, wb + tv});
-    case LRB_METHOD_PIPECG:     // pipelined phase: w, dinv windows + z, s, p, x, r tiles
-      return base + std::max({2 * wb + 5 * tv, 2 * wb, wb + tv});
+    case LRB_METHOD_PIPECG:     // pipelined phase: w, dinv windows (+ z, s, p, x, r tiles)
+      return base + std::max({2 * wb + (staged_tails ? 5 : 0) * tv, 2 * wb, wb + tv});
     default:                    // CG / PCG: z, p_old windows (+ x tile); check: x (+ p) windows + b tile
       return base + (LRB_LAZY_X ? 2 * wb + tv : std::max(2 * wb, wb + tv));
   }
@@ -1103,7 +1107,8 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
         for (int64_t lt = 0; lt < P->d.ntiles; ++lt) {
           const int64_t need = tile_geometry(P, lt, p, 0, h);
           if (need <= 0 || need > stage_bytes) continue;   // not staged (direct loads)
-          best = std::max(best, method_need(m, kRecBytes + h.vbytes, int64_t(h.wtot) * 8));
+          best = std::max(best, method_need(m, kRecBytes + h.vbytes, int64_t(h.wtot) * 8,
+                                            pipe_staged_tails(D.n_tiles)));
         }
       }
       best = (best + 127) & ~int64_t(127);
@@ -1117,7 +1122,10 @@ static int setup_device(TeamDevice& D, std::vector<PartDev>& table, lrb_part* co
     m_stages[LRB_METHOD_CG] = m_stages[LRB_METHOD_PCG] = n_stages;
   }
   for (int m = 0; m < kMethods; ++m) {
-    const void* sfn = (use_stream && m_stages[m]) ? stream_kernel(m, D.inl) : nullptr;
+    const void* sfn = (use_stream && m_stages[m])
+                          ? (m == LRB_METHOD_PIPECG && pipe_staged_tails(D.n_tiles) ? pipecg_t_stream_kernel(D.inl)
+                                                                                   : stream_kernel(m, D.inl))
+                          : nullptr;
     if (sfn) {
       D.fn[m] = sfn;
       D.block[m] = kStreamThreads;

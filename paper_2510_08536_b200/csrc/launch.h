@@ -1,5 +1,5 @@
 // Kernel entry points of the separately compiled CUDA translation units
-// (scatter.cu, solve_cg.cu, solve_bicgstab.cu, solve_pcg1.cu, solve_pipecg.cu), for the host
+// (scatter.cu, solve_cg.cu, solve_bicgstab.cu, solve_pcg1.cu, solve_pipecg*.cu), for the host
 // side in device.cu.  Internal; not part of the public interface.
 #pragma once
 
@@ -24,6 +24,7 @@ const void* cg_stream_kernel(bool jac, bool inl);        // solve_cg.cu
 const void* bicgstab_classic_kernel(bool inl);           // solve_bicgstab.cu
 const void* bicgstab_stream_kernel(bool inl);            // solve_bicgstab.cu
 const void* pcg1_stream_kernel(bool inl);                // solve_pcg1.cu
-const void* pipecg_stream_kernel(bool inl);              // solve_pipecg.cu
+const void* pipecg_stream_kernel(bool inl);              // solve_pipecg.cu (own-row vectors loaded)
+const void* pipecg_t_stream_kernel(bool inl);            // solve_pipecg_t.cu (own-row vectors staged)
 
 }  // namespace lrb

@@ -231,6 +231,8 @@ struct Spec {
   int ntv;                 // tile vectors
   const double* wv[4];
   const double* tv[6];
+  int npv;                 // SpMV phases: tile vectors the consumers load themselves,
+  const double* pv[6];     //   pulled toward L2 when the tile's copies are issued
 };
 
 
@@ -439,6 +441,9 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
 #pragma unroll
       for (int v = 0; v < 6; ++v)
         if (v < sp.ntv) bulk_g2s(d + size_t(v) * kVecTileBytes, sp.tv[v] + cur.row0, vec_bytes, full, pol_vec);
+#pragma unroll
+      for (int v = 0; v < 6; ++v)
+        if (v < sp.npv) bulk_prefetch_l2(sp.pv[v] + cur.row0, vec_bytes);
     }
     if (kProf && T.prof_cta && pw == 0) S.cnt[kind * kCntPer + 7] += clock64() - ci;
     if (tl) S.cnt[4 * kCntPer + 3] = (unsigned long long)global_ns();
@@ -459,6 +464,9 @@ __device__ __forceinline__ void produce_spmv(const TeamDev& T, const StreamSmem&
 #pragma unroll
         for (int w = 0; w < kMaxWin; ++w)
           if (v < spn.nwv && w < nxt.nw) bulk_prefetch_l2(spn.wv[v] + nxt.wa[w], unsigned(nxt.wl[w] * 8));
+#pragma unroll
+      for (int v = 0; v < 6; ++v)
+        if (v < spn.npv) bulk_prefetch_l2(spn.pv[v] + nxt.row0, unsigned((nxt.rows * 8 + 15) & ~15));
     }
     cur = nxt;
   }
@@ -1772,7 +1780,7 @@ __device__ __forceinline__ void stream_phase_pipe(const TeamDev& T, const Stream
   gseq += stage_count(T.n_tiles);
 }
 
-template <bool INL, bool DEFER>
+template <bool INL, bool DEFER, bool TAILS>
 __global__ void LRB_STREAM_BOUNDS
     team_pipecg_stream_kernel(const __grid_constant__ TeamDev T) {
   const PartDev* __restrict__ parts = T.parts;
@@ -1875,7 +1883,8 @@ __global__ void LRB_STREAM_BOUNDS
       stream_phase_pipe<3, INL>(
           T, S, gseq, red, 1, din, flat, want,
           [&](const PartDev& P) {
-            return Spec{2, 5, {wbuf(P, ob), P.dinv}, {P.t, P.s, P.p0, xbuf(P, ob), P.r}};
+            if (TAILS) return Spec{2, 5, {wbuf(P, ob), P.dinv}, {P.t, P.s, P.p0, xbuf(P, ob), P.r}};
+            return Spec{2, 0, {wbuf(P, ob), P.dinv}, {}, 5, {P.t, P.s, P.p0, xbuf(P, ob), P.r}};
           },
           [&](double* pab) {   // reducer warp, lane 0: this phase's alpha, beta, breakdown
             double a, b;
@@ -1903,11 +1912,20 @@ __global__ void LRB_STREAM_BOUNDS
               const int qd = diag_pos(H, slot, sl, H.row0 + lr);
               w_i = ww[qd];
               d_i = dw[qd];
-              z_o = t.tail(0)[lr];
-              s_o = t.tail(1)[lr];
-              p_o = t.tail(2)[lr];
-              x_o = t.tail(3)[lr];
-              r_i = t.tail(4)[lr];
+              if (TAILS) {
+                z_o = t.tail(0)[lr];
+                s_o = t.tail(1)[lr];
+                p_o = t.tail(2)[lr];
+                x_o = t.tail(3)[lr];
+                r_i = t.tail(4)[lr];
+              } else {   // own-row vectors straight from global memory (smaller stages, deeper ring)
+                const int64_t i = H.row0 + lr;
+                z_o = __ldcs(P.t + i);
+                s_o = __ldcs(P.s + i);
+                p_o = __ldcs(P.p0 + i);
+                x_o = __ldcs(xbuf(P, ob) + i);
+                r_i = __ldcs(P.r + i);
+              }
             } else {
               if (lr >= H.rows || bad) return;
               const int64_t i = H.row0 + lr;
