@@ -660,7 +660,9 @@ def finish_line(args, rec, method, desc, N, n_cpu, alpha, sampler):
         "gpu_launches": int(rec["launches"]),
         "clocks": sampler.summary(),
     }
-    t = traffic_ratio(args.workload)
+    # the capture of this workload's solve kernel: "<workload>_<method>", or
+    # "<workload>" for two-phase PCG
+    t = traffic_ratio(f"{args.workload}_{method}") or (traffic_ratio(args.workload) if method == "pcg" else None)
     if t:
         # ncu DRAM bytes per algorithmic byte of the solve kernel, applied to this
         # run's launches (same kernel, same config)

@@ -195,3 +195,36 @@ def test_bicgstab_solution_against_direct_solve(dims, n_cpu, alpha):
     xd = spla.spsolve(A, b)
     assert np.linalg.norm(x - xd) <= 1e-9 * np.linalg.norm(xd)
     assert np.linalg.norm(A @ x - b) <= 1e-11 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("defer", ["0", "1"])
+def test_pipecg_repeated_solves(defer, monkeypatch):
+    """Regression (deferred variant): the reducer of phase k+1 published its
+    scalars into the buffer that slow warps of the post-phase code of phase k
+    were still reading, which split a CTA's control flow and deadlocked the
+    second 68-iteration solve at 100^3 (tools/pipe_repro.py).  Repeated
+    solves over timesteps must stay deterministic and equal the oracle's
+    iteration counts within one."""
+    monkeypatch.setenv("LRB_PIPE_DEFER", defer)
+    monkeypatch.setenv("LRB_BARRIER_TIMEOUT_S", "20")
+    _, asm, pm = cavity_case((100, 100, 100), 8, 8)
+    steps = [2, 2, 3, 2, 3]
+
+    def program(ctx):
+        m, ifs = asm[ctx.rank]
+        s = lrb.repartition(m, ifs, pm, ctx)
+        out = []
+        for st in steps:
+            lrb.update(s, *lrb.perturb_coefficients(m, ifs, st), "direct")
+            if s.is_owner:
+                x, rep = lrb.cg_solve(s.matrix, s.halo, np.ones(s.matrix.n_owned), TOL, 2000, s.comm,
+                                      method="pipecg", history=True)
+                out.append((rep.iterations, rep.converged, tuple(rep.history), x.copy()))
+        return out
+
+    res = lrb.run_world(pm.n_cpu, program, timeout=600)[0]
+    it2, it3 = res[0][0], res[2][0]
+    for (it, conv, hist, x), st in zip(res, steps):
+        assert conv and it == (it2 if st == 2 else it3)
+    for a, b in ((0, 1), (0, 3), (2, 4)):   # same timestep, bit-identical
+        assert res[a][2] == res[b][2] and np.array_equal(res[a][3], res[b][3])
