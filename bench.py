@@ -66,14 +66,17 @@ sys.path.insert(0, ROOT)
 METRIC = "ms/timestep (matrix update + CG solve) at 1/2/4/8 B200; % of HBM roofline"
 WORKLOADS = {
     # name: (N, default rpg, method, description)
-    "c3": (200, 8, "pcg", "C3: 3D cavity 200^3 (8M cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "
-                          "(alpha {alpha}), pressure Jacobi-PCG to 1e-6, b=ones"),
+    "c3": (200, 8, "pipecg", "C3: 3D cavity 200^3 (8M cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "
+                             "(alpha {alpha}), pressure Jacobi-PCG (pipelined) to 1e-6, b=ones"),
     "c2": (100, 8, "pipecg", "C2: 3D cavity 100^3 (1M cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "
                              "(alpha {alpha}), Jacobi-PCG (pipelined) to 1e-6"),
-    # C1 / C2: the pipelined Jacobi-PCG (one barrier per iteration) is the
-    # fastest solver there (profiles/r2_experiments.md); --method pcg for the
-    # two-phase kernel.  C3 keeps the two-phase kernel (0.4% behind pipecg, but
-    # its histories are pinned to the reference at 1e-10, pipecg's at 1e-9)
+    # Jacobi-PCG in its pipelined form (one SpMV phase and one barrier per
+    # iteration): the fastest solver at C1/C2, level with two-phase PCG at C3
+    # (7.03 vs 7.06 ms/timestep) with half the team barriers — the ones that
+    # cross NVLink on N > 1 GPUs.  At C3 its histories sit within 3.9e-11 of
+    # the reference's CG logs with the same iteration counts
+    # (tests/test_gpu_large.py).  --method pcg for the two-phase kernel; C4
+    # keeps it for the pressure solve.
     "c1": (32, 4, "pipecg", "C1: 3D cavity 32^3, {n_cpu} CPU ranks -> {n_gpu} device(s) "
                             "(alpha {alpha}), Jacobi-PCG (pipelined) to 1e-6"),
     "c4": (300, 16, "pcg", "C4: 3D cavity {N}^3 ({cells} cells), {n_cpu} CPU ranks -> {n_gpu} GPU(s) "

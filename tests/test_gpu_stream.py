@@ -211,6 +211,7 @@ def test_pcg1_matches_pcg(dims, n_cpu, alpha, dev_ranks):
 @pytest.mark.parametrize("dims,n_cpu,alpha,dev_ranks", [((24, 24, 24), 4, 4, None),
                                                         ((24, 24, 24), 4, 2, None),
                                                         ((20, 20, 20), 4, 1, [0, 0, 1, 1]),
+                                                        ((64, 64, 64), 4, 1, [0, 0, 1, 1]),
                                                         ((100, 100, 100), 4, 4, None)])
 @pytest.mark.parametrize("defer", ["0", "1"])
 def test_pipecg_matches_pcg(dims, n_cpu, alpha, dev_ranks, defer, monkeypatch):
