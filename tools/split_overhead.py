@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--n", type=int, default=200)
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--repeat", type=int, default=3)
+    ap.add_argument("--method", default="pcg")
     args = ap.parse_args()
     import paper_2510_08536_b200 as lrb
     from paper_2510_08536_b200.device import Team
@@ -60,7 +61,7 @@ def main():
         team.profile(4 * MAX_ITER)
         ms, its = [], None
         for _ in range(args.repeat):
-            xs, rep, hist = team.solve("pcg", bs, TOL, MAX_ITER, hist_cap=MAX_ITER)
+            xs, rep, hist = team.solve(args.method, bs, TOL, MAX_ITER, hist_cap=MAX_ITER)
             ms.append(rep.device_ms)
             its = rep.iterations
         ts = team.phase_times_ns().reshape(-1, 2)
@@ -68,8 +69,8 @@ def main():
         if ref_x is None:
             ref_x = xs
         same = all(np.array_equal(a, b) for a, b in zip(xs, ref_x))
-        print(json.dumps({"device_ranks": split, "kernels": split,
-                          "ctas_per_kernel": team.kernel_info("pcg")["grid"],
+        print(json.dumps({"method": args.method, "device_ranks": split, "kernels": split,
+                          "ctas_per_kernel": team.kernel_info(args.method)["grid"],
                           "iterations": its, "solve_ms": round(float(np.median(ms)), 4),
                           "us_per_iteration": round(float(np.median(ms)) * 1e3 / its, 2),
                           "barrier_last_arrival_to_release_us": round(float(np.median(sync_us)), 2),
